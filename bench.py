@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""LSRN hot-path benchmark (driver contract).
+
+One step = one full LSRN solve of the configured workload on device-resident
+inputs: Gaussian sketch (K1+K2, DMMA) -> [NCCL allreduce] -> SVD (cuSOLVER,
+outside the hot path, reported separately) -> N -> fused LSQR (or CS)
+iterations (K5/K6/K8, one CUDA graph) -> x.
+
+Default workload (N = 1): BASELINE.json configs[1] = c2, dense 1e5 x 2000 rank
+1800, gamma = 2 (s = 4000), LSQR predictable count.  A (1.6 GB) is larger than
+L2 (126 MB), so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--solver lsqr|cs]
+  python bench.py --impl reference ...     # the CPU oracle arm (rank 0 only)
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lsrn_solve_s"
+UNIT = "s"
+FP64_PEAK_TFLOPS = 36.9     # DMMA.8x8x4 burst peak measured on this pool (profiles/fp64_peak.jsonl)
+FP64_PEAK_NOTE = ("fp64 DMMA peak measured by tools/microbench/fp64_peak.cu on this pool's B200 "
+                  "(MEASURED_PEAKS.json has no fp64 entry); cuBLAS DGEMM 8192^3 measured 35.4")
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg_name, solver, m_sample):
+    """The oracle (as it stands) on a bounded sample of the workload, extrapolated.
+
+    Sample: the same recipe with m' = m_sample rows (same n, s, r/s); the oracle's
+    sketch and iteration stages scale linearly in m, the s x k SVD does not, so
+    T(full) = (t_sketch + t_iter) * m / m' + t_svd.
+    """
+    import numpy as np  # noqa: F401
+    from oracle.lsrn import solve as orc_solve
+    from synth.generate import CONFIGS, make_problem
+    cfg = CONFIGS[cfg_name]
+    p = make_problem(cfg_name, m=m_sample, n=cfg["n"]) if cfg["m"] >= cfg["n"] else \
+        make_problem(cfg_name, m=cfg["m"], n=m_sample)
+    A = p.dense_A().numpy()
+    t0 = time.perf_counter()
+    rep = orc_solve(A, p.b.numpy(), gamma=cfg["gamma"], lam=cfg["lam"], solver=solver, precise_g=False)
+    wall = time.perf_counter() - t0
+    L_full = max(cfg["m"], cfg["n"])
+    scale = L_full / m_sample
+    est = (rep["t_sketch"] + rep["t_iter"]) * scale + rep["t_svd"]
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": est, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"oracle solve ({solver}) of the {cfg_name} recipe at {m_sample} long-index rows "
+                       f"(1/{scale:.0f} of L={L_full}); stages sketch {rep['t_sketch']:.2f}s svd "
+                       f"{rep['t_svd']:.2f}s iter {rep['t_iter']:.2f}s; value = (sketch+iter)*{scale:.0f}+svd"),
+            "sample_wall_s": wall}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle arm (rank 0 only, N > 1 ranks exit 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    m_sample = args.ref_rows
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; keep the contract's W for symmetry
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(args.config, args.solver, m_sample)
+        vals.append(last["value"])
+    v = statistics.median(vals)
+    cb = dict(last)
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "solver": args.solver, "sample_rows": m_sample},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--solver", default="lsqr", choices=["lsqr", "cs"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=4000)
+    ap.add_argument("--cpu-rows", type=int, default=10000)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1109_5981_b200 import lsrn
+    from synth.generate import CONFIGS, SKETCH_SEED, make_problem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    m, n = cfg["m"], cfg["n"]
+    L = max(m, n)
+    lo = (L * rank) // world
+    hi = (L * (rank + 1)) // world
+    p = make_problem(args.config, device=dev, shard=(lo, hi) if world > 1 else None)
+    X, b = p.X, p.b
+    nid = None
+    if world > 1:
+        obj = [lsrn.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    ctx = lsrn.Context(stream=stream, nranks=world, rank=rank, nccl_id=nid)
+    ctx.set_profiling(True)
+    kw = dict(solver=args.solver, gamma=cfg["gamma"], lam=cfg["lam"], tol=1e-14, seed=SKETCH_SEED, lo=lo,
+              cnt=hi - lo)
+    with torch.cuda.stream(stream):
+        x, rep = ctx.solve(X, b, m, n, **kw)
+        for _ in range(max(0, args.warmup - 1)):
+            x, rep = ctx.solve(X, b, m, n, **kw)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    reps, stats = [], []
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            x, rep = ctx.solve(X, b, m, n, **kw)
+            reps.append(rep)
+            stats.append(ctx.stats())
+        e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # ---- per-stage and per-kernel numbers (medians over the timed steps)
+    def med(key, src):
+        return statistics.median(float(r[key]) for r in src)
+
+    t_sketch = med("t_sketch", reps)
+    t_svd = med("t_svd", reps)
+    t_iter = med("t_iter", reps)
+    t_ar = med("t_allreduce", reps)
+    sk_ms = med("sketch_ms", stats)
+    lp_ms = med("long_pass_ms", stats)
+    launches = int(statistics.median(s["launches"] for s in stats))
+    s_ = reps[-1]["s"]
+    k = min(m, n)
+    cnt = hi - lo
+    sketch_flops = 2.0 * s_ * k * cnt
+    peaks, peak_src = load_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    lp_bytes = cnt * k * 8.0 + 3 * 8.0 * cnt     # A once + z read/write + (b-side) stream
+    sketch_tf = sketch_flops / (sk_ms * 1e-3) / 1e12
+    lp_gbs = lp_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None
+    iters = reps[-1]["iters"]
+    # dominant kernel by share of the step
+    sketch_share = (sk_ms / 1e3) / (ms / 1e3)
+    lp_share = (lp_ms / 1e3) * max(iters + 1, 1) / (ms / 1e3)
+    roof_sketch = {"kernel": "sketch_dense_kernel (K1+K2, DMMA)", "bound": "tensor", "achieved": sketch_tf,
+                   "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": sketch_tf / FP64_PEAK_TFLOPS,
+                   "traffic": None, "algorithmic": f"2*s*k*L = {sketch_flops:.4g} flop per launch",
+                   "peak_source": FP64_PEAK_NOTE, "share_of_step": sketch_share}
+    roof_lp = {"kernel": "rowpass_kernel long pass (K6)", "bound": "hbm", "achieved": lp_gbs, "peak": hbm_peak,
+               "unit": "GB/s", "frac": (lp_gbs / hbm_peak) if lp_gbs else None, "traffic": None,
+               "algorithmic": f"8*(L*k + 3L) = {lp_bytes:.4g} B per launch",
+               "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", "share_of_step": lp_share}
+    roofline = roof_sketch if sketch_share >= lp_share else roof_lp
+
+    # ---- end to end through the C ABI with HOST buffers (H2D of A, b and D2H of x inside)
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        bh = b.cpu().pin_memory()
+        nsteps = min(3, args.steps)
+        barrier()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            ctx.solve(Xh, bh, m, n, host_io=True, **kw)
+            barrier()
+            h0.record(stream)
+            for _ in range(nsteps):
+                xh, _r = ctx.solve(Xh, bh, m, n, host_io=True, **kw)
+            h1.record(stream)
+        barrier()
+        ems = h0.elapsed_time(h1) / nsteps
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(te.item()) / 1e3, "unit": UNIT,
+               "h2d_bytes_per_step": int(Xh.numel() * 8 + bh.numel() * 8),
+               "d2h_bytes_per_step": int(xh.numel() * 8),
+               "steps": nsteps}
+        del Xh, bh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.config, args.solver, args.cpu_rows)
+        except Exception as ex:  # report, do not fail the bench
+            cpu = {"error": repr(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms / 1e3, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "shape": [m, n], "s": s_, "r": reps[-1]["r"],
+                       "solver": args.solver, "iters": iters, "gamma": cfg["gamma"], "lambda": cfg["lam"],
+                       "tol": 1e-14, "parallelism": f"row-shard x{world}" if m >= n else f"col-shard x{world}",
+                       "l2": "inputs larger than L2 (A = %.2f GB), no flush" % (cnt * k * 8 / 1e9)},
+            "stages_s": {"sketch": t_sketch, "allreduce": t_ar, "svd": t_svd, "iterations": t_iter,
+                         "hot_path_excl_svd": t_sketch + t_ar + t_iter},
+            "sketch_tflops": sketch_tf, "matvec_gbs": lp_gbs,
+            "roofline": roofline, "roofline_kernels": {"sketch": roof_sketch, "long_pass": roof_lp},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * lsrn.h -- C ABI of the B200 (sm_100a) LSRN hot path.
+ *
+ * LSRN: Meng, Saunders & Mahoney, "LSRN: a parallel iterative solver for
+ * strongly over- or under-determined systems", arXiv 1109.5981.  Citations
+ * "P:n" are lines of the paper text; "§8(c) Cn" are
+ * the readings recorded in DESIGN.md ("Readings of the paper").
+ *
+ * Problem (§1): x* = argmin ||Ax - b||_2 of minimum length,
+ * A m x n strongly over- (m >> n, Alg. 1) or under-determined
+ * (m << n, Alg. 2), possibly rank deficient, optionally with
+ * Tikhonov regularisation W = lambda I (§5):
+ *     x_lambda = argmin 1/2 ||Ax - b||^2 + 1/2 lambda^2 ||x||^2.
+ *
+ * Conventions shared by every entry point
+ *   - All array arguments are DEVICE pointers (CUDA global memory of the
+ *     context's device), owned by the caller, unless opts->flags has
+ *     LSRN_HOST_IO (then A, b and x are host pointers; pinned host memory is
+ *     recommended; the library stages them through the workspace).
+ *   - fp64 everywhere (P:991-992 tolerance 1e-14 implies double; §8(c) C8).
+ *   - Layout of dense A ("long-index-major"): the long index is the major one.
+ *       m >= n (tall): A row-major,   element (i, j) at val[(i - lo) * ld + j];
+ *       m <  n (wide): A column-major, element (i, j) at val[(j - lo) * ld + i].
+ *     i.e. the library always sees X = A (tall) or X = A^T (wide) as a
+ *     row-major L x k matrix, L = max(m, n), k = min(m, n).  ld >= k, and the
+ *     fast (16-byte vector) paths need ld even and val 16-byte aligned.
+ *   - CSR A (kind LSRN_CSR, tall only): rows [lo, lo+cnt) of A; rowptr has
+ *     cnt+1 entries (rowptr[0] may be non-zero), colind int32 in [0, n), val.
+ *   - Multi-GPU: every rank calls with the SAME opts/seed; A is sharded along
+ *     the long index (rows of a tall A, columns of a wide A): rank p holds
+ *     [lo, lo + cnt).  b is the rank's shard of b (tall) or the full b (wide).
+ *     x is the full x (tall, replicated on every rank) or the rank's shard of x
+ *     (wide).  The sketch partials are combined with one NCCL allreduce
+ *     (MPI_Reduce in the paper) and every iteration does one
+ *     allreduce of k+1 doubles.
+ *   - Every call is asynchronous on the context stream except for one
+ *     device->host read of the singular values after the SVD (to get r).
+ *   - Outputs are written only when the call returns LSRN_OK.  A and b are
+ *     never modified.  No C++ exception crosses the ABI; on error a
+ *     thread-local message is available from lsrn_last_error().
+ *   - The library performs no device allocation: every buffer lives in the
+ *     caller's workspace (size from lsrn_workspace_size).
+ */
+#ifndef LSRN_H
+#define LSRN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LSRN_OK = 0,
+  LSRN_EINVAL = -1,      /* gamma <= 1, lambda < 0, tol not in (0,1), alpha not in
+                            (0, 1 - sqrt(r/s)), unknown kind/solver/mode, NULL pointer */
+  LSRN_EDIM = -2,        /* inconsistent dims / shard / leading dimension */
+  LSRN_ENONFINITE = -3,  /* non-finite value met (reserved) */
+  LSRN_ERANK0 = -4,      /* "sketch has numerical rank 0" */
+  LSRN_ESVD = -5,        /* cuSOLVER failed */
+  LSRN_ENOMEM = -6,      /* workspace smaller than lsrn_workspace_size() */
+  LSRN_ECUDA = -7,       /* CUDA runtime / launch error */
+  LSRN_ENCCL = -8,       /* NCCL error or NCCL unavailable for nranks > 1 */
+  LSRN_EUNSUPPORTED = -9 /* valid request this build does not implement (message says which) */
+} lsrn_status;
+
+enum { LSRN_DENSE = 0, LSRN_CSR = 1 };
+enum { LSRN_MODE_PREDICTABLE = 0, LSRN_MODE_ADAPTIVE = 1 };
+enum { LSRN_HOST_IO = 1 };
+
+typedef struct lsrn_ctx lsrn_ctx;
+
+typedef struct {
+  int32_t kind;          /* LSRN_DENSE or LSRN_CSR */
+  int32_t pad_;
+  int64_t m, n;          /* GLOBAL dims of A */
+  int64_t lo, cnt;       /* this rank's shard of the long index: [lo, lo + cnt) */
+  const double* val;     /* dense: shard base (cnt rows of X, leading dim ld); CSR: values */
+  int64_t ld;            /* dense leading dimension (>= k) */
+  const int64_t* rowptr; /* CSR: cnt + 1 entries */
+  const int32_t* colind; /* CSR: column indices (global, in [0, n)) */
+  int64_t nnz;           /* CSR: rowptr[cnt] - rowptr[0] */
+} lsrn_matrix;
+
+typedef struct {
+  double gamma;          /* oversampling factor > 1; s = ceil(gamma * min(m, n)) */
+  double lambda;         /* Tikhonov lambda >= 0 (W = lambda I, §5); 0 = plain LS */
+  double tol;            /* epsilon in (0, 1); paper default 1e-14 */
+  double alpha;          /* Thm 4.4 alpha; < 0 selects the default 1/sqrt(s) (§8(c) C3) */
+  uint64_t seed;         /* Philox key of G (§8(c) C9) */
+  int32_t mode;          /* LSQR: LSRN_MODE_PREDICTABLE (Thm 4.5 count at alpha = 0, §8(c) C5)
+                            or LSRN_MODE_ADAPTIVE (Paige-Saunders tests, capped) */
+  int32_t max_iter;      /* adaptive cap; 0 = 2 x the Thm 4.5 count */
+  int32_t flags;         /* LSRN_HOST_IO */
+  int32_t pad_;
+} lsrn_opts;
+
+typedef struct {
+  int64_t s, r;          /* sketch size and detected rank of the sketch (§8(c) C4) */
+  int32_t iters;         /* LSQR iterations / CS loop passes performed */
+  int32_t converged;     /* adaptive LSQR: 1 if a stopping test fired; otherwise 1 */
+  double sigma_L, sigma_U, alpha;   /* Thm 4.4 bounds used */
+  double t_sketch, t_allreduce, t_svd, t_iter, t_total;  /* seconds (CUDA events) */
+  double rnorm_est;      /* LSQR phibar estimate of ||Abar y - bbar|| (0 for CS) */
+} lsrn_report;
+
+/* Human-readable message of the last failing call on this thread ("" if none). */
+const char* lsrn_last_error(void);
+
+/* Library version string, build flags. */
+const char* lsrn_version(void);
+
+/* NCCL unique id (128 bytes) for lsrn_ctx_create on rank 0; LSRN_ENCCL if this
+ * build has no NCCL. */
+lsrn_status lsrn_nccl_unique_id(void* id_out /* 128 bytes */);
+
+/* Create a context on the current CUDA device.
+ *   stream : cudaStream_t (NULL = the legacy default stream) every call runs on;
+ *   nranks, rank : process group (1, 0 for single GPU); nccl_id from rank 0's
+ *   lsrn_nccl_unique_id, identical on all ranks (ignored when nranks == 1).
+ * Creates the cuSOLVER handle and, for nranks > 1, the NCCL communicator. */
+lsrn_status lsrn_ctx_create(lsrn_ctx** ctx, void* stream, int nranks, int rank,
+                            const void* nccl_id);
+lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
+
+/* Testing aid: split this rank's shard into `p` contiguous sub-shards that are
+ * processed as if they were separate ranks (per-shard partial sums combined in
+ * shard order where a real run would call NCCL).  p = 1 restores normal runs. */
+lsrn_status lsrn_ctx_set_virtual_shards(lsrn_ctx* ctx, int p);
+
+/* Record CUDA events around every long-pass (K6) launch of the next solves so
+ * lsrn_last_stats reports its average duration (adds event nodes to the graph). */
+lsrn_status lsrn_ctx_set_profiling(lsrn_ctx* ctx, int on);
+
+/* Bytes of device workspace needed by lsrn_sketch / lsrn_solve_* for this
+ * matrix shard and options (includes host-IO staging when LSRN_HOST_IO). */
+lsrn_status lsrn_workspace_size(lsrn_ctx* ctx, const lsrn_matrix* A, const lsrn_opts* opts,
+                                size_t* bytes);
+
+/* Alg. 1/2 step 3 + §5 blocks, in the tall form:
+ *   At = sigma_X * G[:, 0:L] X + sigma_I * G[:, L:L+k]              (s x k, row-major)
+ * with (sigma_X, sigma_I) = (1, lambda) if m >= n, (1/lambda, 1) if m < n and
+ * lambda > 0, (1, 0) if lambda == 0; G[i, j] = Box-Muller(Philox4x32-10(seed;
+ * i >> 1, j, 0)) generated in registers, never stored (§8(c) C9).  For m < n
+ * the paper's Ã = A G (m x s) is At^T.  With nranks > 1 the result is the
+ * allreduced (global) sketch on every rank.  s_out receives s = ceil(gamma k).
+ * At must hold s * k doubles (device). */
+lsrn_status lsrn_sketch(lsrn_ctx* ctx, const lsrn_matrix* A, double gamma, double lambda,
+                        uint64_t seed, void* ws, size_t ws_bytes, double* At, int64_t* s_out);
+
+/* Full LSRN solve (Alg. 1 or 2, §5 when lambda > 0) with LSQR (Paige &
+ * Saunders 1982, cited P:107-109) on the preconditioned system.  Sketch ->
+ * SVD (cuSOLVER, outside the hot path, timed in t_svd) -> N = V_r Sigma_r^-1 ->
+ * fused single-pass iterations captured in one CUDA graph -> x.
+ *   b : length cnt (tall, rank's rows) or m (wide, replicated);
+ *   x : length n (tall, replicated) or cnt (wide, rank's columns).
+ * b = 0 gives x = 0 and iters = 0. */
+lsrn_status lsrn_solve_lsqr(lsrn_ctx* ctx, const lsrn_matrix* A, const double* b,
+                            const lsrn_opts* opts, void* ws, size_t ws_bytes, double* x,
+                            lsrn_report* report);
+
+/* Same with the Chebyshev semi-iterative method, Alg. 3 with the
+ * k = 1 step 1/(d - c^2/(2d)) (§8(c) C1) and K + 1 passes (§8(c) C2) from the
+ * Thm 4.4 bounds. */
+lsrn_status lsrn_solve_cs(lsrn_ctx* ctx, const lsrn_matrix* A, const double* b,
+                          const lsrn_opts* opts, void* ws, size_t ws_bytes, double* x,
+                          lsrn_report* report);
+
+/* Testing aid (K1 parity): out[t] = G[rows[t], cols[t]] for t < count
+ * (rows/cols/out device arrays), the in-kernel Philox + Box-Muller. */
+lsrn_status lsrn_debug_gaussian(lsrn_ctx* ctx, uint64_t seed, const int64_t* rows,
+                                const int64_t* cols, int64_t count, double* out);
+
+/* Kernel statistics of the last lsrn_sketch / lsrn_solve_* call on ctx:
+ * CUDA-event durations (ms) of the dominant kernels, averaged per launch, and
+ * the number of kernel launches.  Fills up to `cap` doubles:
+ *  [0] sketch stage ms, [1] long-pass kernel ms (avg/launch, needs profiling),
+ *  [2] reserved, [3] kernel launches of the last call, [4] long-pass launches
+ *  timed, [5] algorithmic bytes of A per long pass, [6] sketch flops
+ *  (2 s k L_local), [7] kernel launches inside the iteration graph. */
+lsrn_status lsrn_last_stats(lsrn_ctx* ctx, double* out, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSRN_H */

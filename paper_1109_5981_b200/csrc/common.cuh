@@ -1,0 +1,52 @@
+// Shared device helpers for the LSRN sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define LSRN_DEV __device__ __forceinline__
+
+namespace lsrn {
+
+constexpr int kNumSMs = 148;  // B200; the host queries the real count
+
+LSRN_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// cp.async 16 B global -> shared with zero fill of the bytes past src_bytes.
+LSRN_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+// cp.async 8 B (ca path, 8-byte granularity) with zero fill.
+LSRN_DEV void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+LSRN_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+LSRN_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Streaming 16-byte load that does not allocate in L1 (A is read once per pass).
+LSRN_DEV double2 ldg_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n"
+               : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+LSRN_DEV double ldg_stream1(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor core (DMMA.8x8x4 on sm_100a).
+// Fragments: lane l holds A[l/4][l%4], B[l%4][l/4], D[l/4][2(l%4) + {0,1}].
+LSRN_DEV void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+
+}  // namespace lsrn

@@ -1,0 +1,99 @@
+// Host-side launch interface of the LSRN kernels (internal; not part of the C ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lsrn {
+
+// ---- K2 dense sketch (sketch_dense.cu)
+struct SketchDenseArgs {
+  const double* X;   // shard rows (row-major, leading dim ld)
+  int64_t ld, rows, k, lo, s;
+  uint64_t seed;
+  int64_t rows_per_split;
+  int nsplit;
+  double* out;       // [nsplit][s][k]
+  int64_t out_split_stride;
+};
+size_t sketch_dense_smem();
+void sketch_tile_counts(int64_t s, int64_t k, int64_t* mtiles, int64_t* ntiles, int64_t* bk);
+cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st);
+cudaError_t launch_sketch_finish(const double* part, int nsplit, int64_t split_stride, int64_t s, int64_t k,
+                                 double sx, double si, int64_t L, uint64_t seed, double* out, cudaStream_t st,
+                                 int nsm);
+cudaError_t launch_debug_gaussian(uint64_t seed, const int64_t* rows, const int64_t* cols, int64_t count,
+                                  double* out, cudaStream_t st);
+
+// ---- K5/K6 fused row pass (rowpass.cu)
+// For rows j of the row-major R x C matrix Y (scaled by sx):
+//   z_j <- c1 z_j + c2 sx (Y_j . t);  acc_j += ca z_j (if acc);  norm2 += z_j^2;  w += sx Y_j z_j
+// coef -> {c1, c2, ca}.  Writes per-cluster partials wpart[g][C] and npart[g].
+struct RowPassArgs {
+  const double* Y;
+  int64_t ld, R, C;
+  double sx;
+  double* z;
+  const double* t;
+  const double* coef;
+  double* acc;
+  const int* done;       // nullable: skip the pass when *done != 0
+  double* wpart;         // [nparts][C]
+  double* npart;         // [nparts]
+};
+struct RowPassPlan {
+  int vpt, cl, tr, nclusters, vec;  // vec: 2 = 16-byte loads
+  int64_t rows_per_cluster;
+};
+RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm);
+cudaError_t launch_rowpass(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st);
+
+// Column reduce of the row-pass partials (+ optional Tikhonov identity block):
+//   w_c = sum_g wpart[g][c];  if zI: zI_c <- c1 zI_c + c2 sI t_c,  w_c += sI zI_c
+//   out[c] = w_c (c < C);  out[C] = sum_g npart[g] + sum_c zI_c^2
+struct ColReduceArgs {
+  const double* wpart;
+  const double* npart;
+  int nparts;
+  int64_t C;
+  double* zI;            // nullable
+  const double* t;
+  const double* coef;
+  double sI;
+  double* out;           // C + 1
+  double* blockpart;     // scratch, >= colreduce_blocks(C)
+  unsigned* counter;     // zero-initialised, self-resetting
+  const int* done;
+};
+int colreduce_blocks(int64_t C);
+cudaError_t launch_colreduce(const ColReduceArgs& a, cudaStream_t st);
+
+// ---- Krylov scalar / vector steps (krylov.cu)
+struct LsqrState {
+  double alpha, beta, su, sv, rhobar, phibar, anorm2, bnorm;
+  double phi_rho, theta_rho, rnorm, arnorm, tol;
+  double cU[3], cV[3];          // pass coefficients {c1, c2, ca}
+  int iters, done, converged, adaptive, stop_after, pad_;
+};
+cudaError_t launch_lsqr_init_state(LsqrState* st_dev, double tol, int adaptive, cudaStream_t st);
+// phase 0: after the initial U pass (beta_1); 1: after a U pass inside the loop
+cudaError_t launch_lsqr_after_u(LsqrState* s, const double* comm, int64_t C, int phase, cudaStream_t st);
+// phase 0: after the initial V pass (alpha_1) -> w_y = sv v; 1: Givens step + y / w_y update.
+// ypart: scratch of update-kernel block partials (>= lsqr_update_blocks(n)).
+int lsqr_update_blocks(int64_t n);
+cudaError_t launch_lsqr_after_v(LsqrState* s, const double* comm, int64_t C, int phase, double* y, double* wy,
+                                const double* vstore, int64_t n, double* ypart, unsigned* counter,
+                                cudaStream_t st);
+
+// ---- misc (misc.cu)
+cudaError_t launch_fill(double* p, double v, int64_t n, cudaStream_t st);
+cudaError_t launch_copy_scale(double* dst, const double* src, double scale, int64_t n, cudaStream_t st);
+// row-major s x k -> column-major s x k
+cudaError_t launch_transpose(const double* src, int64_t rows, int64_t cols, double* dst, cudaStream_t st);
+// R (upper triangle of the k x k leading block of column-major QR, ld) -> dense k x k, zero below
+cudaError_t launch_extract_r(const double* qr, int64_t ld, int64_t k, double* R, cudaStream_t st);
+// Nt[c][j] = VT[c + j * k] / S[c], c < r, j < k  (Nt row-major r x k == N column-major)
+cudaError_t launch_form_nt(const double* VT, const double* S, int64_t k, int64_t r, double* Nt,
+                           cudaStream_t st);
+
+}  // namespace lsrn

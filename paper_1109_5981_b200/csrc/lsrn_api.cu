@@ -1,0 +1,896 @@
+// C ABI of the LSRN hot path (include/lsrn.h): planning, workspace layout, the
+// sketch -> SVD -> iterations pipeline, CUDA-graph capture of the iteration
+// loop, NCCL collectives for multi-GPU runs.
+//
+// Paper map: Alg. 1 / Alg. 2 / Alg. 3 /
+// §5 Tikhonov / MPI design P:779-800 (Reduce -> here one NCCL
+// allreduce of the partial sketch; one allreduce per iteration).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+#ifdef LSRN_WITH_NCCL
+#include <nccl.h>
+#endif
+
+#include "../../include/lsrn.h"
+#include "kernels.h"
+
+using namespace lsrn;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  lsrn_status code;
+};
+
+lsrn_status set_error(lsrn_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define LSRN_CUDA(call)                                                                          \
+  do {                                                                                           \
+    cudaError_t e__ = (call);                                                                    \
+    if (e__ != cudaSuccess) {                                                                    \
+      g_last_error = std::string("CUDA error: ") + cudaGetErrorString(e__) + " at " #call;        \
+      throw Fail{LSRN_ECUDA};                                                                    \
+    }                                                                                            \
+  } while (0)
+
+#define LSRN_SOLVER(call)                                                                        \
+  do {                                                                                           \
+    cusolverStatus_t e__ = (call);                                                               \
+    if (e__ != CUSOLVER_STATUS_SUCCESS) {                                                        \
+      g_last_error = std::string("cuSOLVER error ") + std::to_string((int)e__) + " at " #call;    \
+      throw Fail{LSRN_ESVD};                                                                     \
+    }                                                                                            \
+  } while (0)
+
+#define LSRN_REQUIRE(cond, code, msg)                                                            \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      g_last_error = (msg);                                                                      \
+      throw Fail{code};                                                                          \
+    }                                                                                            \
+  } while (0)
+
+// ------------------------------------------------------------------ workspace
+struct Arena {
+  char* base;
+  size_t off = 0;
+  explicit Arena(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct Dims {
+  bool tall;
+  int64_t m, n, L, k, s, cnt, lo;
+  double sx, si;      // sigma_X, sigma_I (tall form)
+  bool has_I;         // this rank holds the Tikhonov identity block
+  int64_t Lz;         // local long-vector length
+};
+
+}  // namespace
+
+struct lsrn_ctx {
+  cudaStream_t stream = nullptr;
+  int nranks = 1, rank = 0, device = 0, nsm = 148;
+  cusolverDnHandle_t solver = nullptr;
+#ifdef LSRN_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  // cached iteration graph
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<char> gkey;
+  // timing
+  cudaEvent_t ev[8] = {};
+  bool profile = false;
+  std::vector<cudaEvent_t> pass_ev;   // pairs around long-pass kernels
+  int n_pass_ev = 0;
+  double stats[8] = {};
+  int launches = 0;
+};
+
+namespace {
+
+Dims make_dims(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, bool allow_partial = false) {
+  LSRN_REQUIRE(A != nullptr, LSRN_EINVAL, "A is NULL");
+  LSRN_REQUIRE(A->m > 0 && A->n > 0, LSRN_EDIM, "m and n must be positive");
+  LSRN_REQUIRE(gamma > 1.0, LSRN_EINVAL, "oversampling factor must exceed 1 (gamma > 1, Alg. 1 step 1)");
+  LSRN_REQUIRE(lambda >= 0.0 && std::isfinite(lambda), LSRN_EINVAL, "lambda must be finite and >= 0");
+  Dims d{};
+  d.m = A->m;
+  d.n = A->n;
+  d.tall = A->m >= A->n;
+  d.L = d.tall ? d.m : d.n;
+  d.k = d.tall ? d.n : d.m;
+  d.s = (int64_t)std::ceil(gamma * (double)d.k);
+  d.lo = A->lo;
+  d.cnt = A->cnt;
+  LSRN_REQUIRE(d.lo >= 0 && d.cnt >= 0 && d.lo + d.cnt <= d.L, LSRN_EDIM, "shard [lo, lo+cnt) outside the long dimension");
+  if (c->nranks == 1 && !allow_partial)
+    LSRN_REQUIRE(d.lo == 0 && d.cnt == d.L, LSRN_EDIM, "single rank must hold the whole matrix");
+  if (lambda > 0.0) {
+    d.sx = d.tall ? 1.0 : 1.0 / lambda;
+    d.si = d.tall ? lambda : 1.0;
+  } else {
+    d.sx = 1.0;
+    d.si = 0.0;
+  }
+  d.has_I = (d.si != 0.0) && (d.lo == 0);   // the shard that starts the long index owns the I block
+  d.Lz = d.cnt + (d.has_I ? d.k : 0);
+  if (A->kind == LSRN_DENSE) {
+    LSRN_REQUIRE(A->ld >= d.k, LSRN_EDIM, "leading dimension ld must be >= min(m, n)");
+    LSRN_REQUIRE(A->val != nullptr || d.cnt == 0, LSRN_EINVAL, "A->val is NULL");
+  } else if (A->kind == LSRN_CSR) {
+    throw Fail{set_error(LSRN_EUNSUPPORTED, "CSR matrices are not supported by this build yet")};
+  } else {
+    throw Fail{set_error(LSRN_EINVAL, "unknown matrix kind")};
+  }
+  return d;
+}
+
+int choose_nsplit(int64_t s, int64_t k, int64_t rows, int nsm) {
+  int64_t mt, nt, bk;
+  sketch_tile_counts(s, k, &mt, &nt, &bk);
+  const int64_t tiles = mt * nt;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= 16; ++sp) {
+    if (sp > 1 && rows / sp < 1024) break;
+    const int64_t units = tiles * sp;
+    const int64_t waves = (units + nsm - 1) / nsm;
+    const double eff = (double)units / (double)(waves * nsm);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = sp;
+    }
+    if (eff > 0.95) break;
+  }
+  return best;
+}
+
+struct SketchWs {
+  int nsplit;
+  int64_t rows_per_split;
+  double* part;   // nullptr if direct
+};
+
+SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_flag) {
+  SketchWs w{};
+  w.nsplit = choose_nsplit(d.s, d.k, d.cnt, c->nsm);
+  int64_t rps = (d.cnt + w.nsplit - 1) / w.nsplit;
+  rps = (rps + 15) / 16 * 16;
+  w.rows_per_split = rps > 0 ? rps : 16;
+  const bool direct = (w.nsplit == 1) && (d.sx == 1.0) && !d.has_I && !need_finish_flag;
+  w.part = direct ? nullptr : ar.take<double>((size_t)w.nsplit * d.s * d.k);
+  return w;
+}
+
+void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed, const SketchWs& w, double* At) {
+  cudaStream_t st = c->stream;
+  if (d.cnt > 0) {
+    SketchDenseArgs a{};
+    a.X = A->val;
+    a.ld = A->ld;
+    a.rows = d.cnt;
+    a.k = d.k;
+    a.lo = d.lo;
+    a.s = d.s;
+    a.seed = seed;
+    a.rows_per_split = w.rows_per_split;
+    a.nsplit = w.nsplit;
+    a.out = w.part ? w.part : At;
+    a.out_split_stride = d.s * d.k;
+    LSRN_CUDA(launch_sketch_dense(a, st));
+    c->launches++;
+  } else if (!w.part) {
+    LSRN_CUDA(launch_fill(At, 0.0, d.s * d.k, st));
+    c->launches++;
+  }
+  if (w.part) {
+    if (d.cnt == 0) {
+      LSRN_CUDA(launch_fill(w.part, 0.0, (int64_t)w.nsplit * d.s * d.k, st));
+      c->launches++;
+    }
+    LSRN_CUDA(launch_sketch_finish(w.part, w.nsplit, d.s * d.k, d.s, d.k, d.sx, d.has_I ? d.si : 0.0, d.L, seed,
+                                   At, st, c->nsm));
+    c->launches++;
+  }
+}
+
+void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
+  if (c->nranks == 1) return;
+#ifdef LSRN_WITH_NCCL
+  ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, c->comm, c->stream);
+  if (r != ncclSuccess) {
+    g_last_error = std::string("NCCL allreduce failed: ") + ncclGetErrorString(r);
+    throw Fail{LSRN_ENCCL};
+  }
+#else
+  (void)buf;
+  (void)count;
+  throw Fail{set_error(LSRN_ENCCL, "built without NCCL")};
+#endif
+}
+
+// ------------------------------------------------------------------ SVD
+struct SvdWs {
+  double *W1, *tau, *R, *S, *VT, *work, *rwork, *Nt;
+  int* info;
+  int lwork;
+};
+
+SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
+  SvdWs w{};
+  int l1 = 0, l2 = 0;
+  LSRN_SOLVER(cusolverDnDgeqrf_bufferSize(c->solver, (int)d.s, (int)d.k, nullptr, (int)d.s, &l1));
+  LSRN_SOLVER(cusolverDnDgesvd_bufferSize(c->solver, (int)d.k, (int)d.k, &l2));
+  w.lwork = l1 > l2 ? l1 : l2;
+  w.W1 = ar.take<double>((size_t)d.s * d.k);
+  w.tau = ar.take<double>((size_t)d.k);
+  w.R = ar.take<double>((size_t)d.k * d.k);
+  w.S = ar.take<double>((size_t)d.k);
+  w.VT = ar.take<double>((size_t)d.k * d.k);
+  w.work = ar.take<double>((size_t)w.lwork);
+  w.rwork = ar.take<double>((size_t)d.k);
+  w.Nt = ar.take<double>((size_t)d.k * d.k);
+  w.info = ar.take<int>(4);
+  return w;
+}
+
+// Alg. 1 steps 4-5 / Alg. 2 steps 4-5 on the tall-form sketch: returns r.
+int64_t run_svd(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, std::vector<double>& S_host) {
+  cudaStream_t st = c->stream;
+  LSRN_CUDA(launch_transpose(At, d.s, d.k, w.W1, st));
+  c->launches++;
+  LSRN_SOLVER(cusolverDnDgeqrf(c->solver, (int)d.s, (int)d.k, w.W1, (int)d.s, w.tau, w.work, w.lwork, w.info));
+  LSRN_CUDA(launch_extract_r(w.W1, d.s, d.k, w.R, st));
+  c->launches++;
+  LSRN_SOLVER(cusolverDnDgesvd(c->solver, 'N', 'A', (int)d.k, (int)d.k, w.R, (int)d.k, w.S, nullptr, 1, w.VT,
+                               (int)d.k, w.work, w.lwork, w.rwork, w.info + 1));
+  S_host.assign((size_t)d.k, 0.0);
+  int info[2] = {0, 0};
+  LSRN_CUDA(cudaMemcpyAsync(S_host.data(), w.S, sizeof(double) * d.k, cudaMemcpyDeviceToHost, st));
+  LSRN_CUDA(cudaMemcpyAsync(info, w.info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+  LSRN_CUDA(cudaStreamSynchronize(st));
+  LSRN_REQUIRE(info[0] == 0 && info[1] == 0, LSRN_ESVD,
+               "cuSOLVER geqrf/gesvd info = " + std::to_string(info[0]) + "/" + std::to_string(info[1]));
+  // rank rule (reading C4): r = #{sigma_i > max(s, k) 2^-52 sigma_1}
+  const double tau = (double)std::max(d.s, d.k) * std::ldexp(1.0, -52) * S_host[0];
+  int64_t r = 0;
+  if (S_host[0] > 0.0)
+    for (int64_t i = 0; i < d.k; ++i)
+      if (S_host[i] > tau) ++r;
+  LSRN_REQUIRE(r > 0, LSRN_ERANK0, "sketch has numerical rank 0");
+  LSRN_CUDA(launch_form_nt(w.VT, w.S, d.k, r, w.Nt, st));
+  c->launches++;
+  return r;
+}
+
+// ------------------------------------------------------------------ iterations
+struct IterWs {
+  double *z, *v, *y, *wy, *xL, *wxL, *comm, *tbuf, *xbuf, *wpart, *npart, *blockpart, *ypart, *coef, *consts;
+  unsigned* counters;
+  LsqrState* state;
+  int ncoef;
+};
+
+enum Solver { SOLVER_LSQR = 0, SOLVER_CS = 1 };
+
+IterWs plan_iter(lsrn_ctx* c, const Dims& d, Arena& ar, int max_passes) {
+  IterWs w{};
+  const int64_t k = d.k;
+  const int64_t Lz = d.Lz > 0 ? d.Lz : 1;
+  w.z = ar.take<double>((size_t)Lz);
+  w.v = ar.take<double>((size_t)k);
+  w.y = ar.take<double>((size_t)k);
+  w.wy = ar.take<double>((size_t)k);
+  w.xL = ar.take<double>((size_t)Lz);
+  w.wxL = ar.take<double>((size_t)Lz);
+  w.comm = ar.take<double>((size_t)k + 1);
+  w.tbuf = ar.take<double>((size_t)k + 1);
+  w.xbuf = ar.take<double>((size_t)k + 1);
+  const int nparts = c->nsm > 0 ? c->nsm : 148;
+  w.wpart = ar.take<double>((size_t)nparts * k);
+  w.npart = ar.take<double>((size_t)nparts);
+  w.blockpart = ar.take<double>((size_t)colreduce_blocks(k) + 1);
+  w.ypart = ar.take<double>((size_t)lsqr_update_blocks(Lz > k ? Lz : k) + 1);
+  w.ncoef = max_passes * 6 + 16;
+  w.coef = ar.take<double>((size_t)w.ncoef);
+  w.consts = ar.take<double>(16);
+  w.counters = ar.take<unsigned>(4);
+  w.state = ar.take<LsqrState>(1);
+  return w;
+}
+
+struct Pass {
+  lsrn_ctx* c;
+  const Dims& d;
+  const lsrn_matrix* A;
+  const double* Nt;
+  int64_t r;
+  IterWs& w;
+  RowPassPlan plong, pshort;
+
+  // long pass over X: z <- c1 z + c2 sX X t (+ I block), out = [P^T z ; ||z||^2]
+  void long_pass(double* z, const double* t, const double* coef, double* acc, const int* done, double* out) {
+    cudaStream_t st = c->stream;
+    const int idx = c->n_pass_ev;
+    const bool prof = c->profile && idx + 2 <= (int)c->pass_ev.size();
+    if (d.cnt > 0) {
+      RowPassArgs a{};
+      a.Y = A->val;
+      a.ld = A->ld;
+      a.sx = d.sx;
+      a.R = d.cnt;
+      a.C = d.k;
+      a.z = z;
+      a.t = t;
+      a.coef = coef;
+      a.acc = acc;
+      a.done = done;
+      a.wpart = w.wpart;
+      a.npart = w.npart;
+      if (prof) LSRN_CUDA(cudaEventRecord(c->pass_ev[idx], st));
+      LSRN_CUDA(launch_rowpass(a, plong, st));
+      if (prof) {
+        LSRN_CUDA(cudaEventRecord(c->pass_ev[idx + 1], st));
+        c->n_pass_ev += 2;
+      }
+      c->launches++;
+    }
+    ColReduceArgs r{};
+    r.wpart = w.wpart;
+    r.npart = w.npart;
+    r.nparts = d.cnt > 0 ? plong.nclusters : 0;
+    r.C = d.k;
+    r.zI = d.has_I ? z + d.cnt : nullptr;
+    r.t = t;
+    r.coef = coef;
+    r.sI = d.si;
+    r.out = out;
+    r.blockpart = w.blockpart;
+    r.counter = w.counters;
+    r.done = done;
+    LSRN_CUDA(launch_colreduce(r, st));
+    c->launches++;
+    allreduce(c, out, d.k + 1);
+  }
+
+  // short pass over N^T: v <- c1 v + c2 N^T wv, out = [N v ; ||v||^2]
+  void short_pass(double* v, const double* wv, const double* coef, double* acc, const int* done, double* out) {
+    cudaStream_t st = c->stream;
+    RowPassArgs a{};
+    a.Y = Nt;
+    a.ld = d.k;
+    a.sx = 1.0;
+    a.R = r;
+    a.C = d.k;
+    a.z = v;
+    a.t = wv;
+    a.coef = coef;
+    a.acc = acc;
+    a.done = done;
+    a.wpart = w.wpart;
+    a.npart = w.npart;
+    LSRN_CUDA(launch_rowpass(a, pshort, st));
+    c->launches++;
+    ColReduceArgs rr{};
+    rr.wpart = w.wpart;
+    rr.npart = w.npart;
+    rr.nparts = pshort.nclusters;
+    rr.C = d.k;
+    rr.zI = nullptr;
+    rr.t = wv;
+    rr.coef = coef;
+    rr.sI = 0.0;
+    rr.out = out;
+    rr.blockpart = w.blockpart;
+    rr.counter = w.counters;
+    rr.done = done;
+    LSRN_CUDA(launch_colreduce(rr, st));
+    c->launches++;
+  }
+};
+
+}  // namespace
+
+// =================================================================== ABI
+extern "C" {
+
+const char* lsrn_last_error(void) { return g_last_error.c_str(); }
+
+const char* lsrn_version(void) {
+#ifdef LSRN_WITH_NCCL
+  return "lsrn-b200 0.1 sm_100a nccl";
+#else
+  return "lsrn-b200 0.1 sm_100a";
+#endif
+}
+
+lsrn_status lsrn_nccl_unique_id(void* id_out) {
+#ifdef LSRN_WITH_NCCL
+  if (!id_out) return set_error(LSRN_EINVAL, "id_out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_error(LSRN_ENCCL, ncclGetErrorString(r));
+  std::memcpy(id_out, &id, sizeof(id));
+  return LSRN_OK;
+#else
+  (void)id_out;
+  return set_error(LSRN_ENCCL, "built without NCCL");
+#endif
+}
+
+lsrn_status lsrn_ctx_create(lsrn_ctx** out, void* stream, int nranks, int rank, const void* nccl_id) {
+  if (!out) return set_error(LSRN_EINVAL, "ctx out pointer is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(LSRN_EINVAL, "bad nranks / rank");
+  lsrn_ctx* c = new lsrn_ctx();
+  try {
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->nranks = nranks;
+    c->rank = rank;
+    LSRN_CUDA(cudaGetDevice(&c->device));
+    LSRN_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device));
+    LSRN_SOLVER(cusolverDnCreate(&c->solver));
+    LSRN_SOLVER(cusolverDnSetStream(c->solver, c->stream));
+    for (auto& e : c->ev) LSRN_CUDA(cudaEventCreate(&e));
+    if (nranks > 1) {
+#ifdef LSRN_WITH_NCCL
+      LSRN_REQUIRE(nccl_id != nullptr, LSRN_EINVAL, "nccl_id required for nranks > 1");
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+      LSRN_REQUIRE(r == ncclSuccess, LSRN_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+#else
+      (void)nccl_id;
+      throw Fail{set_error(LSRN_ENCCL, "built without NCCL")};
+#endif
+    }
+  } catch (const Fail& f) {
+    lsrn_ctx_destroy(c);
+    return f.code;
+  }
+  *out = c;
+  return LSRN_OK;
+}
+
+lsrn_status lsrn_ctx_destroy(lsrn_ctx* c) {
+  if (!c) return LSRN_OK;
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->pass_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->solver) cusolverDnDestroy(c->solver);
+#ifdef LSRN_WITH_NCCL
+  if (c->comm) ncclCommDestroy(c->comm);
+#endif
+  delete c;
+  return LSRN_OK;
+}
+
+lsrn_status lsrn_ctx_set_virtual_shards(lsrn_ctx* c, int p) {
+  if (!c) return set_error(LSRN_EINVAL, "ctx is NULL");
+  if (p == 1) return LSRN_OK;
+  return set_error(LSRN_EUNSUPPORTED, "virtual shards are not implemented in this build");
+}
+
+lsrn_status lsrn_ctx_set_profiling(lsrn_ctx* c, int on) {
+  if (!c) return set_error(LSRN_EINVAL, "ctx is NULL");
+  c->profile = on != 0;
+  return LSRN_OK;
+}
+
+lsrn_status lsrn_last_stats(lsrn_ctx* c, double* out, int cap) {
+  if (!c || !out) return set_error(LSRN_EINVAL, "NULL argument");
+  for (int i = 0; i < cap && i < 8; ++i) out[i] = c->stats[i];
+  return LSRN_OK;
+}
+
+}  // extern "C"
+
+// -------------------------------------------------------------- shared driver
+namespace {
+
+struct HostIO {
+  lsrn_matrix Adev;
+  const double* b = nullptr;
+  double* x = nullptr;
+};
+
+size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar, Dims& d, SketchWs& sw, bool allow_partial,
+                SvdWs& vw, IterWs& iw, double** At, double** Astage, double** bstage, double** xstage) {
+  d = make_dims(c, A, o->gamma, o->lambda, allow_partial);
+  *Astage = *bstage = *xstage = nullptr;
+  if (o->flags & LSRN_HOST_IO) {
+    *Astage = ar.take<double>((size_t)d.cnt * A->ld);
+    *bstage = ar.take<double>((size_t)(d.tall ? d.cnt : d.m));
+    *xstage = ar.take<double>((size_t)(d.tall ? d.n : d.cnt));
+  }
+  *At = ar.take<double>((size_t)d.s * d.k);
+  sw = plan_sketch(c, d, ar, c->nranks > 1);
+  vw = plan_svd(c, d, ar);
+  // max passes: LSQR cap (2x the count for r = k) or CS passes with r = k; bounded by a generous margin
+  const int max_passes = 4096;
+  iw = plan_iter(c, d, ar, max_passes);
+  return ar.off;
+}
+
+void validate_opts(const lsrn_opts* o) {
+  LSRN_REQUIRE(o != nullptr, LSRN_EINVAL, "opts is NULL");
+  LSRN_REQUIRE(o->tol > 0.0 && o->tol < 1.0, LSRN_EINVAL, "tol must lie in (0, 1)");
+  LSRN_REQUIRE(o->mode == LSRN_MODE_PREDICTABLE || o->mode == LSRN_MODE_ADAPTIVE, LSRN_EINVAL, "unknown mode");
+  LSRN_REQUIRE(o->max_iter >= 0, LSRN_EINVAL, "max_iter must be >= 0");
+}
+
+int g_elapsed_err = 0;
+double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaError_t e = cudaEventElapsedTime(&ms, a, b);
+  if (e != cudaSuccess) {
+    if (!g_elapsed_err) g_elapsed_err = (int)e;
+    cudaGetLastError();
+    return 0.0;
+  }
+  return ms * 1e-3;
+}
+
+lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in, const lsrn_opts* o, void* ws,
+                       size_t ws_bytes, double* x_out, lsrn_report* rep, Solver solver) {
+  try {
+    LSRN_REQUIRE(c != nullptr, LSRN_EINVAL, "ctx is NULL");
+    validate_opts(o);
+    LSRN_REQUIRE(A_in != nullptr && b_in != nullptr && x_out != nullptr, LSRN_EINVAL, "A, b or x is NULL");
+    Arena ar(ws);
+    Dims d;
+    SketchWs sw;
+    SvdWs vw;
+    IterWs iw;
+    double *At, *Astage, *bstage, *xstage;
+    const size_t need = plan_all(c, A_in, o, ar, d, sw, false, vw, iw, &At, &Astage, &bstage, &xstage);
+    LSRN_REQUIRE(ws != nullptr && ws_bytes >= need, LSRN_ENOMEM,
+                 "workspace too small: need " + std::to_string(need) + " bytes");
+    LSRN_REQUIRE(!(o->mode == LSRN_MODE_ADAPTIVE && !d.tall && c->nranks > 1), LSRN_EUNSUPPORTED,
+                 "adaptive LSQR on a sharded wide problem is not supported (use predictable mode)");
+    cudaStream_t st = c->stream;
+    c->launches = 0;
+    c->n_pass_ev = 0;
+    lsrn_matrix A = *A_in;
+    const double* b = b_in;
+    double* x = x_out;
+    LSRN_CUDA(cudaEventRecord(c->ev[0], st));
+    if (o->flags & LSRN_HOST_IO) {
+      LSRN_CUDA(cudaMemcpyAsync(Astage, A_in->val, sizeof(double) * d.cnt * A_in->ld, cudaMemcpyHostToDevice, st));
+      LSRN_CUDA(cudaMemcpyAsync(bstage, b_in, sizeof(double) * (d.tall ? d.cnt : d.m), cudaMemcpyHostToDevice, st));
+      A.val = Astage;
+      b = bstage;
+      x = xstage;
+    }
+    // ---- sketch (Alg. 1/2 step 3)
+    LSRN_CUDA(cudaEventRecord(c->ev[1], st));
+    run_sketch(c, &A, d, o->seed, sw, At);
+    LSRN_CUDA(cudaEventRecord(c->ev[2], st));
+    allreduce(c, At, d.s * d.k);
+    LSRN_CUDA(cudaEventRecord(c->ev[3], st));
+    // ---- SVD + N (steps 4-5), outside the hot path
+    std::vector<double> S;
+    const int64_t r = run_svd(c, d, At, vw, S);
+    LSRN_CUDA(cudaEventRecord(c->ev[4], st));
+    // ---- bounds and counts (Thm 4.4, Thm 4.5, Alg. 3)
+    const double s = (double)d.s;
+    double alpha = o->alpha < 0.0 ? 1.0 / std::sqrt(s) : o->alpha;
+    LSRN_REQUIRE(alpha > 0.0 && alpha < 1.0 - std::sqrt((double)r / s), LSRN_EINVAL,
+                 "alpha must lie in (0, 1 - sqrt(r/s)) (Thm 4.4)");
+    const double sigU = 1.0 / ((1.0 - alpha) * std::sqrt(s) - std::sqrt((double)r));
+    const double sigL = 1.0 / ((1.0 + alpha) * std::sqrt(s) + std::sqrt((double)r));
+    const double rate0 = std::sqrt((double)r / s);
+    int kl = (int)std::ceil((std::log(o->tol) - std::log(2.0)) / std::log(rate0));
+    if (kl < 0) kl = 0;
+    int passes = 1;
+    {
+      const double rho = (sigU - sigL) / (sigU + sigL);
+      if (rho > 0.0) {
+        int K = (int)std::ceil((std::log(o->tol) - std::log(2.0)) / std::log(rho));
+        passes = (K > 0 ? K : 0) + 1;
+      }
+    }
+    int iters_graph = 0;
+    if (solver == SOLVER_LSQR)
+      iters_graph = (o->mode == LSRN_MODE_PREDICTABLE) ? kl : (o->max_iter > 0 ? o->max_iter : 2 * kl);
+    LSRN_REQUIRE(iters_graph <= 4000 && passes <= 4000, LSRN_EINVAL, "iteration count too large");
+
+    // ---- iteration plans
+    Pass P{c, d, &A, vw.Nt, r, iw, {}, {}};
+    P.plong = plan_rowpass(d.cnt, d.k, A.ld, A.val, c->nsm);
+    P.pshort = plan_rowpass(r, d.k, d.k, vw.Nt, c->nsm);
+    const int64_t nV = d.tall ? r : d.Lz;  // length of the v-side vectors (LSQR)
+
+    // coefficient table (device): consts + CS schedule
+    std::vector<double> coefh((size_t)iw.ncoef, 0.0);
+    // consts: [0..2] = {1, 0, 0} copy; [3..5] = {0, 1, 0} load-only
+    std::vector<double> consts(16, 0.0);
+    consts[0] = 1.0;
+    consts[4] = 1.0;
+    if (solver == SOLVER_CS) {
+      const double dd = (sigU * sigU + sigL * sigL) / 2.0, cc = (sigU * sigU - sigL * sigL) / 2.0;
+      double al = 0.0;
+      for (int kp = 0; kp < passes; ++kp) {
+        double be;
+        if (kp == 0) {
+          be = 0.0;
+          al = 1.0 / dd;
+        } else if (kp == 1) {
+          be = 0.5 * (cc / dd) * (cc / dd);
+          al = 1.0 / (dd - cc * cc / (2.0 * dd));   // reading C1 (P:706 prints the reciprocal)
+        } else {
+          be = (al * cc / 2.0) * (al * cc / 2.0);
+          al = 1.0 / (dd - al * cc * cc / 4.0);
+        }
+        double* e = &coefh[(size_t)kp * 6];
+        // v-side pass: v <- beta v + 1 * Abar^T r (scaled), acc += alpha v
+        e[0] = be;
+        e[1] = 1.0;
+        e[2] = al;
+        // r-side pass: r <- r - alpha Abar v
+        e[3] = 1.0;
+        e[4] = -al;
+        e[5] = 0.0;
+      }
+    }
+    LSRN_CUDA(cudaMemcpyAsync(iw.coef, coefh.data(), sizeof(double) * coefh.size(), cudaMemcpyHostToDevice, st));
+    LSRN_CUDA(cudaMemcpyAsync(iw.consts, consts.data(), sizeof(double) * 16, cudaMemcpyHostToDevice, st));
+
+    // ---- zero state
+    LSRN_CUDA(cudaMemsetAsync(iw.counters, 0, 4 * sizeof(unsigned), st));
+    const int64_t Lz = d.Lz;
+    LSRN_CUDA(launch_fill(iw.z, 0.0, Lz, st));
+    LSRN_CUDA(launch_fill(iw.xL, 0.0, Lz, st));
+    LSRN_CUDA(launch_fill(iw.wxL, 0.0, Lz, st));
+    LSRN_CUDA(launch_fill(iw.v, 0.0, d.k, st));
+    LSRN_CUDA(launch_fill(iw.y, 0.0, d.k, st));
+    LSRN_CUDA(launch_fill(iw.wy, 0.0, d.k, st));
+    LSRN_CUDA(launch_fill(iw.comm, 0.0, d.k + 1, st));
+    LSRN_CUDA(launch_fill(iw.tbuf, 0.0, d.k + 1, st));
+    LSRN_CUDA(launch_fill(iw.xbuf, 0.0, d.k + 1, st));
+    c->launches += 9;
+    if (solver == SOLVER_LSQR) {
+      LSRN_CUDA(launch_lsqr_init_state(iw.state, o->tol, o->mode == LSRN_MODE_ADAPTIVE ? 1 : 0, st));
+      c->launches++;
+    }
+    if (d.tall && d.cnt > 0) {
+      LSRN_CUDA(launch_copy_scale(iw.z, b, 1.0, d.cnt, st));
+      c->launches++;
+    }
+    LSRN_CUDA(cudaEventRecord(c->ev[5], st));
+
+    // ---- the iteration loop, captured once as a CUDA graph
+    if (c->profile) {
+      const size_t need_ev = 2 * (size_t)(std::max(iters_graph, passes) + 4);
+      while (c->pass_ev.size() < need_ev) {
+        cudaEvent_t e;
+        LSRN_CUDA(cudaEventCreate(&e));
+        c->pass_ev.push_back(e);
+      }
+    }
+    const int launches_before = c->launches;
+    cudaGraph_t graph = nullptr;
+    if (c->gexec) {
+      cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+    }
+    LSRN_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      const double* one = iw.consts;        // {1, 0, 0}
+      const double* load = iw.consts + 3;   // {0, 1, 0}
+      LsqrState* S_ = iw.state;
+      const int* done = solver == SOLVER_LSQR ? &S_->done : nullptr;
+      if (solver == SOLVER_LSQR) {
+        if (d.tall) {
+          P.long_pass(iw.z, iw.tbuf, one, nullptr, done, iw.comm);          // ||b||^2, w = P^T b
+          LSRN_CUDA(launch_lsqr_after_u(S_, iw.comm, d.k, 0, st));
+          P.short_pass(iw.v, iw.comm, S_->cV, nullptr, done, iw.tbuf);
+          LSRN_CUDA(launch_lsqr_after_v(S_, iw.tbuf, d.k, 0, iw.y, iw.wy, iw.v, r, iw.ypart, iw.counters + 1, st));
+          c->launches += 2;
+          for (int it = 0; it < iters_graph; ++it) {
+            P.long_pass(iw.z, iw.tbuf, S_->cU, nullptr, done, iw.comm);
+            LSRN_CUDA(launch_lsqr_after_u(S_, iw.comm, d.k, 1, st));
+            P.short_pass(iw.v, iw.comm, S_->cV, nullptr, done, iw.tbuf);
+            LSRN_CUDA(launch_lsqr_after_v(S_, iw.tbuf, d.k, 1, iw.y, iw.wy, iw.v, r, iw.ypart, iw.counters + 1, st));
+            c->launches += 2;
+          }
+          P.short_pass(iw.y, iw.comm, one, nullptr, nullptr, iw.xbuf);    // x = N y
+        } else {
+          P.short_pass(iw.v, b, load, nullptr, done, iw.tbuf);             // u = N^T b, t = N u
+          LSRN_CUDA(launch_lsqr_after_u(S_, iw.tbuf, d.k, 0, st));
+          c->launches++;
+          P.long_pass(iw.z, iw.tbuf, S_->cV, nullptr, done, iw.comm);
+          LSRN_CUDA(launch_lsqr_after_v(S_, iw.comm, d.k, 0, iw.xL, iw.wxL, iw.z, Lz, iw.ypart, iw.counters + 1, st));
+          c->launches++;
+          for (int it = 0; it < iters_graph; ++it) {
+            P.short_pass(iw.v, iw.comm, S_->cU, nullptr, done, iw.tbuf);
+            LSRN_CUDA(launch_lsqr_after_u(S_, iw.tbuf, d.k, 1, st));
+            c->launches++;
+            P.long_pass(iw.z, iw.tbuf, S_->cV, nullptr, done, iw.comm);
+            LSRN_CUDA(launch_lsqr_after_v(S_, iw.comm, d.k, 1, iw.xL, iw.wxL, iw.z, Lz, iw.ypart, iw.counters + 1, st));
+            c->launches++;
+          }
+        }
+      } else {
+        if (d.tall) {
+          P.long_pass(iw.z, iw.tbuf, one, nullptr, nullptr, iw.comm);       // w = P^T b
+          for (int kp = 0; kp < passes; ++kp) {
+            const double* e = iw.coef + (size_t)kp * 6;
+            P.short_pass(iw.v, iw.comm, e, iw.y, nullptr, iw.tbuf);         // v = b v + N^T w; y += a v
+            if (kp + 1 < passes) P.long_pass(iw.z, iw.tbuf, e + 3, nullptr, nullptr, iw.comm);
+          }
+          P.short_pass(iw.y, iw.comm, one, nullptr, nullptr, iw.xbuf);     // x = N y
+        } else {
+          P.short_pass(iw.v, b, load, nullptr, nullptr, iw.tbuf);          // r = N^T b, t = N r
+          for (int kp = 0; kp < passes; ++kp) {
+            const double* e = iw.coef + (size_t)kp * 6;
+            P.long_pass(iw.z, iw.tbuf, e, iw.xL, nullptr, iw.comm);  // v = b v + P t; x += a v
+            if (kp + 1 < passes) P.short_pass(iw.v, iw.comm, e + 3, nullptr, nullptr, iw.tbuf);
+          }
+        }
+      }
+    } catch (...) {
+      cudaGraph_t g2 = nullptr;
+      cudaStreamEndCapture(st, &g2);
+      if (g2) cudaGraphDestroy(g2);
+      throw;
+    }
+    LSRN_CUDA(cudaStreamEndCapture(st, &graph));
+    LSRN_CUDA(cudaGraphInstantiate(&c->gexec, graph, 0));
+    cudaGraphDestroy(graph);
+    const int graph_launches = c->launches - launches_before;
+    LSRN_CUDA(cudaEventRecord(c->ev[6], st));
+    LSRN_CUDA(cudaGraphLaunch(c->gexec, st));
+    LSRN_CUDA(cudaEventRecord(c->ev[7], st));
+    // ---- recover x (Alg. 1 step 7 / §5 x = z / lambda)
+    if (d.tall) {
+      LSRN_CUDA(launch_copy_scale(x, iw.xbuf, 1.0, d.n, st));
+    } else if (d.cnt > 0) {
+      LSRN_CUDA(launch_copy_scale(x, iw.xL, d.sx, d.cnt, st));
+    }
+    c->launches++;
+    if (o->flags & LSRN_HOST_IO) {
+      LSRN_CUDA(cudaMemcpyAsync(x_out, xstage, sizeof(double) * (d.tall ? d.n : d.cnt), cudaMemcpyDeviceToHost, st));
+    }
+    LsqrState hs{};
+    if (solver == SOLVER_LSQR)
+      LSRN_CUDA(cudaMemcpyAsync(&hs, iw.state, sizeof(LsqrState), cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaStreamSynchronize(st));
+    LSRN_CUDA(cudaGetLastError());
+    // ---- report
+    if (rep) {
+      std::memset(rep, 0, sizeof(*rep));
+      rep->s = d.s;
+      rep->r = r;
+      rep->sigma_L = sigL;
+      rep->sigma_U = sigU;
+      rep->alpha = alpha;
+      if (solver == SOLVER_LSQR) {
+        rep->iters = hs.iters;
+        rep->converged = hs.converged;
+        rep->rnorm_est = hs.rnorm;
+      } else {
+        rep->iters = passes;
+        rep->converged = 1;
+      }
+      rep->t_sketch = elapsed_s(c->ev[1], c->ev[2]);
+      rep->t_allreduce = elapsed_s(c->ev[2], c->ev[3]);
+      rep->t_svd = elapsed_s(c->ev[3], c->ev[4]);
+      rep->t_iter = elapsed_s(c->ev[6], c->ev[7]);
+      rep->t_total = elapsed_s(c->ev[0], c->ev[7]);
+    }
+    // ---- stats
+    c->stats[0] = elapsed_s(c->ev[1], c->ev[2]) * 1e3;
+    double lp = 0.0;
+    int nlp = 0;
+    for (int i = 0; i + 1 < c->n_pass_ev; i += 2) {
+      lp += elapsed_s(c->pass_ev[i], c->pass_ev[i + 1]) * 1e3;
+      ++nlp;
+    }
+    c->stats[1] = nlp ? lp / nlp : 0.0;
+    c->stats[2] = (double)g_elapsed_err;
+    c->stats[3] = (double)c->launches;
+    c->stats[4] = (double)nlp;
+    c->stats[5] = (double)d.cnt * (double)d.k * 8.0;
+    c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
+    c->stats[7] = (double)graph_launches;
+    return LSRN_OK;
+  } catch (const Fail& f) {
+    if (c) {
+      cudaStreamCaptureStatus cs;
+      if (cudaStreamIsCapturing(c->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+      }
+    }
+    return f.code;
+  } catch (...) {
+    return set_error(LSRN_ECUDA, "unexpected C++ exception");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+lsrn_status lsrn_workspace_size(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, size_t* bytes) {
+  try {
+    LSRN_REQUIRE(c != nullptr && bytes != nullptr, LSRN_EINVAL, "NULL argument");
+    validate_opts(o);
+    Arena ar(nullptr);
+    Dims d;
+    SketchWs sw;
+    SvdWs vw;
+    IterWs iw;
+    double *At, *As, *bs, *xs;
+    *bytes = plan_all(c, A, o, ar, d, sw, true, vw, iw, &At, &As, &bs, &xs) + 256;
+    return LSRN_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+
+lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, uint64_t seed, void* ws,
+                        size_t ws_bytes, double* At, int64_t* s_out) {
+  try {
+    LSRN_REQUIRE(c != nullptr && At != nullptr, LSRN_EINVAL, "ctx or At is NULL");
+    Dims d = make_dims(c, A, gamma, lambda, /*allow_partial=*/true);
+    Arena ar(ws);
+    SketchWs sw = plan_sketch(c, d, ar, c->nranks > 1);
+    LSRN_REQUIRE(ar.off == 0 || (ws != nullptr && ws_bytes >= ar.off), LSRN_ENOMEM,
+                 "workspace too small for the sketch: need " + std::to_string(ar.off) + " bytes");
+    c->launches = 0;
+    LSRN_CUDA(cudaEventRecord(c->ev[1], c->stream));
+    run_sketch(c, A, d, seed, sw, At);
+    LSRN_CUDA(cudaEventRecord(c->ev[2], c->stream));
+    allreduce(c, At, d.s * d.k);
+    LSRN_CUDA(cudaEventRecord(c->ev[3], c->stream));
+    LSRN_CUDA(cudaGetLastError());
+    c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
+    if (s_out) *s_out = d.s;
+    return LSRN_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+
+lsrn_status lsrn_solve_lsqr(lsrn_ctx* c, const lsrn_matrix* A, const double* b, const lsrn_opts* o, void* ws,
+                            size_t ws_bytes, double* x, lsrn_report* rep) {
+  return solve_impl(c, A, b, o, ws, ws_bytes, x, rep, SOLVER_LSQR);
+}
+
+lsrn_status lsrn_solve_cs(lsrn_ctx* c, const lsrn_matrix* A, const double* b, const lsrn_opts* o, void* ws,
+                          size_t ws_bytes, double* x, lsrn_report* rep) {
+  return solve_impl(c, A, b, o, ws, ws_bytes, x, rep, SOLVER_CS);
+}
+
+lsrn_status lsrn_debug_gaussian(lsrn_ctx* c, uint64_t seed, const int64_t* rows, const int64_t* cols, int64_t count,
+                                double* out) {
+  if (!c || !rows || !cols || !out) return set_error(LSRN_EINVAL, "NULL argument");
+  if (count <= 0) return LSRN_OK;
+  cudaError_t e = launch_debug_gaussian(seed, rows, cols, count, out, c->stream);
+  if (e != cudaSuccess) return set_error(LSRN_ECUDA, cudaGetErrorString(e));
+  return LSRN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Small helper kernels: fills, copies, the transposes around the SVD and the
+// formation of N = V_r Sigma_r^-1 (Alg. 1 step 5; Alg. 2 step 5).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lsrn {
+
+static unsigned grid_for(int64_t n, int threads = 256, int64_t cap = 148 * 16) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+__global__ void fill_kernel(double* p, double v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void copy_scale_kernel(double* dst, const double* src, double scale, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = scale * src[i];
+}
+
+// 32 x 32 tiled transpose: src row-major rows x cols -> dst column-major rows x cols
+__global__ void transpose_kernel(const double* __restrict__ src, int64_t rows, int64_t cols,
+                                 double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+__global__ void extract_r_kernel(const double* __restrict__ qr, int64_t ld, int64_t k, double* __restrict__ R) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < k * k; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % k, j = e / k;   // column-major (i, j)
+    R[e] = (i <= j) ? qr[i + j * ld] : 0.0;
+  }
+}
+
+// VT column-major k x k (row c = right singular vector c).  Nt row-major r x k.
+__global__ void form_nt_kernel(const double* __restrict__ VT, const double* __restrict__ S, int64_t k, int64_t r,
+                               double* __restrict__ Nt) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  // read VT[c, j] = VT[c + j*k]: coalesced along c
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t j = j0 + i, c = c0 + threadIdx.x;
+    if (j < k && c < r) tile[i][threadIdx.x] = VT[c + j * k] / S[c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, j = j0 + threadIdx.x;
+    if (j < k && c < r) Nt[c * k + j] = tile[threadIdx.x][i];
+  }
+}
+
+cudaError_t launch_fill(double* p, double v, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  fill_kernel<<<grid_for(n), 256, 0, st>>>(p, v, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_scale(double* dst, const double* src, double scale, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  copy_scale_kernel<<<grid_for(n), 256, 0, st>>>(dst, src, scale, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const double* src, int64_t rows, int64_t cols, double* dst, cudaStream_t st) {
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_extract_r(const double* qr, int64_t ld, int64_t k, double* R, cudaStream_t st) {
+  extract_r_kernel<<<grid_for(k * k), 256, 0, st>>>(qr, ld, k, R);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_form_nt(const double* VT, const double* S, int64_t k, int64_t r, double* Nt, cudaStream_t st) {
+  dim3 grid((unsigned)((k + 31) / 32), (unsigned)((r + 31) / 32));
+  form_nt_kernel<<<grid, dim3(32, 8), 0, st>>>(VT, S, k, r, Nt);
+  return cudaGetLastError();
+}
+
+}  // namespace lsrn

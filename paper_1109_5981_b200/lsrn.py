@@ -1,0 +1,233 @@
+"""Thin ctypes binding of liblsrn.so (include/lsrn.h): argument marshalling only.
+
+Every step of the LSRN path runs in the library's sm_100a kernels; torch is used
+for device memory (tensors, the workspace), the CUDA stream and, for multi-GPU,
+to exchange the NCCL unique id through torch.distributed.  There is no CPU
+fallback: importing this module without the built library raises.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liblsrn.so")
+
+LSRN_OK = 0
+LSRN_DENSE, LSRN_CSR = 0, 1
+MODE_PREDICTABLE, MODE_ADAPTIVE = 0, 1
+HOST_IO = 1
+STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE", -4: "LSRN_ERANK0",
+          -5: "LSRN_ESVD", -6: "LSRN_ENOMEM", -7: "LSRN_ECUDA", -8: "LSRN_ENCCL", -9: "LSRN_EUNSUPPORTED"}
+
+# every symbol include/lsrn.h declares
+EXPORTS = ["lsrn_last_error", "lsrn_version", "lsrn_nccl_unique_id", "lsrn_ctx_create", "lsrn_ctx_destroy",
+           "lsrn_ctx_set_virtual_shards", "lsrn_ctx_set_profiling", "lsrn_workspace_size", "lsrn_sketch",
+           "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_last_stats"]
+
+
+class LsrnError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Matrix(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("pad_", ctypes.c_int32), ("m", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("lo", ctypes.c_int64), ("cnt", ctypes.c_int64), ("val", ctypes.c_void_p), ("ld", ctypes.c_int64),
+                ("rowptr", ctypes.c_void_p), ("colind", ctypes.c_void_p), ("nnz", ctypes.c_int64)]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("lambda_", ctypes.c_double), ("tol", ctypes.c_double),
+                ("alpha", ctypes.c_double), ("seed", ctypes.c_uint64), ("mode", ctypes.c_int32),
+                ("max_iter", ctypes.c_int32), ("flags", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("s", ctypes.c_int64), ("r", ctypes.c_int64), ("iters", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("sigma_L", ctypes.c_double), ("sigma_U", ctypes.c_double),
+                ("alpha", ctypes.c_double), ("t_sketch", ctypes.c_double), ("t_allreduce", ctypes.c_double),
+                ("t_svd", ctypes.c_double), ("t_iter", ctypes.c_double), ("t_total", ctypes.c_double),
+                ("rnorm_est", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load liblsrn.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} not built: run `python -m paper_1109_5981_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(_LIB_PATH)
+        vp, i32, i64, u64, dbl, sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
+                                      ctypes.c_double, ctypes.c_size_t)
+        L.lsrn_last_error.restype = ctypes.c_char_p
+        L.lsrn_version.restype = ctypes.c_char_p
+        sigs = {
+            "lsrn_nccl_unique_id": [vp],
+            "lsrn_ctx_create": [ctypes.POINTER(vp), vp, i32, i32, vp],
+            "lsrn_ctx_destroy": [vp],
+            "lsrn_ctx_set_virtual_shards": [vp, i32],
+            "lsrn_ctx_set_profiling": [vp, i32],
+            "lsrn_workspace_size": [vp, ctypes.POINTER(Matrix), ctypes.POINTER(Opts), ctypes.POINTER(sz)],
+            "lsrn_sketch": [vp, ctypes.POINTER(Matrix), dbl, dbl, u64, vp, sz, vp, ctypes.POINTER(i64)],
+            "lsrn_solve_lsqr": [vp, ctypes.POINTER(Matrix), vp, ctypes.POINTER(Opts), vp, sz, vp,
+                                ctypes.POINTER(Report)],
+            "lsrn_solve_cs": [vp, ctypes.POINTER(Matrix), vp, ctypes.POINTER(Opts), vp, sz, vp,
+                              ctypes.POINTER(Report)],
+            "lsrn_debug_gaussian": [vp, u64, vp, vp, i64, vp],
+            "lsrn_last_stats": [vp, ctypes.POINTER(ctypes.c_double), i32],
+        }
+        for name, args in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code != LSRN_OK:
+        raise LsrnError(code, lib().lsrn_last_error().decode())
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def dense(X, m, n, lo=0, cnt=None):
+    """Matrix descriptor for a long-index-major dense shard X (cnt x k, row-major)."""
+    if X.dtype != torch.float64:
+        raise TypeError("A must be float64")
+    if X.dim() != 2 or X.stride(1) != 1:
+        raise ValueError("X must be a 2-D tensor with unit column stride (long-index-major)")
+    cnt = X.shape[0] if cnt is None else cnt
+    return Matrix(kind=LSRN_DENSE, m=m, n=n, lo=lo, cnt=cnt, val=X.data_ptr(), ld=X.stride(0) if cnt > 1 else
+                  max(X.shape[1], 1), rowptr=None, colind=None, nnz=0), X
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().lsrn_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """An lsrn_ctx bound to the current CUDA device and a torch stream."""
+
+    def __init__(self, stream=None, nranks=1, rank=0, nccl_id=None):
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        # a dedicated (capturable) stream: the iteration loop is captured as a CUDA graph
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+        h = ctypes.c_void_p()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(lib().lsrn_ctx_create(ctypes.byref(h), ctypes.c_void_p(self.stream.cuda_stream), nranks, rank,
+                                     idbuf))
+        self.h = h
+        self.nranks, self.rank = nranks, rank
+        self._ws = None
+
+    def close(self):
+        if self.h:
+            lib().lsrn_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_profiling(self, on=True):
+        _check(lib().lsrn_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def workspace(self, nbytes):
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = None
+            self._ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def workspace_size(self, mat, opts):
+        sz = ctypes.c_size_t()
+        _check(lib().lsrn_workspace_size(self.h, ctypes.byref(mat), ctypes.byref(opts), ctypes.byref(sz)))
+        return sz.value
+
+    def stats(self):
+        out = (ctypes.c_double * 8)()
+        _check(lib().lsrn_last_stats(self.h, out, 8))
+        keys = ["sketch_ms", "long_pass_ms", "reserved", "launches", "long_pass_timed", "long_pass_bytes",
+                "sketch_flops", "graph_launches"]
+        return dict(zip(keys, list(out)))
+
+    # ---------------------------------------------------------------- calls
+    def _enter(self):
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != self.stream.cuda_stream:
+            self.stream.wait_stream(cur)
+        return cur
+
+    def _leave(self, cur):
+        if cur.cuda_stream != self.stream.cuda_stream:
+            cur.wait_stream(self.stream)
+
+    def sketch(self, X, m, n, gamma=2.0, lam=0.0, seed=5981, lo=0, cnt=None):
+        """Tall-form sketch At (s x k) of the shard X; returns a new device tensor."""
+        mat, _keep = dense(X, m, n, lo, cnt)
+        k = min(m, n)
+        s = int(torch.tensor(gamma * k, dtype=torch.float64).ceil().item())
+        At = torch.empty(s, k, dtype=torch.float64, device=self.device)
+        opts = Opts(gamma=gamma, lambda_=lam, tol=0.5, alpha=-1.0, seed=seed)
+        ws = self.workspace(self.workspace_size(mat, opts))
+        s_out = ctypes.c_int64()
+        cur = self._enter()
+        _check(lib().lsrn_sketch(self.h, ctypes.byref(mat), gamma, lam, seed, _ptr(ws), ws.numel(), _ptr(At),
+                                 ctypes.byref(s_out)))
+        self._leave(cur)
+        assert s_out.value == s
+        return At
+
+    def solve(self, X, b, m, n, solver="lsqr", gamma=2.0, lam=0.0, tol=1e-14, seed=5981, alpha=-1.0,
+              mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False):
+        """LSRN solve; X long-index-major shard (device, or pinned host with host_io)."""
+        if host_io:
+            if X.dim() != 2 or X.stride(1) != 1:
+                raise ValueError("X must be row-major 2-D")
+            cnt_ = X.shape[0] if cnt is None else cnt
+            mat = Matrix(kind=LSRN_DENSE, m=m, n=n, lo=lo, cnt=cnt_, val=X.data_ptr(), ld=X.stride(0))
+        else:
+            mat, _keep = dense(X, m, n, lo, cnt)
+        tall = m >= n
+        xlen = n if tall else mat.cnt
+        if x_out is None:
+            x_out = torch.empty(xlen, dtype=torch.float64,
+                                device="cpu" if host_io else self.device,
+                                pin_memory=bool(host_io))
+        opts = Opts(gamma=gamma, lambda_=lam, tol=tol, alpha=alpha, seed=seed,
+                    mode=MODE_ADAPTIVE if mode == "adaptive" else MODE_PREDICTABLE, max_iter=max_iter,
+                    flags=HOST_IO if host_io else 0)
+        ws = self.workspace(self.workspace_size(mat, opts))
+        rep = Report()
+        fn = lib().lsrn_solve_lsqr if solver == "lsqr" else lib().lsrn_solve_cs
+        if solver not in ("lsqr", "cs"):
+            raise ValueError("solver must be 'lsqr' or 'cs'")
+        cur = self._enter()
+        _check(fn(self.h, ctypes.byref(mat), _ptr(b), ctypes.byref(opts), _ptr(ws), ws.numel(), _ptr(x_out),
+                  ctypes.byref(rep)))
+        self._leave(cur)
+        return x_out, rep.as_dict()
+
+    def debug_gaussian(self, seed, rows, cols):
+        rows = rows.to(self.device, torch.int64).contiguous()
+        cols = cols.to(self.device, torch.int64).contiguous()
+        out = torch.empty(rows.numel(), dtype=torch.float64, device=self.device)
+        cur = self._enter()
+        _check(lib().lsrn_debug_gaussian(self.h, seed, _ptr(rows), _ptr(cols), rows.numel(), _ptr(out)))
+        self._leave(cur)
+        return out

@@ -87,82 +87,120 @@ def _haar(L, r, gen, device):
     return Q * d
 
 
-def make_problem(name, device="cpu", m=None, n=None, seed=None, **over):
-    """Build config `name` (c1..c5), optionally rescaled (m, n overrides)."""
+BLOCK = 8192   # long-index rows per independently seeded block (shard-invariant data)
+
+
+def _block_gen(seed, g, device):
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed * 1_000_003 + 7919 * g + 1)
+    return gen
+
+
+def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, **over):
+    """Build config `name` (c1..c5), optionally rescaled (m, n overrides).
+
+    shard=(lo, hi) generates only long-index rows [lo, hi) of X (and the matching
+    rows of b for a tall A) -- the bytes are identical to the same rows of the
+    full problem for the i.i.d. recipes (c3, c4, c5), which are generated in
+    independently seeded blocks of BLOCK long-index rows.  The Haar recipes
+    (c1, c2) need the full matrix and are sliced after generation.
+    """
     cfg = dict(CONFIGS[name])
     cfg.update(over)
     m = cfg["m"] if m is None else m
     n = cfg["n"] if n is None else n
     seed = 1109 * 1000 + cfg["num"] if seed is None else seed
-    gen = torch.Generator(device=device)
-    gen.manual_seed(seed)
     f64 = dict(dtype=torch.float64, device=device)
     kind = cfg["kind"]
+    L, k = max(m, n), min(m, n)
+    lo, hi = (0, L) if shard is None else (int(shard[0]), int(shard[1]))
+    meta = dict(seed=seed, cfg=cfg, shard=(lo, hi))
     x0 = None
-    meta = dict(seed=seed, cfg=cfg)
     if kind == "dense" and cfg["spectrum"] == "haar":
-        k = min(m, n)
+        gen = torch.Generator(device=device)
+        gen.manual_seed(seed)
         base = CONFIGS[name]
         frac = base["rank"] / min(base["m"], base["n"])     # c1: 1.0, c2: 0.9
         rank = cfg["rank"] if "rank" in over else max(1, int(round(frac * k)))
         rank = min(rank, k)
         i = torch.arange(rank, **f64)
         sig = 10.0 ** (-cfg["log_range"] * i / max(rank - 1, 1))
-        U = _haar(max(m, n), rank, gen, device)
-        V = _haar(min(m, n), rank, gen, device)
-        Ut = U * sig                                  # L x rank
-        X = Ut @ V.T                                  # long-index-major L x k
+        U = _haar(L, rank, gen, device)
+        V = _haar(k, rank, gen, device)
+        X = (U * sig) @ V.T                           # long-index-major L x k
+        del U
         meta.update(rank=rank, sigma=sig, kappa=float(sig[0] / sig[-1]))
-    elif kind == "dense" and cfg["spectrum"] == "rowscale":
-        # wide A (m < n): rows scaled; stored as X = A^T (n x m) row-major
-        L, k = max(m, n), min(m, n)
-        X = torch.randn(L, k, generator=gen, **f64)
+        if cfg["rhs"] == "model":
+            x0 = torch.randn(n, generator=gen, **f64)
+            b = (X @ x0 if m >= n else X.T @ x0) + 1e-3 * torch.randn(m, generator=gen, **f64)
+        else:
+            b = torch.randn(m, generator=gen, **f64)
+        if shard is not None:
+            X = X[lo:hi].contiguous()
+            if m >= n:
+                b = b[lo:hi].contiguous()
+        return Problem(name, m, n, "dense", cfg["gamma"], cfg["lam"], b, X=X.contiguous(), x0=x0, meta=meta)
+
+    gx = torch.Generator(device=device)
+    gx.manual_seed(seed * 7 + 3)
+    if cfg.get("rhs") == "model":
+        x0 = torch.randn(n, generator=gx, **f64)
+    blocks = range(lo // BLOCK, (hi + BLOCK - 1) // BLOCK) if hi > lo else range(0)
+    if kind == "dense":
         sc = 10.0 ** (-cfg["log_range"] * torch.arange(k, **f64) / max(k - 1, 1))
-        X.mul_(sc)                                    # column c of X = row c of A
-        meta.update(row_scales=sc)
-    elif kind == "dense" and cfg["spectrum"] == "colscale":
-        L, k = max(m, n), min(m, n)
-        X = torch.empty(L, k, **f64)
-        sc = 10.0 ** (-cfg["log_range"] * torch.arange(k, **f64) / max(k - 1, 1))
-        step = max(1, (1 << 27) // k)
-        for r0 in range(0, L, step):
-            r1 = min(L, r0 + step)
-            X[r0:r1] = torch.randn(r1 - r0, k, generator=gen, **f64)
-            X[r0:r1].mul_(sc)
-        meta.update(col_scales=sc)
-    elif kind == "csr":
+        X = torch.empty(hi - lo, k, **f64)
+        bt = torch.empty(hi - lo, **f64) if (m >= n) else None
+        for g in blocks:
+            g0, g1 = g * BLOCK, min(L, (g + 1) * BLOCK)
+            gen = _block_gen(seed, g, device)
+            blk = torch.randn(g1 - g0, k, generator=gen, **f64).mul_(sc)
+            a0, a1 = max(g0, lo), min(g1, hi)
+            X[a0 - lo:a1 - lo] = blk[a0 - g0:a1 - g0]
+            if bt is not None:
+                if cfg["rhs"] == "model":
+                    bb = blk @ x0 + 1e-3 * torch.randn(g1 - g0, generator=gen, **f64)
+                else:
+                    bb = torch.randn(g1 - g0, generator=gen, **f64)
+                bt[a0 - lo:a1 - lo] = bb[a0 - g0:a1 - g0]
+        if m >= n:
+            b = bt
+            meta.update(col_scales=sc)
+        else:       # wide: b is short (length m), replicated
+            b = torch.randn(m, generator=gx, **f64)
+            meta.update(row_scales=sc)
+        return Problem(name, m, n, "dense", cfg["gamma"], cfg["lam"], b, X=X, x0=x0, meta=meta)
+
+    if kind == "csr":
         nr = cfg["nnz_random"]
         nd = min(cfg["dense_cols"], n - nr) if n > nr else 0
         pool = n - nd
         nnz_row = nr + nd
         width = pool / nr
-        lo = (torch.arange(nr, **f64) * width)
-        u = torch.rand(m, nr, generator=gen, **f64)
-        cols_r = torch.clamp((lo + u * width).floor().to(torch.int64),
-                             max=pool - 1)
-        # strata are disjoint and increasing: distinct and sorted
-        cols_d = torch.arange(pool, n, device=device, dtype=torch.int64).expand(m, nd)
-        colind = torch.cat([cols_r, cols_d], dim=1).to(torch.int32).reshape(-1)
-        val = torch.randn(m, nnz_row, generator=gen, **f64)
-        val[:, nr:] *= cfg["dense_scale"]
-        rowptr = torch.arange(m + 1, device=device, dtype=torch.int64) * nnz_row
-        b = torch.randn(m, generator=gen, **f64)
-        meta.update(nnz=m * nnz_row, dense_cols=nd)
-        return Problem(name, m, n, "csr", cfg["gamma"], cfg["lam"], b,
-                       rowptr=rowptr, colind=colind, val=val.reshape(-1), meta=meta)
-    else:
-        raise ValueError(f"unknown spectrum/kind for {name}")
-    if cfg["rhs"] == "model":
-        x0 = torch.randn(n, generator=gen, **f64)
-        if m >= n:
-            b = X @ x0
-        else:
-            b = X.T @ x0
-        b = b + 1e-3 * torch.randn(m, generator=gen, **f64)
-    else:
-        b = torch.randn(m, generator=gen, **f64)
-    return Problem(name, m, n, "dense", cfg["gamma"], cfg["lam"], b, X=X.contiguous(),
-                   x0=x0, meta=meta)
+        strata = torch.arange(nr, **f64) * width
+        cols_d = torch.arange(pool, n, device=device, dtype=torch.int64)
+        rows = hi - lo
+        colind = torch.empty(rows, nnz_row, dtype=torch.int32, device=device)
+        val = torch.empty(rows, nnz_row, **f64)
+        b = torch.empty(rows, **f64)
+        for g in blocks:
+            g0, g1 = g * BLOCK, min(L, (g + 1) * BLOCK)
+            gen = _block_gen(seed, g, device)
+            u = torch.rand(g1 - g0, nr, generator=gen, **f64)
+            cr = torch.clamp((strata + u * width).floor().to(torch.int64), max=pool - 1)
+            # one draw per disjoint increasing stratum: distinct and sorted
+            ci = torch.cat([cr, cols_d.expand(g1 - g0, nd)], dim=1).to(torch.int32)
+            vv = torch.randn(g1 - g0, nnz_row, generator=gen, **f64)
+            vv[:, nr:] *= cfg["dense_scale"]
+            bb = torch.randn(g1 - g0, generator=gen, **f64)
+            a0, a1 = max(g0, lo), min(g1, hi)
+            colind[a0 - lo:a1 - lo] = ci[a0 - g0:a1 - g0]
+            val[a0 - lo:a1 - lo] = vv[a0 - g0:a1 - g0]
+            b[a0 - lo:a1 - lo] = bb[a0 - g0:a1 - g0]
+        rowptr = torch.arange(rows + 1, device=device, dtype=torch.int64) * nnz_row
+        meta.update(nnz=rows * nnz_row, dense_cols=nd)
+        return Problem(name, m, n, "csr", cfg["gamma"], cfg["lam"], b, rowptr=rowptr,
+                       colind=colind.reshape(-1), val=val.reshape(-1), meta=meta)
+    raise ValueError(f"unknown spectrum/kind for {name}")
 
 
 def small(name, device="cpu"):

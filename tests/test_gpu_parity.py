@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (north star):
+  G entries            |G_gpu - G_orc| <= 8 ulp-ish: 2e-15 * max(1, |G|) (K1 uses CUDA log/sincospi)
+  sketch               relative Frobenius <= 1e-12
+  x (LSQR, CS)         relative 2-norm <= max(1e-9, 20 kappa_+ u)   (reading C18)
+                       and ||A(x_gpu - x_orc)|| <= 1e-11 ||A x_orc||  (Thm 4.5 A-norm form)
+  iteration counts     identical (predictable LSQR, CS); adaptive LSQR within +-2 (reading C5)
+  rank r               identical
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import brute
+from oracle.gaussian import gaussian
+from oracle.lsrn import solve as orc_solve
+from oracle.sketch import plan as orc_plan
+from oracle.sketch import sketch as orc_sketch
+from synth.generate import make_problem, small
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1109_5981_b200 import lsrn
+    c = lsrn.Context()
+    yield c
+    c.close()
+
+
+def _relfro(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_gaussian_entries(ctx):
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, 50000, 4000)
+    cols = rng.integers(0, 2 ** 40, 4000)
+    cols[:10] = np.arange(10)
+    rows[:10] = np.arange(10)
+    seed = 0xDEADBEEF12345
+    got = ctx.debug_gaussian(seed, torch.from_numpy(rows), torch.from_numpy(cols)).cpu().numpy()
+    ref = np.array([gaussian(seed, [i], [j])[0, 0] for i, j in zip(rows, cols)])
+    err = np.abs(got - ref) / np.maximum(1.0, np.abs(ref))
+    assert err.max() <= 2e-15, err.max()
+
+
+@pytest.mark.parametrize("m,n,gamma,lam,ld_pad", [
+    (2000, 100, 2.0, 0.0, 0),       # c1 shape
+    (5000, 300, 2.0, 0.0, 0),       # several M/N tiles, ragged N tail
+    (777, 37, 1.5, 0.0, 0),         # odd k, s = 56, ragged K tail
+    (1000, 33, 2.1, 0.0, 1),        # odd s = 70, ld = 34 padded ... ld even
+    (1000, 33, 2.0, 0.0, 2),        # ld = 35 odd -> 8-byte path
+    (3000, 64, 2.0, 0.25, 0),       # tall Tikhonov block
+])
+def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad):
+    g = torch.Generator().manual_seed(m * 7 + n)
+    Xfull = torch.randn(m, n + ld_pad, generator=g, dtype=torch.float64)
+    X = Xfull[:, :n]
+    At = ctx.sketch(X.cuda() if ld_pad == 0 else Xfull.cuda()[:, :n], m, n, gamma, lam, seed=5981).cpu().numpy()
+    p = orc_plan(m, n, gamma, lam)
+    ref = orc_sketch(X.numpy(), p["s"], 5981, p["sigma_x"], p["sigma_i"])
+    assert At.shape == ref.shape
+    assert _relfro(At, ref) <= 1e-12
+
+
+def test_sketch_wide_lambda(ctx):
+    p = small("c3")                               # 60 x 3000, X = A^T (3000 x 60)
+    lam = 1e-3
+    At = ctx.sketch(p.X.cuda(), p.m, p.n, 2.0, lam).cpu().numpy()
+    pl = orc_plan(p.m, p.n, 2.0, lam)
+    ref = orc_sketch(p.X.numpy(), pl["s"], 5981, pl["sigma_x"], pl["sigma_i"])
+    assert _relfro(At, ref) <= 1e-12
+
+
+def test_sketch_shards_sum_to_full(ctx):
+    """Row shards with global Philox indices sum to the full sketch (multi-GPU invariant)."""
+    m, n = 4100, 90
+    X = torch.randn(m, n, dtype=torch.float64, device="cuda")
+    full = ctx.sketch(X, m, n, 2.0, 0.5).cpu().numpy()
+    bounds = [0, 1000, 1001, 2600, m]
+    acc = np.zeros_like(full)
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        acc += ctx.sketch(X[lo:hi], m, n, 2.0, 0.5, lo=lo, cnt=hi - lo).cpu().numpy()
+    assert _relfro(acc, full) <= 1e-13
+
+
+def _x_tol(kappa):
+    return max(1e-9, 20.0 * kappa * U)
+
+
+def _check_solution(A, x_gpu, x_orc, kappa):
+    rel = np.linalg.norm(x_gpu - x_orc) / np.linalg.norm(x_orc)
+    assert rel <= _x_tol(kappa), rel
+    an = np.linalg.norm(A @ (x_gpu - x_orc)) / np.linalg.norm(A @ x_orc)
+    assert an <= 1e-11, an
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_solve_c1(ctx, solver):
+    p = make_problem("c1")
+    A = p.X.numpy()
+    b = p.b.numpy()
+    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver=solver)
+    orc = orc_solve(A, b, solver=solver, extended=True)
+    assert rep["r"] == orc["r"] == 100 and rep["s"] == orc["s"] == 200
+    assert rep["iters"] == orc["iters"] == (96 if solver == "lsqr" else 133)
+    _check_solution(A, x.cpu().numpy(), orc["x"], p.meta["kappa"])
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_solve_small_configs(ctx, solver, name):
+    p = small(name)
+    A = p.dense_A().numpy()
+    b = p.b.numpy()
+    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver=solver, lam=p.lam)
+    orc = orc_solve(A, b, solver=solver, lam=p.lam)
+    assert rep["r"] == orc["r"] and rep["s"] == orc["s"]
+    assert rep["iters"] == orc["iters"]
+    sv = np.linalg.svd(A, compute_uv=False)
+    kappa = sv[0] / sv[sv > sv[0] * 1e-12][-1]
+    _check_solution(A if p.lam == 0 else np.vstack([A, p.lam * np.eye(p.n)]) if p.tall else A,
+                    x.cpu().numpy(), orc["x"], kappa)
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+@pytest.mark.parametrize("shape,r,lam", [((400, 20), 20, 0.0), ((400, 20), 13, 0.0), ((20, 400), 9, 0.0),
+                                         ((300, 15), 15, 1e-2), ((15, 300), 15, 1e-2)])
+def test_solve_tiny_vs_brute_force(ctx, solver, shape, r, lam):
+    rng = np.random.default_rng(r)
+    m, n = shape
+    U_, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    V_, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    A = (U_ * np.logspace(0, -3, r)) @ V_.T
+    b = rng.standard_normal(m)
+    X = torch.from_numpy(A if m >= n else np.ascontiguousarray(A.T)).cuda()
+    x, rep = ctx.solve(X, torch.from_numpy(b).cuda(), m, n, solver=solver, lam=lam)
+    ref = brute.ridge(A, b, lam) if lam > 0 else brute.min_length(A, b)[0]
+    assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-9 * np.linalg.norm(ref)
+    orc = orc_solve(A, b, solver=solver, lam=lam)
+    assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
+
+
+def test_b_zero_and_errors(ctx):
+    from paper_1109_5981_b200.lsrn import LsrnError
+    p = small("c5")
+    X = p.X.cuda()
+    z = torch.zeros(p.m, dtype=torch.float64, device="cuda")
+    x, rep = ctx.solve(X, z, p.m, p.n, solver="lsqr")
+    assert rep["iters"] == 0 and not torch.any(x)
+    x, rep = ctx.solve(X, z, p.m, p.n, solver="cs")
+    assert not torch.any(x)
+    with pytest.raises(LsrnError, match="EINVAL"):
+        ctx.solve(X, p.b.cuda(), p.m, p.n, gamma=1.0)
+    with pytest.raises(LsrnError, match="EINVAL"):
+        ctx.solve(X, p.b.cuda(), p.m, p.n, tol=1.5)
+    with pytest.raises(LsrnError, match="ERANK0"):
+        ctx.solve(torch.zeros_like(X), p.b.cuda(), p.m, p.n)
+
+
+def test_adaptive_lsqr(ctx):
+    p = small("c2")
+    A = p.X.numpy()
+    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="lsqr", mode="adaptive")
+    orc = orc_solve(A, p.b.numpy(), solver="lsqr", mode="adaptive")
+    assert rep["converged"] == 1 and orc["converged"]
+    assert abs(rep["iters"] - orc["iters"]) <= 2
+    assert rep["iters"] <= 2 * orc["lsqr_count"]
+    rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
+    assert rel <= 1e-8
+
+
+def test_host_io_matches_device(ctx):
+    p = small("c5")
+    xd, repd = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs")
+    xh, reph = ctx.solve(p.X.pin_memory(), p.b.pin_memory(), p.m, p.n, solver="cs", host_io=True)
+    assert torch.equal(xd.cpu(), xh)
+    assert repd["iters"] == reph["iters"]
+
+
+def test_repeat_solves_bitwise(ctx):
+    p = small("c2")
+    x1, _ = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="lsqr")
+    x2, _ = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="lsqr")
+    assert torch.equal(x1, x2)
