@@ -171,6 +171,7 @@ def main():
     import torch
     import torch.distributed as dist
 
+    from paper_1109_5981_b200 import dist as lsrn_dist
     from paper_1109_5981_b200 import lsrn
     from synth.generate import CONFIGS, SKETCH_SEED, make_problem
 
@@ -185,18 +186,12 @@ def main():
     cfg = CONFIGS[args.config]
     m, n = cfg["m"], cfg["n"]
     L = max(m, n)
-    lo = (L * rank) // world
-    hi = (L * (rank + 1)) // world
+    lo, hi = lsrn_dist.shard_bounds(L, world, rank)
     p = make_problem(args.config, device=dev, shard=(lo, hi) if world > 1 else None)
     X, b = p.X, p.b
-    nid = None
-    if world > 1:
-        obj = [lsrn.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
     stream = torch.cuda.Stream(dev)
     torch.cuda.synchronize()
-    ctx = lsrn.Context(stream=stream, nranks=world, rank=rank, nccl_id=nid)
+    ctx = lsrn_dist.context(stream=stream)
     ctx.set_profiling(True)
     kw = dict(solver=args.solver, gamma=cfg["gamma"], lam=cfg["lam"], tol=1e-14, seed=SKETCH_SEED, lo=lo,
               cnt=hi - lo)
@@ -216,6 +211,7 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     reps, stats = [], []
+    torch.cuda.nvtx.range_push("lsrn_step")
     with torch.cuda.stream(stream):
         e0.record(stream)
         for _ in range(args.steps):
@@ -223,6 +219,7 @@ def main():
             reps.append(rep)
             stats.append(ctx.stats())
         e1.record(stream)
+    torch.cuda.nvtx.range_pop()
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
@@ -248,7 +245,7 @@ def main():
     sketch_flops = 2.0 * s_ * k * cnt
     peaks, peak_src = load_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    lp_bytes = cnt * k * 8.0 + 3 * 8.0 * cnt     # A once + z read/write + (b-side) stream
+    lp_bytes = cnt * (8.0 * k + 16.0)            # per row: the row of A once + u_j read and write
     sketch_tf = sketch_flops / (sk_ms * 1e-3) / 1e12
     lp_gbs = lp_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None
     iters = reps[-1]["iters"]
@@ -261,7 +258,7 @@ def main():
                    "peak_source": FP64_PEAK_NOTE, "share_of_step": sketch_share}
     roof_lp = {"kernel": "rowpass_kernel long pass (K6)", "bound": "hbm", "achieved": lp_gbs, "peak": hbm_peak,
                "unit": "GB/s", "frac": (lp_gbs / hbm_peak) if lp_gbs else None, "traffic": None,
-               "algorithmic": f"8*(L*k + 3L) = {lp_bytes:.4g} B per launch",
+               "algorithmic": f"rows*(8k+16) = {lp_bytes:.4g} B per launch",
                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", "share_of_step": lp_share}
     roofline = roof_sketch if sketch_share >= lp_share else roof_lp
 

@@ -44,9 +44,15 @@ struct RowPassArgs {
 struct RowPassPlan {
   int vpt, cl, tr, nclusters, vec;  // vec: 2 = 16-byte loads
   int64_t rows_per_cluster;
+  int bulk = 0;                     // 1: rowpass_bulk_kernel (TMA bulk-copy ring)
+  int64_t cq = 0;                   // bulk: columns per CTA slice
+  int nst = 0;                      // bulk: pipeline stages
 };
-RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm);
+// allow_bulk = false forces the register-load kernel (tests compare both)
+RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, bool allow_bulk = true);
 cudaError_t launch_rowpass(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st);
+bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, RowPassPlan* p);
+cudaError_t launch_rowpass_bulk(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st);
 
 // Column reduce of the row-pass partials (+ optional Tikhonov identity block):
 //   w_c = sum_g wpart[g][c];  if zI: zI_c <- c1 zI_c + c2 sI t_c,  w_c += sI zI_c

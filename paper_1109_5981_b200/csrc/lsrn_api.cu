@@ -345,10 +345,10 @@ struct Pass {
       a.done = done;
       a.wpart = w.wpart;
       a.npart = w.npart;
-      if (prof) LSRN_CUDA(cudaEventRecord(c->pass_ev[idx], st));
+      if (prof) LSRN_CUDA(cudaEventRecordWithFlags(c->pass_ev[idx], st, cudaEventRecordExternal));
       LSRN_CUDA(launch_rowpass(a, plong, st));
       if (prof) {
-        LSRN_CUDA(cudaEventRecord(c->pass_ev[idx + 1], st));
+        LSRN_CUDA(cudaEventRecordWithFlags(c->pass_ev[idx + 1], st, cudaEventRecordExternal));
         c->n_pass_ev += 2;
       }
       c->launches++;

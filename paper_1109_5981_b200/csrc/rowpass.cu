@@ -214,8 +214,9 @@ cudaError_t launch_colreduce(const ColReduceArgs& a, cudaStream_t st) {
 }
 
 // --------------------------------------------------------------- planning
-RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm) {
+RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, bool allow_bulk) {
   RowPassPlan p{};
+  if (allow_bulk && plan_rowpass_bulk(R, C, ld, Y, nsm, &p)) return p;
   p.vec = ((ld % 2) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0) ? 2 : 1;
   if (C <= 512) p.vpt = 1;
   else if (C <= 1024) p.vpt = 2;
@@ -257,6 +258,7 @@ static cudaError_t launch_t(const RowPassArgs& a, const RowPassPlan& p, cudaStre
 }
 
 cudaError_t launch_rowpass(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  if (p.bulk) return launch_rowpass_bulk(a, p, st);
   if (p.cl > 16) return cudaErrorInvalidValue;
   if (p.vec == 2) {
     switch (p.vpt) {

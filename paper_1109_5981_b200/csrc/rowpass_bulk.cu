@@ -1,0 +1,304 @@
+// K5 / K6 on the TMA bulk-copy engine: the fused single-pass matvec of
+// rowpass.cu, with the rows of Y streamed into a shared-memory ring by
+// cp.async.bulk (1-D TMA) and mbarrier completion instead of per-thread loads.
+//
+// Same contract as rowpass_kernel (kernels.h RowPassArgs): for every row j
+//     z_j <- c1 z_j + c2 sx (Y_j . t);  acc_j += ca z_j;  norm2 += z_j^2;  w += sx Y_j z_j.
+// The paper counts flops(Av) + flops(A^T u) per iteration; this
+// pass reads each row of A (or N^T) from HBM exactly once.
+//
+// Why bulk copies: the pass is HBM-bound and needs ~40 KB in flight per SM to
+// cover DRAM latency at 6.5 TB/s.  Per-thread 16-byte loads kept only one row
+// tile (32 KB) in flight and reached ~48 % of the measured copy bandwidth
+// (profiles/r01_ncu_full_sketch_rowpass.json).  Here one elected thread keeps
+// NST - 1 stages of TR rows (32-64 KB each) in flight while the CTA reduces the
+// current stage out of shared memory.
+//
+// Layout: cluster g owns a contiguous chunk of rows; CTA q of the cluster owns
+// the column slice [q Cq, (q+1) Cq) (Cq <= 4096 doubles = 32 KB); thread tid owns
+// columns 2 (tid + 256 p) + {0, 1} of the slice, p < P, and keeps t and w for
+// them in registers.  Partial row dots of the cluster's CTAs are exchanged
+// through distributed shared memory (one cluster barrier per stage).
+// Deterministic: fixed row chunks and reduction trees, no atomics.
+#include <algorithm>
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace lsrn {
+
+namespace {
+
+LSRN_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+LSRN_DEV void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+LSRN_DEV void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+LSRN_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> this CTA's shared memory, completion on `bar`.
+LSRN_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int THREADS = 256;
+constexpr int NWARP = THREADS / 32;
+constexpr int kMaxStages = 8;
+
+}  // namespace
+
+// TR rows per stage; P column pairs per thread (slice width <= 512 P).
+template <int P, int TR>
+__global__ void __launch_bounds__(THREADS, 1)
+rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq, int nst) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kMaxStages];
+  __shared__ double red[2][NWARP][TR];
+  __shared__ double xs[2][16][TR];
+  if (a.done != nullptr && *a.done != 0) return;     // uniform over the grid
+
+  const int q = (CL > 1) ? (int)cg::this_cluster().block_rank() : 0;
+  const int64_t g = blockIdx.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t C = a.C;
+  const int64_t c0 = (int64_t)q * Cq;
+  const int64_t ncol = max((int64_t)0, min(Cq, C - c0));       // this CTA's slice width (even)
+  const unsigned row_bytes = (unsigned)(ncol * 8);
+  const int64_t stage_ld = Cq;                                   // doubles per staged row
+  double* stage = reinterpret_cast<double*>(smem_raw);           // [nst][TR][stage_ld]
+
+  const double c1 = a.coef[0], c2 = a.coef[1] * a.sx;
+  const double ca = (a.acc != nullptr) ? a.coef[2] : 0.0;
+
+  const int64_t r0 = g * rows_per_cluster;
+  const int64_t r1 = min(a.R, r0 + rows_per_cluster);
+  const int64_t ntiles = (r1 > r0) ? (r1 - r0 + TR - 1) / TR : 0;
+
+  auto issue = [&](int64_t tile) {     // one thread: stage tile % nst <- rows of `tile`
+    const int st = (int)(tile % nst);
+    const int64_t rb = r0 + tile * TR;
+    const int nr = (int)min((int64_t)TR, r1 - rb);
+    if (row_bytes == 0) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&full[st])) : "memory");
+      return;
+    }
+    mbar_arrive_expect_tx(&full[st], row_bytes * (unsigned)nr);
+    for (int tr = 0; tr < nr; ++tr)
+      bulk_g2s(stage + ((int64_t)st * TR + tr) * stage_ld, a.Y + (rb + tr) * a.ld + c0, row_bytes, &full[st]);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int64_t t = 0; t < min((int64_t)nst, ntiles); ++t) issue(t);
+  }
+
+  double2 tv[P], wv[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int64_t cl = 2 * (tid + THREADS * p);
+    const int64_t c = c0 + cl;
+    tv[p].x = (cl < ncol) ? a.t[c] : 0.0;
+    tv[p].y = (cl + 1 < ncol) ? a.t[c + 1] : 0.0;
+    wv[p] = make_double2(0.0, 0.0);
+  }
+
+  double norm = 0.0;
+  int buf = 0;
+  for (int64_t tile = 0; tile < ntiles; ++tile) {
+    const int st = (int)(tile % nst);
+    const unsigned parity = (unsigned)((tile / nst) & 1);
+    const int64_t rb = r0 + tile * TR;
+    double zo[TR];
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr) zo[tr] = (rb + tr < r1) ? a.z[rb + tr] : 0.0;
+    mbar_wait(&full[st], parity);
+
+    double2 y[TR][P];
+    double d[TR];
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr) {
+      const double* row = stage + ((int64_t)st * TR + tr) * stage_ld;
+      const bool rok = rb + tr < r1;
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int64_t cl = 2 * (tid + THREADS * p);
+        y[tr][p] = (rok && cl < ncol) ? *reinterpret_cast<const double2*>(row + cl) : make_double2(0.0, 0.0);
+        s = fma(y[tr][p].x, tv[p].x, fma(y[tr][p].y, tv[p].y, s));
+      }
+      d[tr] = s;
+    }
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr) {
+      const double s = warp_sum(d[tr]);
+      if (lane == 0) red[buf][warp][tr] = s;
+    }
+    __syncthreads();                       // stage st fully read; partial dots visible
+    if (tid == 0 && tile + nst < ntiles) issue(tile + nst);
+    double dot[TR];
+    if (CL > 1) {
+      cg::cluster_group cluster = cg::this_cluster();
+      if (tid < TR) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) s += red[buf][w][tid];
+        for (int rr = 0; rr < CL; ++rr) *cluster.map_shared_rank(&xs[buf][q][tid], rr) = s;
+      }
+      cluster.sync();
+#pragma unroll
+      for (int tr = 0; tr < TR; ++tr) {
+        double s = 0.0;
+        for (int qq = 0; qq < CL; ++qq) s += xs[buf][qq][tr];
+        dot[tr] = s;
+      }
+    } else {
+#pragma unroll
+      for (int tr = 0; tr < TR; ++tr) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NWARP; ++w) s += red[buf][w][tr];
+        dot[tr] = s;
+      }
+    }
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr) {
+      const int64_t row = rb + tr;
+      double zn = 0.0;
+      if (row < r1) {
+        zn = fma(c1, zo[tr], c2 * dot[tr]);
+        norm = fma(zn, zn, norm);
+        if (q == 0 && tid == 0) {
+          a.z[row] = zn;
+          if (a.acc != nullptr) a.acc[row] = fma(ca, zn, a.acc[row]);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        wv[p].x = fma(y[tr][p].x, zn, wv[p].x);
+        wv[p].y = fma(y[tr][p].y, zn, wv[p].y);
+      }
+    }
+    buf ^= 1;
+  }
+  double* wp = a.wpart + g * C;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int64_t cl = 2 * (tid + THREADS * p);
+    if (cl < ncol) wp[c0 + cl] = a.sx * wv[p].x;
+    if (cl + 1 < ncol) wp[c0 + cl + 1] = a.sx * wv[p].y;
+  }
+  if (q == 0 && tid == 0) a.npart[g] = norm;
+  if (CL > 1) cg::this_cluster().sync();   // keep smem alive until remote stores land
+}
+
+// ------------------------------------------------------------------ planning
+namespace {
+constexpr int64_t kMaxSlice = 4096;        // doubles per CTA slice (32 KB per staged row)
+constexpr size_t kStageBudget = 192 * 1024;
+}  // namespace
+
+bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, RowPassPlan* p) {
+  // 16-byte aligned rows and an even slice width: every bulk copy is a multiple of 16 bytes
+  if (C <= 0 || (C & 1) || (ld & 1) || (reinterpret_cast<uintptr_t>(Y) & 15)) return false;
+  int cl = (int)((C + kMaxSlice - 1) / kMaxSlice);
+  if (cl > 16) return false;
+  int64_t cq = (C + cl - 1) / cl;
+  cq = (cq + 1) & ~int64_t(1);
+  int vpt = 1;
+  while (512 * vpt < cq) vpt *= 2;
+  int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8 / vpt, 32768 / (cq * 8)));
+  int t2 = 1;
+  while (t2 * 2 <= tr) t2 *= 2;
+  tr = t2;
+  const size_t stage_bytes = (size_t)tr * cq * 8;
+  int nst = (int)std::min<size_t>(kMaxStages, kStageBudget / stage_bytes);
+  if (nst < 2) return false;
+  int nclusters = nsm / cl;
+  if (nclusters < 1) nclusters = 1;
+  const int64_t tiles = (R + tr - 1) / tr;
+  if ((int64_t)nclusters > tiles) nclusters = (int)(tiles > 0 ? tiles : 1);
+  p->vpt = vpt;
+  p->cl = cl;
+  p->tr = tr;
+  p->nclusters = nclusters;
+  p->vec = 2;
+  p->rows_per_cluster = std::max<int64_t>(1, (R + nclusters - 1) / nclusters);
+  p->bulk = 1;
+  p->cq = cq;
+  p->nst = nst;
+  return true;
+}
+
+template <int P, int TR>
+static cudaError_t launch_bulk_t(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  const size_t smem = (size_t)p.nst * TR * p.cq * 8;
+  cudaError_t e = cudaFuncSetAttribute(rowpass_bulk_kernel<P, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  if (p.cl > 8) {
+    e = cudaFuncSetAttribute(rowpass_bulk_kernel<P, TR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.nclusters * p.cl));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)p.cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, rowpass_bulk_kernel<P, TR>, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
+}
+
+// only P * TR <= 8 is planned (the row tile lives in registers: 2 P TR doubles per thread)
+template <int P>
+static cudaError_t launch_bulk_p(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  if constexpr (P * 8 <= 8) { if (p.tr == 8) return launch_bulk_t<P, 8>(a, p, st); }
+  if constexpr (P * 4 <= 8) { if (p.tr == 4) return launch_bulk_t<P, 4>(a, p, st); }
+  if constexpr (P * 2 <= 8) { if (p.tr == 2) return launch_bulk_t<P, 2>(a, p, st); }
+  if (p.tr == 1) return launch_bulk_t<P, 1>(a, p, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_rowpass_bulk(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  switch (p.vpt) {
+    case 1: return launch_bulk_p<1>(a, p, st);
+    case 2: return launch_bulk_p<2>(a, p, st);
+    case 4: return launch_bulk_p<4>(a, p, st);
+    default: return launch_bulk_p<8>(a, p, st);
+  }
+}
+
+}  // namespace lsrn

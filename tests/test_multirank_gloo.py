@@ -1,0 +1,130 @@
+"""The N > 1 decomposition on CPU: world_size-2 gloo process groups.
+
+The GPU path shards the long dimension (§4.3): rank p sketches its
+rows with GLOBAL Philox indices, the partial sketches are allreduced, and each
+iteration does local long passes plus one allreduce of the short vector.  These
+tests run that decomposition with gloo collectives on the oracle's arithmetic
+and check it against the single-process oracle, and they exercise the host-side
+plumbing of paper_1109_5981_b200.dist (shard bounds, NCCL-id exchange).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1109_5981_b200.dist import exchange_unique_id, shard_bounds
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(fn, world=2):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_entry, args=(fn, r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = [q.get() for _ in range(world)]
+    for r in res:
+        assert r[1] == "ok", r
+    return sorted(res)
+
+
+def _entry(fn, rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        fn(rank, world)
+        q.put((rank, "ok"))
+    except Exception as ex:  # report to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,world", [(10, 3), (7, 7), (0, 2), (100_000, 8), (5, 8)])
+def test_shard_bounds_partition(L, world):
+    b = [shard_bounds(L, world, r) for r in range(world)]
+    assert b[0][0] == 0 and b[-1][1] == L
+    for (lo, hi), (lo2, _) in zip(b, b[1:]):
+        assert hi == lo2 and hi >= lo
+    sizes = [hi - lo for lo, hi in b]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def _id_exchange(rank, world):
+    got = exchange_unique_id(lambda: bytes(range(rank, rank + 128)))
+    assert got == bytes(range(0, 128)), got[:4]
+
+
+def test_unique_id_exchange_gloo():
+    _run(_id_exchange)
+
+
+def _sketch_shards(rank, world):
+    from oracle.gaussian import gaussian_block
+    from oracle.sketch import sketch
+    rng = np.random.default_rng(3)
+    L, k, s, seed = 1001, 13, 26, 5981
+    X = rng.standard_normal((L, k))
+    lo, hi = shard_bounds(L, world, rank)
+    part = gaussian_block(seed, 0, s, lo, hi) @ X[lo:hi]           # global indices j = lo..hi-1
+    t = torch.from_numpy(part)
+    dist.all_reduce(t)
+    full = sketch(X, s, seed)
+    err = np.linalg.norm(t.numpy() - full) / np.linalg.norm(full)
+    assert err <= 1e-13, err
+
+
+def test_sharded_sketch_allreduce_equals_full():
+    _run(_sketch_shards)
+
+
+def _cs_shards(rank, world):
+    """Alg. 3 with row-sharded A N: local products + one allreduce per pass."""
+    from oracle import bounds
+    from oracle.krylov import chebyshev, cs_schedule
+    from oracle.precond import factor
+    from oracle.sketch import sketch
+    rng = np.random.default_rng(5)
+    m, n = 900, 20
+    A = rng.standard_normal((m, n)) * np.logspace(0, -3, n)
+    b = rng.standard_normal(m)
+    s = 40
+    N, _, r = factor(sketch(A, s, 5981))
+    sl, su = bounds.sigma_bounds(s, r, bounds.default_alpha(s))
+    passes = bounds.cs_passes(sl, su, 1e-14)
+    ref = N @ chebyshev(lambda y: A @ (N @ y), lambda u: N.T @ (A.T @ u), b, sl, su, passes)
+    lo, hi = shard_bounds(m, world, rank)
+    Ap, rp = A[lo:hi], b[lo:hi].copy()
+    d = (su ** 2 + sl ** 2) / 2.0
+    c = (su ** 2 - sl ** 2) / 2.0
+    v = np.zeros(r)
+    y = np.zeros(r)
+    for beta, alpha in cs_schedule(d, c, passes):
+        w = torch.from_numpy(Ap.T @ rp)          # local long pass
+        dist.all_reduce(w)                       # the one collective per pass
+        v = beta * v + N.T @ w.numpy()
+        y = y + alpha * v
+        rp = rp - alpha * (Ap @ (N @ v))
+    x = N @ y
+    err = np.linalg.norm(x - ref) / np.linalg.norm(ref)
+    assert err <= 1e-10, err
+
+
+def test_sharded_chebyshev_allreduce_equals_single_process():
+    _run(_cs_shards)
