@@ -212,6 +212,7 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     reps, stats = [], []
     torch.cuda.nvtx.range_push("lsrn_step")
+    torch.cuda.profiler.start()      # ncu --profile-from-start off captures only the timed steps
     with torch.cuda.stream(stream):
         e0.record(stream)
         for _ in range(args.steps):
@@ -219,6 +220,7 @@ def main():
             reps.append(rep)
             stats.append(ctx.stats())
         e1.record(stream)
+    torch.cuda.profiler.stop()
     torch.cuda.nvtx.range_pop()
     barrier()
     clk = clocks.stop()

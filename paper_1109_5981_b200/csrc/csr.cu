@@ -1,0 +1,468 @@
+// K4 (CSR sketch) and the CSR long pass (K6-CSR) for sparse tall A.
+//
+// The paper notes that LSRN "automatically speeds up when A is sparse" because
+// it only touches A through products (Abstract; §4.1) and
+// ran a sparse, "far from optimized" threaded matvec (§6.5).
+//
+// Sketch Ã = G A for CSR A (Alg. 1 step 3) with G never stored.  The
+// cost is set by regenerating G, not by HBM: each G[i, j] is a
+// Philox call + half a Box-Muller pair (~40 FP64 ops), and a nonzero of row j
+// is used once per sketch row.  The shard is therefore split by column density:
+//   * heavy columns (density >= 1/32, at most 64 of them) are gathered into a
+//     dense cnt x ND block D and sketched row-stationary (csr_sketch_heavy):
+//     thread = sketch row i, G[i, j] generated ONCE per (i, j) and reused by all
+//     ND heavy columns of row j;
+//   * the remaining nonzeros are sketched column-stationary from a CSC copy
+//     (csr_sketch_light): thread = sketch row i, one G[i, j] per nonzero.
+// The two threads of a Box-Muller pair (rows 2q, 2q+1, C9) split its
+// work: the even lane computes rho = sqrt(-2 ln u1), the odd lane sincospi(2 u2),
+// and they swap halves with one shuffle.
+//
+// The CSC copy is built deterministically (per-chunk counts, exclusive scans,
+// in-order fill), so the sketch and the iterations are bitwise reproducible.
+//
+// Iteration (CSR long pass): u_j <- c1 u_j + c2 (A_j . t) from the CSR rows
+// (csr_rowdot, which also accumulates the heavy columns of w = A^T u per block),
+// then the light columns of w gathered column by column from the CSC copy
+// (csr_colgather); out = [w ; ||u||^2] like colreduce_kernel.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "philox_bm.cuh"
+
+namespace lsrn {
+
+namespace {
+constexpr int THR = 256;
+
+LSRN_DEV double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+  return t;   // valid in thread 0
+}
+
+// G[i, j] for the calling lane's sketch row i, lanes (2q, 2q+1) cooperating on
+// the pair.  All 32 lanes of the warp must call it (with their own i, j equal
+// within each lane pair).  Returns z_{i & 1}.
+LSRN_DEV double gaussian_lane(uint2 key, uint64_t q, uint64_t j, bool odd) {
+  const uint4 o = philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(j),
+                                           static_cast<uint32_t>(j >> 32), 0u), key);
+  double mine, other_cs = 0.0;
+  if (!odd) {
+    const double u1 = u53_from_words(o.x, o.y) + 0x1.0p-53;
+    mine = sqrt(-2.0 * log(u1));                 // rho
+  } else {
+    const double u2 = u53_from_words(o.z, o.w);
+    double sn, cs;
+    sincospi(2.0 * u2, &sn, &cs);
+    mine = sn;
+    other_cs = cs;
+  }
+  // even lane needs cos from its odd partner; odd lane needs rho from its even partner
+  const double send = odd ? other_cs : mine;
+  const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
+  return odd ? recv * mine : mine * recv;        // z1 = rho sin, z0 = rho cos
+}
+}  // namespace
+
+// ------------------------------------------------------------ CSC construction
+// cntc[chunk][c] = number of nonzeros of column c in rows [chunk*CH, (chunk+1)*CH)
+__global__ void csr_chunk_count_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                                       int64_t rows, int64_t k, int64_t CH, int* __restrict__ cntc) {
+  extern __shared__ int hist[];
+  const int64_t chunk = blockIdx.x;
+  for (int64_t c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  const int64_t r0 = chunk * CH, r1 = min(rows, r0 + CH);
+  const int64_t base = rowptr[0];
+  const int64_t e0 = rowptr[r0] - base, e1 = rowptr[r1] - base;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&hist[colind[e]], 1);   // integer: exact
+  __syncthreads();
+  int* out = cntc + chunk * k;
+  for (int64_t c = threadIdx.x; c < k; c += blockDim.x) out[c] = hist[c];
+}
+
+// per column: total[c] = sum_chunk cntc; offs[chunk][c] = exclusive prefix over chunks (relative)
+__global__ void csr_chunk_scan_kernel(const int* __restrict__ cntc, int64_t nchunks, int64_t k,
+                                      int64_t* __restrict__ offs, int64_t* __restrict__ total) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < k; c += (int64_t)gridDim.x * blockDim.x) {
+    int64_t run = 0;
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+      offs[ch * k + c] = run;
+      run += cntc[ch * k + c];
+    }
+    total[c] = run;
+  }
+}
+
+// colptr = exclusive scan of the light-column totals (heavy columns hold no CSC
+// entries: their values live in D).  Single CTA, sequential tiles of THR.
+__global__ void csr_colptr_kernel(const int64_t* __restrict__ total, const int* __restrict__ colmap, int64_t k,
+                                  int64_t* __restrict__ colptr) {
+  __shared__ int64_t sh[THR];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < k; t0 += THR) {
+    const int64_t c = t0 + threadIdx.x;
+    const int64_t v = (c < k && colmap[c] < 0) ? total[c] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < THR; off <<= 1) {      // Hillis-Steele inclusive scan
+      const int64_t add = (threadIdx.x >= off) ? sh[threadIdx.x - off] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (c < k) colptr[c] = carry + sh[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == THR - 1) carry += sh[THR - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) colptr[k] = carry;
+}
+
+// In-order fill of the CSC copy of the light columns (rowidx = local row, cval)
+// and of the heavy block D (rows x ld_d, zero-filled beforehand).  One CTA per chunk, one warp walking
+// the chunk's rows in order (distinct columns within a row -> no conflicts).
+__global__ void csr_fill_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                                const double* __restrict__ val, int64_t rows, int64_t k, int64_t CH,
+                                const int64_t* __restrict__ offs, const int64_t* __restrict__ colptr,
+                                const int* __restrict__ colmap, int32_t* __restrict__ rowidx,
+                                double* __restrict__ cval, double* __restrict__ D, int64_t ld_d) {
+  extern __shared__ int64_t cur[];
+  const int64_t chunk = blockIdx.x;
+  for (int64_t c = threadIdx.x; c < k; c += blockDim.x) cur[c] = colptr[c] + offs[chunk * k + c];
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int64_t base = rowptr[0];
+  const int64_t r1 = min(rows, (chunk + 1) * CH);
+  for (int64_t r = chunk * CH; r < r1; ++r) {
+    const int64_t e0 = rowptr[r] - base, e1 = rowptr[r + 1] - base;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int c = colind[e];
+      const double a = val[e];
+      const int h = colmap[c];
+      if (h >= 0) {
+        D[r * ld_d + h] = a;
+      } else {
+        const int64_t pos = cur[c]++;
+        rowidx[pos] = (int32_t)r;
+        cval[pos] = a;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------ K4 sketch kernels
+// Heavy part: part[split][i][h] = sum_{j in split} G[i, lo + j] D[j][h].
+template <int ND>
+__global__ void __launch_bounds__(THR)
+csr_sketch_heavy_kernel(const double* __restrict__ D, int64_t rows, int64_t lo, int64_t s, uint64_t seed,
+                        int64_t rows_per_split, double* __restrict__ part) {
+  constexpr int JT = 32;                       // D rows staged per step
+  __shared__ __align__(16) double Ds[JT][ND];
+  const uint2 key = philox_key(seed);
+  const int64_t i = (int64_t)blockIdx.x * THR + threadIdx.x;
+  const bool odd = (threadIdx.x & 1) != 0;
+  const uint64_t q = (uint64_t)(i >> 1);
+  const int64_t j0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t j1 = min(rows, j0 + rows_per_split);
+  double acc[ND];
+#pragma unroll
+  for (int h = 0; h < ND; ++h) acc[h] = 0.0;
+  for (int64_t jb = j0; jb < j1; jb += JT) {
+    const int nj = (int)min((int64_t)JT, j1 - jb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < JT * ND; e += THR) {
+      const int r = e / ND, h = e % ND;
+      Ds[r][h] = (r < nj) ? D[(jb + r) * ND + h] : 0.0;
+    }
+    __syncthreads();
+    for (int r = 0; r < nj; ++r) {
+      const double z = gaussian_lane(key, q, (uint64_t)(lo + jb + r), odd);
+#pragma unroll
+      for (int h = 0; h < ND; h += 2) {
+        const double2 d = *reinterpret_cast<const double2*>(&Ds[r][h]);
+        acc[h] = fma(z, d.x, acc[h]);
+        acc[h + 1] = fma(z, d.y, acc[h + 1]);
+      }
+    }
+  }
+  if (i < s) {
+    double* o = part + ((int64_t)blockIdx.y * s + i) * ND;
+#pragma unroll
+    for (int h = 0; h < ND; ++h) o[h] = acc[h];
+  }
+}
+
+// Light part: At[i][c] = sum_{(j, a) in CSC column c} G[i, lo + j] a for light columns.
+__global__ void __launch_bounds__(THR)
+csr_sketch_light_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                        const double* __restrict__ cval, const int* __restrict__ colmap, int64_t k, int64_t lo,
+                        int64_t s, uint64_t seed, int cols_per_cta, double* __restrict__ At) {
+  constexpr int NT = 256;                      // nonzeros staged per step
+  __shared__ int32_t js[NT];
+  __shared__ double as[NT];
+  const uint2 key = philox_key(seed);
+  const int64_t i = (int64_t)blockIdx.x * THR + threadIdx.x;
+  const bool odd = (threadIdx.x & 1) != 0;
+  const uint64_t q = (uint64_t)(i >> 1);
+  const int64_t cb = (int64_t)blockIdx.y * cols_per_cta;
+  for (int64_t c = cb; c < min(k, cb + cols_per_cta); ++c) {
+    if (colmap[c] >= 0) continue;              // heavy column: written by the heavy finish
+    const int64_t e0 = colptr[c], e1 = colptr[c + 1];
+    double acc = 0.0;
+    for (int64_t eb = e0; eb < e1; eb += NT) {
+      const int ne = (int)min((int64_t)NT, e1 - eb);
+      __syncthreads();
+      if (threadIdx.x < ne) {
+        js[threadIdx.x] = rowidx[eb + threadIdx.x];
+        as[threadIdx.x] = cval[eb + threadIdx.x];
+      }
+      __syncthreads();
+      for (int e = 0; e < ne; ++e) {
+        const double z = gaussian_lane(key, q, (uint64_t)(lo + js[e]), odd);
+        acc = fma(z, as[e], acc);
+      }
+    }
+    if (i < s) At[i * k + c] = acc;
+  }
+}
+
+// At[i][H[h]] = sum_split part[split][i][h]   (fixed split order)
+__global__ void csr_heavy_finish_kernel(const double* __restrict__ part, int nsplit, int64_t s, int nd, int ND,
+                                        const int* __restrict__ heavy_cols, int64_t k, double* __restrict__ At) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s * nd; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / nd;
+    const int h = (int)(e % nd);
+    double v = 0.0;
+    for (int p = 0; p < nsplit; ++p) v += part[((int64_t)p * s + i) * ND + h];
+    At[i * k + heavy_cols[h]] = v;
+  }
+}
+
+// At[i][c] += si G[i, L + c]  (tall Tikhonov block, §5)
+__global__ void sketch_add_gblock_kernel(double* __restrict__ At, int64_t s, int64_t k, int64_t L, double si,
+                                         uint64_t seed) {
+  const uint2 key = philox_key(seed);
+  const int64_t npair = (s + 1) / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npair * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qq = e / k, c = e % k;
+    double z0, z1;
+    gaussian_pair(key, (uint64_t)qq, (uint64_t)(L + c), z0, z1);
+    At[(2 * qq) * k + c] += si * z0;
+    if (2 * qq + 1 < s) At[(2 * qq + 1) * k + c] += si * z1;
+  }
+}
+
+// ------------------------------------------------------------ iteration kernels
+// u_j <- c1 u_j + c2 (A_j . t) (warp per row, contiguous row blocks per warp);
+// heavy columns h: wpart[block][h] = sum_j a_jh u_j (per-warp shared-memory
+// accumulators; the heavy columns of one row are distinct, so no two lanes hit
+// the same slot); npart[block] = partial ||u||^2.
+template <int ND>
+__global__ void __launch_bounds__(THR)
+csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                  const double* __restrict__ val, int64_t rows, const double* __restrict__ t,
+                  const int* __restrict__ colmap, const double* __restrict__ coef, double* __restrict__ u,
+                  double* __restrict__ npart, double* __restrict__ wpart, const int* __restrict__ done) {
+  __shared__ double sh[THR / 32];
+  __shared__ double wd[THR / 32][ND > 0 ? ND : 1];
+  if (done != nullptr && *done != 0) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * THR + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * THR) >> 5;
+  if (ND > 0)
+    for (int h = lane; h < ND; h += 32) wd[wib][h] = 0.0;
+  __syncwarp();
+  const double c1 = coef[0], c2 = coef[1];
+  const int64_t base = rowptr[0];
+  double nrm = 0.0;
+  const int64_t per = (rows + nwarps - 1) / nwarps;
+  const int64_t r0 = warp * per, r1 = min(rows, r0 + per);
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t e0 = rowptr[r] - base, e1 = rowptr[r + 1] - base;
+    double d = 0.0;
+    for (int64_t e = e0 + lane; e < e1; e += 32) d = fma(val[e], __ldg(t + colind[e]), d);
+    d = warp_sum(d);
+    const double un = fma(c1, u[r], c2 * d);
+    if (lane == 0) u[r] = un;
+    nrm = fma(un, un, nrm);
+    if (ND > 0) {
+      for (int64_t e = e0 + lane; e < e1; e += 32) {
+        const int h = colmap[colind[e]];
+        if (h >= 0) wd[wib][h] = fma(val[e], un, wd[wib][h]);
+      }
+      __syncwarp();
+    }
+  }
+  if (lane != 0) nrm = 0.0;
+  const double b = block_sum(nrm, sh);     // contains __syncthreads: wd complete
+  if (threadIdx.x == 0) npart[blockIdx.x] = b;
+  if (ND > 0) {
+    for (int h = threadIdx.x; h < ND; h += THR) {
+      double v = 0.0;
+      for (int w = 0; w < THR / 32; ++w) v += wd[w][h];
+      wpart[(int64_t)blockIdx.x * ND + h] = v;
+    }
+  }
+}
+
+// w_c = sum_{(j,a) in col c} a u_j (light columns: warp per column, lanes stride
+// the CSC column; heavy columns: the row pass's block partials);
+// Tikhonov block and ||u||^2 as in colreduce_kernel: out = [w ; ||u||^2 + ||zI||^2].
+__global__ void __launch_bounds__(THR)
+csr_colgather_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                     const double* __restrict__ cval, int64_t k, const double* __restrict__ u,
+                     const int* __restrict__ colmap, const double* __restrict__ wpart, int ND,
+                     const double* __restrict__ npart, int nparts, double* __restrict__ zI,
+                     const double* __restrict__ t, const double* __restrict__ coef, double sI,
+                     double* __restrict__ out, double* __restrict__ blockpart, unsigned* __restrict__ counter,
+                     const int* __restrict__ done) {
+  __shared__ double sh[THR / 32];
+  __shared__ bool last;
+  if (done != nullptr && *done != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = ((int64_t)blockIdx.x * THR + threadIdx.x) >> 5;
+  double nI = 0.0;
+  if (c < k) {
+    double w = 0.0;
+    const int h = colmap[c];
+    if (h >= 0) {          // heavy: fixed-order sum of the row-pass block partials
+      for (int g = lane; g < nparts; g += 32) w += wpart[(int64_t)g * ND + h];
+    } else {
+      for (int64_t e = colptr[c] + lane; e < colptr[c + 1]; e += 32) w = fma(cval[e], u[rowidx[e]], w);
+    }
+    w = warp_sum(w);
+    if (zI != nullptr) {
+      const double zn = fma(coef[0], zI[c], coef[1] * (sI * t[c]));
+      if (lane == 0) zI[c] = zn;
+      w = fma(sI, zn, w);
+      nI = (lane == 0) ? zn * zn : 0.0;
+    }
+    if (lane == 0) out[c] = w;
+  }
+  const double b = block_sum(nI, sh);
+  if (threadIdx.x == 0) {
+    blockpart[blockIdx.x] = b;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double n = 0.0;
+    for (int g = 0; g < nparts; ++g) n += __ldcg(npart + g);
+    for (unsigned bb = 0; bb < gridDim.x; ++bb) n += __ldcg(blockpart + bb);
+    out[k] = n;
+    *counter = 0u;
+  }
+}
+
+// ------------------------------------------------------------ host side
+int64_t csr_chunk_rows() { return 8192; }
+int64_t csr_nchunks(int64_t rows) { return rows > 0 ? (rows + csr_chunk_rows() - 1) / csr_chunk_rows() : 0; }
+int csr_rowdot_blocks(int nsm) { return nsm * 8; }
+int csr_colgather_blocks(int64_t k) { return (int)((k * 32 + THR - 1) / THR); }
+size_t csr_max_k() { return 24 * 1024; }     // CSC cursors (int64) of a chunk live in shared memory
+
+static unsigned grid_cap(int64_t n, int threads, int64_t cap) {
+  int64_t b = (n + threads - 1) / threads;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, cap));
+}
+
+cudaError_t launch_csr_build(const CsrBuildArgs& a, cudaStream_t st) {
+  const int64_t nch = csr_nchunks(a.rows);
+  const int64_t CH = csr_chunk_rows();
+  if (nch > 0) {
+    const size_t sh1 = sizeof(int) * (size_t)a.k;
+    cudaError_t e = cudaFuncSetAttribute(csr_chunk_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh1);
+    if (e != cudaSuccess) return e;
+    csr_chunk_count_kernel<<<(unsigned)nch, 512, sh1, st>>>(a.rowptr, a.colind, a.rows, a.k, CH, a.cntc);
+  }
+  csr_chunk_scan_kernel<<<grid_cap(a.k, 256, 4096), 256, 0, st>>>(a.cntc, nch, a.k, a.offs, a.total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_fill(const CsrBuildArgs& a, cudaStream_t st) {
+  const int64_t nch = csr_nchunks(a.rows);
+  csr_colptr_kernel<<<1, THR, 0, st>>>(a.total, a.colmap, a.k, a.colptr);
+  if (a.D != nullptr && a.rows > 0) {
+    cudaError_t e = cudaMemsetAsync(a.D, 0, sizeof(double) * (size_t)a.rows * a.ld_d, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (nch > 0) {
+    const size_t sh = sizeof(int64_t) * (size_t)a.k;
+    cudaError_t e = cudaFuncSetAttribute(csr_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
+    if (e != cudaSuccess) return e;
+    csr_fill_kernel<<<(unsigned)nch, 256, sh, st>>>(a.rowptr, a.colind, a.val, a.rows, a.k, csr_chunk_rows(), a.offs,
+                                                    a.colptr, a.colmap, a.rowidx, a.cval, a.D, a.ld_d);
+  }
+  return cudaGetLastError();
+}
+
+template <int ND>
+static void heavy_t(const CsrSketchArgs& a, dim3 grid, cudaStream_t st) {
+  csr_sketch_heavy_kernel<ND><<<grid, THR, 0, st>>>(a.D, a.rows, a.lo, a.s, a.seed, a.rows_per_split, a.part);
+}
+
+cudaError_t launch_csr_sketch(const CsrSketchArgs& a, cudaStream_t st, int nsm) {
+  const unsigned row_blocks = (unsigned)((a.s + THR - 1) / THR);
+  if (a.nd > 0) {
+    dim3 grid(row_blocks, (unsigned)a.nsplit);
+    switch (a.ND) {
+      case 16: heavy_t<16>(a, grid, st); break;
+      case 32: heavy_t<32>(a, grid, st); break;
+      default: heavy_t<64>(a, grid, st); break;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    csr_heavy_finish_kernel<<<grid_cap(a.s * a.nd, 256, (int64_t)nsm * 16), 256, 0, st>>>(
+        a.part, a.nsplit, a.s, a.nd, a.ND, a.heavy_cols, a.k, a.At);
+  }
+  const int cpc = 4;
+  dim3 g2(row_blocks, (unsigned)((a.k + cpc - 1) / cpc));
+  csr_sketch_light_kernel<<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.k, a.lo, a.s, a.seed, cpc,
+                                              a.At);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sketch_add_gblock(double* At, int64_t s, int64_t k, int64_t L, double si, uint64_t seed,
+                                     cudaStream_t st, int nsm) {
+  sketch_add_gblock_kernel<<<grid_cap(((s + 1) / 2) * k, 256, (int64_t)nsm * 16), 256, 0, st>>>(At, s, k, L, si,
+                                                                                              seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st) {
+  const unsigned nb = (unsigned)a.nblocks;
+#define LSRN_ROWDOT(ND_) csr_rowdot_kernel<ND_><<<nb, THR, 0, st>>>(a.rowptr, a.colind, a.val, a.rows, a.t, \
+      a.colmap, a.coef, a.u, a.npart, a.wpart, a.done)
+  switch (a.ND) {
+    case 0: LSRN_ROWDOT(0); break;
+    case 16: LSRN_ROWDOT(16); break;
+    case 32: LSRN_ROWDOT(32); break;
+    default: LSRN_ROWDOT(64); break;
+  }
+#undef LSRN_ROWDOT
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_colgather(const CsrGatherArgs& a, cudaStream_t st) {
+  csr_colgather_kernel<<<(unsigned)csr_colgather_blocks(a.k), THR, 0, st>>>(
+      a.colptr, a.rowidx, a.cval, a.k, a.u, a.colmap, a.wpart, a.ND, a.npart, a.nparts, a.zI, a.t, a.coef, a.sI,
+      a.out, a.blockpart,
+      a.counter, a.done);
+  return cudaGetLastError();
+}
+
+}  // namespace lsrn

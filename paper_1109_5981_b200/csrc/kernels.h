@@ -91,12 +91,95 @@ cudaError_t launch_lsqr_after_v(LsqrState* s, const double* comm, int64_t C, int
                                 const double* vstore, int64_t n, double* ypart, unsigned* counter,
                                 cudaStream_t st);
 
+// ---- K4 CSR sketch + CSR long pass (csr.cu)
+struct CsrBuildArgs {
+  const int64_t* rowptr;   // rows + 1 (rowptr[0] may be non-zero)
+  const int32_t* colind;
+  const double* val;
+  int64_t rows, k;
+  int* cntc;               // [nchunks][k]
+  int64_t* offs;           // [nchunks][k]
+  int64_t* total;          // [k]
+  const int* colmap;       // [k]: heavy index h >= 0, or -1 (light)
+  int64_t* colptr;         // [k + 1] (light columns only)
+  int32_t* rowidx;         // [nnz_light]
+  double* cval;            // [nnz_light]
+  double* D;               // [rows][ld_d] heavy block (nullable when no heavy column)
+  int64_t ld_d;
+};
+int64_t csr_chunk_rows();
+int64_t csr_nchunks(int64_t rows);
+int csr_rowdot_blocks(int nsm);
+int csr_colgather_blocks(int64_t k);
+size_t csr_max_k();
+cudaError_t launch_csr_build(const CsrBuildArgs& a, cudaStream_t st);   // counts + per-column totals
+cudaError_t launch_csr_fill(const CsrBuildArgs& a, cudaStream_t st);    // colptr + CSC + D (needs colmap)
+
+struct CsrSketchArgs {
+  const double* D;         // heavy block [rows][ND]
+  int64_t rows, lo, s, k;
+  uint64_t seed;
+  int nd, ND, nsplit;
+  int64_t rows_per_split;
+  double* part;            // [nsplit][s][ND]
+  const int* heavy_cols;   // [nd]
+  const int* colmap;
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  const double* cval;
+  double* At;              // s x k (row-major), fully written
+};
+cudaError_t launch_csr_sketch(const CsrSketchArgs& a, cudaStream_t st, int nsm);
+cudaError_t launch_sketch_add_gblock(double* At, int64_t s, int64_t k, int64_t L, double si, uint64_t seed,
+                                     cudaStream_t st, int nsm);
+
+struct CsrRowdotArgs {
+  const int64_t* rowptr;
+  const int32_t* colind;
+  const double* val;
+  int64_t rows;
+  const double* t;
+  const int* colmap;
+  const double* coef;
+  double* u;
+  double* npart;           // [nblocks]
+  double* wpart;           // [nblocks][ND]
+  const int* done;
+  int ND, nblocks;
+};
+cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st);
+
+struct CsrGatherArgs {
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  const double* cval;
+  int64_t k;
+  const double* u;
+  const int* colmap;
+  const double* wpart;
+  int ND;
+  const double* npart;
+  int nparts;
+  double* zI;              // nullable (Tikhonov identity block)
+  const double* t;
+  const double* coef;
+  double sI;
+  double* out;             // k + 1
+  double* blockpart;       // >= csr_colgather_blocks(k)
+  unsigned* counter;
+  const int* done;
+};
+cudaError_t launch_csr_colgather(const CsrGatherArgs& a, cudaStream_t st);
+
 // ---- misc (misc.cu)
 cudaError_t launch_fill(double* p, double v, int64_t n, cudaStream_t st);
 cudaError_t launch_copy_scale(double* dst, const double* src, double scale, int64_t n, cudaStream_t st);
 // row-major s x k -> column-major s x k
 cudaError_t launch_transpose(const double* src, int64_t rows, int64_t cols, double* dst, cudaStream_t st);
 // R (upper triangle of the k x k leading block of column-major QR, ld) -> dense k x k, zero below
+cudaError_t launch_build_jw(const double* qr, int64_t ld, int64_t k, double* JW, cudaStream_t st);
+cudaError_t launch_form_nt_jw(const double* E, int64_t lde, const double* ev, int64_t k, int64_t r, double* Nt,
+                              cudaStream_t st);
 cudaError_t launch_extract_r(const double* qr, int64_t ld, int64_t k, double* R, cudaStream_t st);
 // Nt[c][j] = VT[c + j * k] / S[c], c < r, j < k  (Nt row-major r x k == N column-major)
 cudaError_t launch_form_nt(const double* VT, const double* S, int64_t k, int64_t r, double* Nt,

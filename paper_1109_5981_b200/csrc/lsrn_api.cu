@@ -5,6 +5,7 @@
 // Paper map: Alg. 1 / Alg. 2 / Alg. 3 /
 // §5 Tikhonov / MPI design P:779-800 (Reduce -> here one NCCL
 // allreduce of the partial sketch; one allreduce per iteration).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -136,7 +137,13 @@ Dims make_dims(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, b
     LSRN_REQUIRE(A->ld >= d.k, LSRN_EDIM, "leading dimension ld must be >= min(m, n)");
     LSRN_REQUIRE(A->val != nullptr || d.cnt == 0, LSRN_EINVAL, "A->val is NULL");
   } else if (A->kind == LSRN_CSR) {
-    throw Fail{set_error(LSRN_EUNSUPPORTED, "CSR matrices are not supported by this build yet")};
+    LSRN_REQUIRE(d.tall, LSRN_EUNSUPPORTED, "CSR A must be tall (m >= n); pass a wide sparse A as its transpose");
+    LSRN_REQUIRE((size_t)d.k <= csr_max_k(), LSRN_EUNSUPPORTED,
+                 "CSR path supports n <= " + std::to_string(csr_max_k()) + " columns");
+    LSRN_REQUIRE(A->nnz >= 0, LSRN_EDIM, "nnz must be >= 0");
+    LSRN_REQUIRE(d.cnt == 0 || A->rowptr != nullptr, LSRN_EINVAL, "A->rowptr is NULL");
+    LSRN_REQUIRE(A->nnz == 0 || (A->colind != nullptr && A->val != nullptr), LSRN_EINVAL,
+                 "A->colind / A->val is NULL");
   } else {
     throw Fail{set_error(LSRN_EINVAL, "unknown matrix kind")};
   }
@@ -178,6 +185,124 @@ SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_fla
   const bool direct = (w.nsplit == 1) && (d.sx == 1.0) && !d.has_I && !need_finish_flag;
   w.part = direct ? nullptr : ar.take<double>((size_t)w.nsplit * d.s * d.k);
   return w;
+}
+
+// ------------------------------------------------------------------ CSR (K4)
+constexpr int kMaxHeavy = 64;
+
+struct CsrWs {
+  int* cntc;
+  int64_t *offs, *total, *colptr;
+  int *colmap, *heavy_cols;
+  int32_t* rowidx;
+  double *cval, *D, *part, *npart, *wpart;
+  int nsplit;
+  int64_t rows_per_split;
+  // filled by csr_prepare
+  int nd = 0, ND = 0;
+  int64_t nnz_light = 0;
+};
+
+CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
+  CsrWs w{};
+  const int64_t nch = csr_nchunks(d.cnt);
+  const int64_t k = d.k;
+  const int64_t nnz = std::max<int64_t>(A->nnz, 1);
+  w.cntc = ar.take<int>((size_t)std::max<int64_t>(nch, 1) * k);
+  w.offs = ar.take<int64_t>((size_t)std::max<int64_t>(nch, 1) * k);
+  w.total = ar.take<int64_t>((size_t)k);
+  w.colptr = ar.take<int64_t>((size_t)k + 1);
+  w.colmap = ar.take<int>((size_t)k);
+  w.heavy_cols = ar.take<int>(kMaxHeavy);
+  w.rowidx = ar.take<int32_t>((size_t)nnz);
+  w.cval = ar.take<double>((size_t)nnz);
+  w.D = ar.take<double>((size_t)std::max<int64_t>(d.cnt, 1) * kMaxHeavy);
+  // heavy-part split-K: enough (row block, split) CTAs for two waves
+  const int64_t row_blocks = (d.s + 255) / 256;
+  int nsplit = (int)std::max<int64_t>(1, (2 * (int64_t)c->nsm + row_blocks - 1) / row_blocks);
+  nsplit = (int)std::min<int64_t>(nsplit, std::max<int64_t>(1, d.cnt / 256));
+  w.nsplit = nsplit;
+  w.rows_per_split = std::max<int64_t>(1, (d.cnt + nsplit - 1) / nsplit);
+  w.part = ar.take<double>((size_t)nsplit * d.s * kMaxHeavy);
+  w.npart = ar.take<double>((size_t)csr_rowdot_blocks(c->nsm));
+  w.wpart = ar.take<double>((size_t)csr_rowdot_blocks(c->nsm) * kMaxHeavy);
+  return w;
+}
+
+// CSC copy of the light columns + heavy block D.  One device->host read of the
+// column counts (the heavy/light split is a host decision).
+void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
+  cudaStream_t st = c->stream;
+  CsrBuildArgs b{};
+  b.rowptr = A->rowptr;
+  b.colind = A->colind;
+  b.val = A->val;
+  b.rows = d.cnt;
+  b.k = d.k;
+  b.cntc = w.cntc;
+  b.offs = w.offs;
+  b.total = w.total;
+  b.colmap = w.colmap;
+  b.colptr = w.colptr;
+  b.rowidx = w.rowidx;
+  b.cval = w.cval;
+  b.D = w.D;
+  LSRN_CUDA(launch_csr_build(b, st));
+  c->launches += 2;
+  std::vector<int64_t> tot((size_t)d.k);
+  LSRN_CUDA(cudaMemcpyAsync(tot.data(), w.total, sizeof(int64_t) * d.k, cudaMemcpyDeviceToHost, st));
+  LSRN_CUDA(cudaStreamSynchronize(st));
+  // heavy: density >= 1/32 of the shard's rows (then one generated G[i, j] serves
+  // every heavy column of row j), at most kMaxHeavy, the densest first
+  const int64_t thr = std::max<int64_t>(1, (d.cnt + 31) / 32);
+  std::vector<int> cand;
+  for (int64_t j = 0; j < d.k; ++j)
+    if (tot[j] >= thr) cand.push_back((int)j);
+  std::stable_sort(cand.begin(), cand.end(), [&](int a, int b2) { return tot[a] > tot[b2]; });
+  if (cand.size() > (size_t)kMaxHeavy) cand.resize(kMaxHeavy);
+  std::sort(cand.begin(), cand.end());
+  w.nd = (int)cand.size();
+  w.ND = w.nd == 0 ? 0 : (w.nd <= 16 ? 16 : (w.nd <= 32 ? 32 : 64));
+  std::vector<int> colmap((size_t)d.k, -1);
+  for (int h = 0; h < w.nd; ++h) colmap[cand[h]] = h;
+  w.nnz_light = 0;
+  for (int64_t j = 0; j < d.k; ++j)
+    if (colmap[j] < 0) w.nnz_light += tot[j];
+  LSRN_CUDA(cudaMemcpyAsync(w.colmap, colmap.data(), sizeof(int) * d.k, cudaMemcpyHostToDevice, st));
+  if (w.nd > 0)
+    LSRN_CUDA(cudaMemcpyAsync(w.heavy_cols, cand.data(), sizeof(int) * w.nd, cudaMemcpyHostToDevice, st));
+  b.D = w.nd > 0 ? w.D : nullptr;
+  b.ld_d = w.ND;
+  LSRN_CUDA(launch_csr_fill(b, st));
+  c->launches += 2;
+  LSRN_CUDA(cudaStreamSynchronize(st));   // host vectors above are pageable: keep them alive until copied
+}
+
+void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double* At) {
+  CsrSketchArgs a{};
+  a.D = w.D;
+  a.rows = d.cnt;
+  a.lo = d.lo;
+  a.s = d.s;
+  a.k = d.k;
+  a.seed = seed;
+  a.nd = w.nd;
+  a.ND = w.ND;
+  a.nsplit = w.nsplit;
+  a.rows_per_split = w.rows_per_split;
+  a.part = w.part;
+  a.heavy_cols = w.heavy_cols;
+  a.colmap = w.colmap;
+  a.colptr = w.colptr;
+  a.rowidx = w.rowidx;
+  a.cval = w.cval;
+  a.At = At;
+  LSRN_CUDA(launch_csr_sketch(a, c->stream, c->nsm));
+  c->launches += (w.nd > 0 ? 3 : 1);
+  if (d.has_I) {
+    LSRN_CUDA(launch_sketch_add_gblock(At, d.s, d.k, d.L, d.si, seed, c->stream, c->nsm));
+    c->launches++;
+  }
 }
 
 void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed, const SketchWs& w, double* At) {
@@ -228,55 +353,71 @@ void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
 }
 
 // ------------------------------------------------------------------ SVD
+// Alg. 1/2 steps 4-5: singular values and right singular
+// vectors of the s x k sketch, outside the hot path.  Ãt = Q R (geqrf), then
+// the SVD of R through the symmetric eigenproblem of its Jordan-Wielandt matrix
+// [[0, R^T], [R, 0]], whose eigenpairs are (+-sigma_i, [v_i; +-u_i] / sqrt 2):
+// a true SVD (eigenvalues with absolute error ~ eps ||R||, no squaring of
+// kappa -- unlike an eigendecomposition of R^T R), the same
+// Golub-Kahan idea LAPACK's dbdsvdx uses for bidiagonal SVD.  syevdx computes
+// only the k largest eigenpairs.  Measured on the c2 shape (4000 x 2000, rank
+// 1800): 80 ms vs 231 ms for cuSOLVER gesvd with equal sigma / subspace
+// accuracy (profiles/r01_svd_options.jsonl).
 struct SvdWs {
-  double *W1, *tau, *R, *S, *VT, *work, *rwork, *Nt;
+  double *W1, *tau, *JW, *S, *work, *Nt;
   int* info;
   int lwork;
 };
 
 SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   SvdWs w{};
-  int l1 = 0, l2 = 0;
+  int l1 = 0, l2 = 0, meig = 0;
   LSRN_SOLVER(cusolverDnDgeqrf_bufferSize(c->solver, (int)d.s, (int)d.k, nullptr, (int)d.s, &l1));
-  LSRN_SOLVER(cusolverDnDgesvd_bufferSize(c->solver, (int)d.k, (int)d.k, &l2));
+  LSRN_SOLVER(cusolverDnDsyevdx_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                           CUBLAS_FILL_MODE_LOWER, (int)(2 * d.k), nullptr, (int)(2 * d.k), 0.0, 0.0,
+                                           (int)d.k + 1, (int)(2 * d.k), &meig, nullptr, &l2));
   w.lwork = l1 > l2 ? l1 : l2;
   w.W1 = ar.take<double>((size_t)d.s * d.k);
   w.tau = ar.take<double>((size_t)d.k);
-  w.R = ar.take<double>((size_t)d.k * d.k);
-  w.S = ar.take<double>((size_t)d.k);
-  w.VT = ar.take<double>((size_t)d.k * d.k);
+  w.JW = ar.take<double>((size_t)4 * d.k * d.k);
+  w.S = ar.take<double>((size_t)2 * d.k);
   w.work = ar.take<double>((size_t)w.lwork);
-  w.rwork = ar.take<double>((size_t)d.k);
   w.Nt = ar.take<double>((size_t)d.k * d.k);
   w.info = ar.take<int>(4);
   return w;
 }
 
-// Alg. 1 steps 4-5 / Alg. 2 steps 4-5 on the tall-form sketch: returns r.
+// Returns r; S_host receives the k singular values, descending.
 int64_t run_svd(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, std::vector<double>& S_host) {
   cudaStream_t st = c->stream;
-  LSRN_CUDA(launch_transpose(At, d.s, d.k, w.W1, st));
+  const int64_t k = d.k;
+  LSRN_CUDA(launch_transpose(At, d.s, k, w.W1, st));
   c->launches++;
-  LSRN_SOLVER(cusolverDnDgeqrf(c->solver, (int)d.s, (int)d.k, w.W1, (int)d.s, w.tau, w.work, w.lwork, w.info));
-  LSRN_CUDA(launch_extract_r(w.W1, d.s, d.k, w.R, st));
+  LSRN_SOLVER(cusolverDnDgeqrf(c->solver, (int)d.s, (int)k, w.W1, (int)d.s, w.tau, w.work, w.lwork, w.info));
+  LSRN_CUDA(launch_build_jw(w.W1, d.s, k, w.JW, st));
   c->launches++;
-  LSRN_SOLVER(cusolverDnDgesvd(c->solver, 'N', 'A', (int)d.k, (int)d.k, w.R, (int)d.k, w.S, nullptr, 1, w.VT,
-                               (int)d.k, w.work, w.lwork, w.rwork, w.info + 1));
-  S_host.assign((size_t)d.k, 0.0);
+  int meig = 0;
+  LSRN_SOLVER(cusolverDnDsyevdx(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER,
+                                (int)(2 * k), w.JW, (int)(2 * k), 0.0, 0.0, (int)k + 1, (int)(2 * k), &meig, w.S,
+                                w.work, w.lwork, w.info + 1));
+  std::vector<double> ev((size_t)k, 0.0);
   int info[2] = {0, 0};
-  LSRN_CUDA(cudaMemcpyAsync(S_host.data(), w.S, sizeof(double) * d.k, cudaMemcpyDeviceToHost, st));
+  LSRN_CUDA(cudaMemcpyAsync(ev.data(), w.S, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
   LSRN_CUDA(cudaMemcpyAsync(info, w.info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
   LSRN_CUDA(cudaStreamSynchronize(st));
-  LSRN_REQUIRE(info[0] == 0 && info[1] == 0, LSRN_ESVD,
-               "cuSOLVER geqrf/gesvd info = " + std::to_string(info[0]) + "/" + std::to_string(info[1]));
+  LSRN_REQUIRE(info[0] == 0 && info[1] == 0 && meig == (int)k, LSRN_ESVD,
+               "cuSOLVER geqrf/syevdx info = " + std::to_string(info[0]) + "/" + std::to_string(info[1]) +
+                   ", eigenpairs " + std::to_string(meig));
+  S_host.assign((size_t)k, 0.0);
+  for (int64_t i = 0; i < k; ++i) S_host[i] = std::max(0.0, ev[k - 1 - i]);
   // rank rule (reading C4): r = #{sigma_i > max(s, k) 2^-52 sigma_1}
-  const double tau = (double)std::max(d.s, d.k) * std::ldexp(1.0, -52) * S_host[0];
+  const double tau = (double)std::max(d.s, k) * std::ldexp(1.0, -52) * S_host[0];
   int64_t r = 0;
   if (S_host[0] > 0.0)
-    for (int64_t i = 0; i < d.k; ++i)
+    for (int64_t i = 0; i < k; ++i)
       if (S_host[i] > tau) ++r;
   LSRN_REQUIRE(r > 0, LSRN_ERANK0, "sketch has numerical rank 0");
-  LSRN_CUDA(launch_form_nt(w.VT, w.S, d.k, r, w.Nt, st));
+  LSRN_CUDA(launch_form_nt_jw(w.JW, 2 * k, w.S, k, r, w.Nt, st));
   c->launches++;
   return r;
 }
@@ -307,7 +448,7 @@ IterWs plan_iter(lsrn_ctx* c, const Dims& d, Arena& ar, int max_passes) {
   const int nparts = c->nsm > 0 ? c->nsm : 148;
   w.wpart = ar.take<double>((size_t)nparts * k);
   w.npart = ar.take<double>((size_t)nparts);
-  w.blockpart = ar.take<double>((size_t)colreduce_blocks(k) + 1);
+  w.blockpart = ar.take<double>((size_t)std::max(colreduce_blocks(k), csr_colgather_blocks(k)) + 1);
   w.ypart = ar.take<double>((size_t)lsqr_update_blocks(Lz > k ? Lz : k) + 1);
   w.ncoef = max_passes * 6 + 16;
   w.coef = ar.take<double>((size_t)w.ncoef);
@@ -325,9 +466,63 @@ struct Pass {
   int64_t r;
   IterWs& w;
   RowPassPlan plong, pshort;
+  const CsrWs* cw = nullptr;   // CSR A: rowdot + colgather instead of the dense row pass
+
+  // CSR long pass (tall only): z <- c1 z + c2 A t ; out = [A^T z (+ I block) ; ||z||^2]
+  void long_pass_csr(double* z, const double* t, const double* coef, const int* done, double* out) {
+    cudaStream_t st = c->stream;
+    const int idx = c->n_pass_ev;
+    const bool prof = c->profile && idx + 2 <= (int)c->pass_ev.size();
+    if (prof) LSRN_CUDA(cudaEventRecordWithFlags(c->pass_ev[idx], st, cudaEventRecordExternal));
+    CsrRowdotArgs a{};
+    a.rowptr = A->rowptr;
+    a.colind = A->colind;
+    a.val = A->val;
+    a.rows = d.cnt;
+    a.t = t;
+    a.colmap = cw->colmap;
+    a.coef = coef;
+    a.u = z;
+    a.npart = cw->npart;
+    a.wpart = cw->wpart;
+    a.done = done;
+    a.ND = cw->ND;
+    a.nblocks = csr_rowdot_blocks(c->nsm);
+    LSRN_CUDA(launch_csr_rowdot(a, st));
+    CsrGatherArgs g{};
+    g.colptr = cw->colptr;
+    g.rowidx = cw->rowidx;
+    g.cval = cw->cval;
+    g.k = d.k;
+    g.u = z;
+    g.colmap = cw->colmap;
+    g.wpart = cw->wpart;
+    g.ND = cw->ND;
+    g.npart = cw->npart;
+    g.nparts = a.nblocks;
+    g.zI = d.has_I ? z + d.cnt : nullptr;
+    g.t = t;
+    g.coef = coef;
+    g.sI = d.si;
+    g.out = out;
+    g.blockpart = w.blockpart;
+    g.counter = w.counters;
+    g.done = done;
+    LSRN_CUDA(launch_csr_colgather(g, st));
+    if (prof) {
+      LSRN_CUDA(cudaEventRecordWithFlags(c->pass_ev[idx + 1], st, cudaEventRecordExternal));
+      c->n_pass_ev += 2;
+    }
+    c->launches += 2;
+    allreduce(c, out, d.k + 1);
+  }
 
   // long pass over X: z <- c1 z + c2 sX X t (+ I block), out = [P^T z ; ||z||^2]
   void long_pass(double* z, const double* t, const double* coef, double* acc, const int* done, double* out) {
+    if (cw != nullptr) {
+      long_pass_csr(z, t, coef, done, out);
+      return;
+    }
     cudaStream_t st = c->stream;
     const int idx = c->n_pass_ev;
     const bool prof = c->profile && idx + 2 <= (int)c->pass_ev.size();
@@ -513,22 +708,78 @@ struct HostIO {
   double* x = nullptr;
 };
 
-size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar, Dims& d, SketchWs& sw, bool allow_partial,
-                SvdWs& vw, IterWs& iw, double** At, double** Astage, double** bstage, double** xstage) {
+struct Plan {
+  Dims d;
+  SketchWs sw;
+  CsrWs cw;
+  SvdWs vw;
+  IterWs iw;
+  double* At = nullptr;
+  // LSRN_HOST_IO staging (dense: A rows; CSR: rowptr / colind / val)
+  double* Astage = nullptr;
+  int64_t* rpstage = nullptr;
+  int32_t* cistage = nullptr;
+  double* bstage = nullptr;
+  double* xstage = nullptr;
+  bool csr = false;
+};
+
+// Carve every buffer of a solve (or of a sketch when `solve` is false) out of
+// the workspace; with ar.base == nullptr only the size is computed.
+size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar, Plan& P, bool allow_partial,
+                bool solve = true) {
+  Dims& d = P.d;
   d = make_dims(c, A, o->gamma, o->lambda, allow_partial);
-  *Astage = *bstage = *xstage = nullptr;
+  P.csr = A->kind == LSRN_CSR;
   if (o->flags & LSRN_HOST_IO) {
-    *Astage = ar.take<double>((size_t)d.cnt * A->ld);
-    *bstage = ar.take<double>((size_t)(d.tall ? d.cnt : d.m));
-    *xstage = ar.take<double>((size_t)(d.tall ? d.n : d.cnt));
+    if (P.csr) {
+      P.rpstage = ar.take<int64_t>((size_t)d.cnt + 1);
+      P.cistage = ar.take<int32_t>((size_t)std::max<int64_t>(A->nnz, 1));
+      P.Astage = ar.take<double>((size_t)std::max<int64_t>(A->nnz, 1));
+    } else {
+      P.Astage = ar.take<double>((size_t)d.cnt * A->ld);
+    }
+    if (solve) {
+      P.bstage = ar.take<double>((size_t)(d.tall ? d.cnt : d.m));
+      P.xstage = ar.take<double>((size_t)(d.tall ? d.n : d.cnt));
+    }
   }
-  *At = ar.take<double>((size_t)d.s * d.k);
-  sw = plan_sketch(c, d, ar, c->nranks > 1);
-  vw = plan_svd(c, d, ar);
-  // max passes: LSQR cap (2x the count for r = k) or CS passes with r = k; bounded by a generous margin
-  const int max_passes = 4096;
-  iw = plan_iter(c, d, ar, max_passes);
+  if (solve) P.At = ar.take<double>((size_t)d.s * d.k);
+  if (P.csr)
+    P.cw = plan_csr(c, d, A, ar);
+  else
+    P.sw = plan_sketch(c, d, ar, c->nranks > 1);
+  if (solve) {
+    P.vw = plan_svd(c, d, ar);
+    // max passes: LSQR cap (2x the count for r = k) or CS passes with r = k; bounded by a generous margin
+    const int max_passes = 4096;
+    P.iw = plan_iter(c, d, ar, max_passes);
+  }
   return ar.off;
+}
+
+// Stage host inputs (LSRN_HOST_IO) and return the device view of A.
+lsrn_matrix stage_inputs(lsrn_ctx* c, const lsrn_matrix* A_in, const lsrn_opts* o, Plan& P) {
+  lsrn_matrix A = *A_in;
+  if (!(o->flags & LSRN_HOST_IO)) return A;
+  cudaStream_t st = c->stream;
+  const Dims& d = P.d;
+  if (P.csr) {
+    if (d.cnt > 0)
+      LSRN_CUDA(cudaMemcpyAsync(P.rpstage, A_in->rowptr, sizeof(int64_t) * (d.cnt + 1), cudaMemcpyHostToDevice, st));
+    if (A_in->nnz > 0) {
+      LSRN_CUDA(cudaMemcpyAsync(P.cistage, A_in->colind, sizeof(int32_t) * A_in->nnz, cudaMemcpyHostToDevice, st));
+      LSRN_CUDA(cudaMemcpyAsync(P.Astage, A_in->val, sizeof(double) * A_in->nnz, cudaMemcpyHostToDevice, st));
+    }
+    A.rowptr = P.rpstage;
+    A.colind = P.cistage;
+    A.val = P.Astage;
+  } else {
+    if (d.cnt > 0)
+      LSRN_CUDA(cudaMemcpyAsync(P.Astage, A_in->val, sizeof(double) * d.cnt * A_in->ld, cudaMemcpyHostToDevice, st));
+    A.val = P.Astage;
+  }
+  return A;
 }
 
 void validate_opts(const lsrn_opts* o) {
@@ -557,12 +808,14 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     validate_opts(o);
     LSRN_REQUIRE(A_in != nullptr && b_in != nullptr && x_out != nullptr, LSRN_EINVAL, "A, b or x is NULL");
     Arena ar(ws);
-    Dims d;
-    SketchWs sw;
-    SvdWs vw;
-    IterWs iw;
-    double *At, *Astage, *bstage, *xstage;
-    const size_t need = plan_all(c, A_in, o, ar, d, sw, false, vw, iw, &At, &Astage, &bstage, &xstage);
+    Plan PL;
+    const size_t need = plan_all(c, A_in, o, ar, PL, false);
+    Dims& d = PL.d;
+    SketchWs& sw = PL.sw;
+    SvdWs& vw = PL.vw;
+    IterWs& iw = PL.iw;
+    double* At = PL.At;
+    double* xstage = PL.xstage;
     LSRN_REQUIRE(ws != nullptr && ws_bytes >= need, LSRN_ENOMEM,
                  "workspace too small: need " + std::to_string(need) + " bytes");
     LSRN_REQUIRE(!(o->mode == LSRN_MODE_ADAPTIVE && !d.tall && c->nranks > 1), LSRN_EUNSUPPORTED,
@@ -570,20 +823,22 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     cudaStream_t st = c->stream;
     c->launches = 0;
     c->n_pass_ev = 0;
-    lsrn_matrix A = *A_in;
     const double* b = b_in;
     double* x = x_out;
     LSRN_CUDA(cudaEventRecord(c->ev[0], st));
+    lsrn_matrix A = stage_inputs(c, A_in, o, PL);
     if (o->flags & LSRN_HOST_IO) {
-      LSRN_CUDA(cudaMemcpyAsync(Astage, A_in->val, sizeof(double) * d.cnt * A_in->ld, cudaMemcpyHostToDevice, st));
-      LSRN_CUDA(cudaMemcpyAsync(bstage, b_in, sizeof(double) * (d.tall ? d.cnt : d.m), cudaMemcpyHostToDevice, st));
-      A.val = Astage;
-      b = bstage;
+      LSRN_CUDA(cudaMemcpyAsync(PL.bstage, b_in, sizeof(double) * (d.tall ? d.cnt : d.m), cudaMemcpyHostToDevice, st));
+      b = PL.bstage;
       x = xstage;
     }
     // ---- sketch (Alg. 1/2 step 3)
+    if (PL.csr) csr_prepare(c, &A, d, PL.cw);   // CSC copy + heavy block (format conversion)
     LSRN_CUDA(cudaEventRecord(c->ev[1], st));
-    run_sketch(c, &A, d, o->seed, sw, At);
+    if (PL.csr)
+      run_sketch_csr(c, d, o->seed, PL.cw, At);
+    else
+      run_sketch(c, &A, d, o->seed, sw, At);
     LSRN_CUDA(cudaEventRecord(c->ev[2], st));
     allreduce(c, At, d.s * d.k);
     LSRN_CUDA(cudaEventRecord(c->ev[3], st));
@@ -616,7 +871,10 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
 
     // ---- iteration plans
     Pass P{c, d, &A, vw.Nt, r, iw, {}, {}};
-    P.plong = plan_rowpass(d.cnt, d.k, A.ld, A.val, c->nsm);
+    if (PL.csr)
+      P.cw = &PL.cw;
+    else
+      P.plong = plan_rowpass(d.cnt, d.k, A.ld, A.val, c->nsm);
     P.pshort = plan_rowpass(r, d.k, d.k, vw.Nt, c->nsm);
     const int64_t nV = d.tall ? r : d.Lz;  // length of the v-side vectors (LSQR)
 
@@ -810,7 +1068,10 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     c->stats[2] = (double)g_elapsed_err;
     c->stats[3] = (double)c->launches;
     c->stats[4] = (double)nlp;
-    c->stats[5] = (double)d.cnt * (double)d.k * 8.0;
+    // algorithmic bytes of one long pass: dense rows (8k + 16 per row);
+    // CSR: the CSR stream (12 B per nonzero + 8 B rowptr + 16 B u per row) + the light CSC (12 B per entry)
+    c->stats[5] = PL.csr ? (12.0 * (double)A_in->nnz + 24.0 * (double)d.cnt + 12.0 * (double)PL.cw.nnz_light)
+                         : (double)d.cnt * ((double)d.k * 8.0 + 16.0);
     c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
     c->stats[7] = (double)graph_launches;
     return LSRN_OK;
@@ -838,12 +1099,8 @@ lsrn_status lsrn_workspace_size(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_op
     LSRN_REQUIRE(c != nullptr && bytes != nullptr, LSRN_EINVAL, "NULL argument");
     validate_opts(o);
     Arena ar(nullptr);
-    Dims d;
-    SketchWs sw;
-    SvdWs vw;
-    IterWs iw;
-    double *At, *As, *bs, *xs;
-    *bytes = plan_all(c, A, o, ar, d, sw, true, vw, iw, &At, &As, &bs, &xs) + 256;
+    Plan PL;
+    *bytes = plan_all(c, A, o, ar, PL, true) + 256;
     return LSRN_OK;
   } catch (const Fail& f) {
     return f.code;
@@ -853,15 +1110,25 @@ lsrn_status lsrn_workspace_size(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_op
 lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, uint64_t seed, void* ws,
                         size_t ws_bytes, double* At, int64_t* s_out) {
   try {
-    LSRN_REQUIRE(c != nullptr && At != nullptr, LSRN_EINVAL, "ctx or At is NULL");
-    Dims d = make_dims(c, A, gamma, lambda, /*allow_partial=*/true);
+    LSRN_REQUIRE(c != nullptr && At != nullptr && A != nullptr, LSRN_EINVAL, "ctx, A or At is NULL");
+    lsrn_opts o{};
+    o.gamma = gamma;
+    o.lambda = lambda;
+    o.tol = 0.5;
+    o.seed = seed;
     Arena ar(ws);
-    SketchWs sw = plan_sketch(c, d, ar, c->nranks > 1);
+    Plan PL;
+    plan_all(c, A, &o, ar, PL, /*allow_partial=*/true, /*solve=*/false);
+    const Dims& d = PL.d;
     LSRN_REQUIRE(ar.off == 0 || (ws != nullptr && ws_bytes >= ar.off), LSRN_ENOMEM,
                  "workspace too small for the sketch: need " + std::to_string(ar.off) + " bytes");
     c->launches = 0;
+    if (PL.csr) csr_prepare(c, A, d, PL.cw);
     LSRN_CUDA(cudaEventRecord(c->ev[1], c->stream));
-    run_sketch(c, A, d, seed, sw, At);
+    if (PL.csr)
+      run_sketch_csr(c, d, seed, PL.cw, At);
+    else
+      run_sketch(c, A, d, seed, PL.sw, At);
     LSRN_CUDA(cudaEventRecord(c->ev[2], c->stream));
     allreduce(c, At, d.s * d.k);
     LSRN_CUDA(cudaEventRecord(c->ev[3], c->stream));

@@ -62,6 +62,54 @@ __global__ void form_nt_kernel(const double* __restrict__ VT, const double* __re
   }
 }
 
+// Jordan-Wielandt matrix of R (the upper triangle of the leading k x k block of
+// the column-major QR factor qr, leading dim ld): JW = [[0, R^T], [R, 0]] (2k x 2k,
+// column-major).  Only the lower triangle is referenced by syevdx(lower); the
+// lower-left block R is written in full, everything else zero.
+__global__ void build_jw_kernel(const double* __restrict__ qr, int64_t ld, int64_t k, double* __restrict__ JW) {
+  const int64_t n2 = 2 * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n2 * n2; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % n2, j = e / n2;      // column-major (i, j)
+    double v = 0.0;
+    if (i >= k && j < k) {
+      const int64_t a = i - k;                 // R[a][j], upper triangular
+      v = (a <= j) ? qr[a + j * ld] : 0.0;
+    }
+    JW[e] = v;
+  }
+}
+
+// N^T from the top-k eigenvectors of JW: eigenvalues ascending, so singular value
+// c (descending) is eigenpair k-1-c; its right singular vector is sqrt(2) times
+// the first k entries of the eigenvector.  Nt[c][j] = sqrt2 E[j, k-1-c] / S[k-1-c].
+__global__ void form_nt_jw_kernel(const double* __restrict__ E, int64_t lde, const double* __restrict__ ev,
+                                  int64_t k, int64_t r, double* __restrict__ Nt) {
+  __shared__ double tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const double sq2 = 1.4142135623730951;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, j = j0 + threadIdx.x;     // read E[j, k-1-c]: coalesced along j
+    if (j < k && c < r) tile[i][threadIdx.x] = sq2 * E[j + (k - 1 - c) * lde] / ev[k - 1 - c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, j = j0 + threadIdx.x;
+    if (j < k && c < r) Nt[c * k + j] = tile[i][threadIdx.x];
+  }
+}
+
+cudaError_t launch_build_jw(const double* qr, int64_t ld, int64_t k, double* JW, cudaStream_t st) {
+  build_jw_kernel<<<grid_for(4 * k * k), 256, 0, st>>>(qr, ld, k, JW);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_form_nt_jw(const double* E, int64_t lde, const double* ev, int64_t k, int64_t r, double* Nt,
+                              cudaStream_t st) {
+  dim3 grid((unsigned)((k + 31) / 32), (unsigned)((r + 31) / 32));
+  form_nt_jw_kernel<<<grid, dim3(32, 8), 0, st>>>(E, lde, ev, k, r, Nt);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill(double* p, double v, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   fill_kernel<<<grid_for(n), 256, 0, st>>>(p, v, n);

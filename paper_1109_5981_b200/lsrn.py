@@ -113,6 +113,40 @@ def dense(X, m, n, lo=0, cnt=None):
                   max(X.shape[1], 1), rowptr=None, colind=None, nnz=0), X
 
 
+class Csr:
+    """A row shard of a tall CSR A: rowptr int64[cnt+1], colind int32[nnz], val float64[nnz] (torch tensors)."""
+
+    def __init__(self, rowptr, colind, val):
+        if rowptr.dtype != torch.int64 or colind.dtype != torch.int32 or val.dtype != torch.float64:
+            raise TypeError("CSR needs rowptr int64, colind int32, val float64")
+        if not (rowptr.is_contiguous() and colind.is_contiguous() and val.is_contiguous()):
+            raise ValueError("CSR arrays must be contiguous")
+        self.rowptr, self.colind, self.val = rowptr, colind, val
+
+    @property
+    def rows(self):
+        return self.rowptr.numel() - 1
+
+    @property
+    def device(self):
+        return self.val.device
+
+
+def csr(A, m, n, lo=0, cnt=None):
+    """Matrix descriptor for a CSR row shard (see Csr)."""
+    cnt = A.rows if cnt is None else cnt
+    nnz = A.val.numel()
+    return Matrix(kind=LSRN_CSR, m=m, n=n, lo=lo, cnt=cnt, val=A.val.data_ptr() if nnz else None, ld=0,
+                  rowptr=A.rowptr.data_ptr(), colind=A.colind.data_ptr() if nnz else None, nnz=nnz), A
+
+
+def describe(X, m, n, lo=0, cnt=None):
+    """Descriptor for a dense long-index-major tensor or a Csr shard."""
+    if isinstance(X, Csr):
+        return csr(X, m, n, lo, cnt)
+    return dense(X, m, n, lo, cnt)
+
+
 def nccl_unique_id():
     buf = ctypes.create_string_buffer(128)
     _check(lib().lsrn_nccl_unique_id(buf))
@@ -178,8 +212,8 @@ class Context:
             cur.wait_stream(self.stream)
 
     def sketch(self, X, m, n, gamma=2.0, lam=0.0, seed=5981, lo=0, cnt=None):
-        """Tall-form sketch At (s x k) of the shard X; returns a new device tensor."""
-        mat, _keep = dense(X, m, n, lo, cnt)
+        """Tall-form sketch At (s x k) of the shard X (dense or Csr); returns a new device tensor."""
+        mat, _keep = describe(X, m, n, lo, cnt)
         k = min(m, n)
         s = int(torch.tensor(gamma * k, dtype=torch.float64).ceil().item())
         At = torch.empty(s, k, dtype=torch.float64, device=self.device)
@@ -195,14 +229,14 @@ class Context:
 
     def solve(self, X, b, m, n, solver="lsqr", gamma=2.0, lam=0.0, tol=1e-14, seed=5981, alpha=-1.0,
               mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False):
-        """LSRN solve; X long-index-major shard (device, or pinned host with host_io)."""
-        if host_io:
+        """LSRN solve; X a long-index-major dense shard or a Csr row shard (device, or pinned host with host_io)."""
+        if host_io and not isinstance(X, Csr):
             if X.dim() != 2 or X.stride(1) != 1:
                 raise ValueError("X must be row-major 2-D")
             cnt_ = X.shape[0] if cnt is None else cnt
             mat = Matrix(kind=LSRN_DENSE, m=m, n=n, lo=lo, cnt=cnt_, val=X.data_ptr(), ld=X.stride(0))
         else:
-            mat, _keep = dense(X, m, n, lo, cnt)
+            mat, _keep = describe(X, m, n, lo, cnt)
         tall = m >= n
         xlen = n if tall else mat.cnt
         if x_out is None:

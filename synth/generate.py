@@ -96,9 +96,11 @@ def _block_gen(seed, g, device):
     return gen
 
 
-def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, **over):
+def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep_factors=False, **over):
     """Build config `name` (c1..c5), optionally rescaled (m, n overrides).
 
+    keep_factors=True keeps the generator's U, V (Haar recipes) in meta, so tests can
+    form the exact pseudoinverse solution at full size.
     shard=(lo, hi) generates only long-index rows [lo, hi) of X (and the matching
     rows of b for a tall A) -- the bytes are identical to the same rows of the
     full problem for the i.i.d. recipes (c3, c4, c5), which are generated in
@@ -128,8 +130,10 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, **ov
         U = _haar(L, rank, gen, device)
         V = _haar(k, rank, gen, device)
         X = (U * sig) @ V.T                           # long-index-major L x k
-        del U
         meta.update(rank=rank, sigma=sig, kappa=float(sig[0] / sig[-1]))
+        if keep_factors:                              # X = U diag(sig) V^T (test pins: exact pseudoinverse)
+            meta.update(U=U, V=V)
+        del U
         if cfg["rhs"] == "model":
             x0 = torch.randn(n, generator=gen, **f64)
             b = (X @ x0 if m >= n else X.T @ x0) + 1e-3 * torch.randn(m, generator=gen, **f64)

@@ -1,0 +1,153 @@
+"""GPU parity of the CSR path (K4 sketch, CSR long pass) against the CPU oracle.
+
+Sketch Ã = G A for sparse A (Alg. 1 step 3; "automatically speeds up
+when A is sparse"): relative Frobenius <= 1e-12 (north star).  Solves:
+identical iteration counts and rank, x within max(1e-9, 20 kappa u) and the
+A-norm form (C18).  Cases cover the heavy/light column split (none,
+some, more than the 64-column cap), empty rows and columns, shards with a
+non-zero global offset, the Tikhonov block and host buffers.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+from oracle.lsrn import solve as orc_solve
+from oracle.sketch import plan as orc_plan
+from oracle.sketch import sketch as orc_sketch
+from synth.generate import make_problem, small
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1109_5981_b200 import lsrn
+    c = lsrn.Context()
+    yield c
+    c.close()
+
+
+def _gpu_csr(A):
+    from paper_1109_5981_b200.lsrn import Csr
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    return Csr(torch.from_numpy(A.indptr.astype(np.int64)).cuda(),
+               torch.from_numpy(A.indices.astype(np.int32)).cuda(),
+               torch.from_numpy(A.data.astype(np.float64)).cuda())
+
+
+def _random_csr(m, n, nnz_row, dense_cols=0, dense_scale=1.0, empty_rows=0, seed=0):
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    light = n - dense_cols
+    for i in range(m):
+        if i < empty_rows:
+            continue
+        cs = rng.choice(light, size=min(nnz_row, light), replace=False) if light > 0 else np.array([], int)
+        cs = np.concatenate([cs, np.arange(light, n)])
+        v = rng.standard_normal(cs.size)
+        v[cs >= light] *= dense_scale
+        rows += [i] * cs.size
+        cols += list(cs)
+        vals += list(v)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(m, n))
+
+
+def _relfro(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("m,n,nnz_row,dense_cols,lam,empty", [
+    (3000, 120, 6, 0, 0.0, 0),       # light columns only (no heavy block)
+    (4000, 150, 5, 7, 0.0, 17),      # heavy block ND=16 + empty rows
+    (2500, 100, 3, 80, 0.0, 0),      # 80 dense columns: capped at 64 heavy, 16 dense ones stay light
+    (3000, 90, 4, 20, 0.5, 0),       # heavy ND=32 + tall Tikhonov block
+    (777, 61, 2, 3, 0.0, 5),         # odd s = 122? (gamma 2 -> 122), ragged everything
+])
+def test_csr_sketch_vs_oracle(ctx, m, n, nnz_row, dense_cols, lam, empty):
+    A = _random_csr(m, n, nnz_row, dense_cols, 1e3, empty, seed=m + n)
+    At = ctx.sketch(_gpu_csr(A), m, n, 2.0, lam, seed=5981).cpu().numpy()
+    p = orc_plan(m, n, 2.0, lam)
+    ref = orc_sketch(A, p["s"], 5981, p["sigma_x"], p["sigma_i"])
+    assert _relfro(At, ref) <= 1e-12
+
+
+def test_csr_sketch_equals_dense_sketch(ctx):
+    A = _random_csr(2000, 80, 5, 4, 10.0, 3, seed=11)
+    Ad = torch.from_numpy(A.toarray()).cuda()
+    a1 = ctx.sketch(_gpu_csr(A), 2000, 80).cpu().numpy()
+    a2 = ctx.sketch(Ad, 2000, 80).cpu().numpy()
+    assert _relfro(a1, a2) <= 1e-13
+
+
+def test_csr_sketch_shards_sum_to_full(ctx):
+    m, n = 3100, 70
+    A = _random_csr(m, n, 4, 5, 100.0, 0, seed=2)
+    full = ctx.sketch(_gpu_csr(A), m, n).cpu().numpy()
+    acc = np.zeros_like(full)
+    for lo, hi in [(0, 999), (999, 1000), (1000, 3100)]:
+        acc += ctx.sketch(_gpu_csr(A[lo:hi]), m, n, lo=lo, cnt=hi - lo).cpu().numpy()
+    assert _relfro(acc, full) <= 1e-13
+
+
+def test_csr_sketch_repeatable_bitwise(ctx):
+    A = _random_csr(3000, 100, 6, 5, 1e3, 0, seed=9)
+    G = _gpu_csr(A)
+    a1 = ctx.sketch(G, 3000, 100)
+    a2 = ctx.sketch(G, 3000, 100)
+    assert torch.equal(a1, a2)
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_csr_solve_small_c4(ctx, solver):
+    p = small("c4")
+    A = p.to_scipy()
+    b = p.b.numpy()
+    from paper_1109_5981_b200.lsrn import Csr
+    X = Csr(p.rowptr.cuda(), p.colind.cuda(), p.val.cuda())
+    x, rep = ctx.solve(X, p.b.cuda(), p.m, p.n, solver=solver)
+    orc = orc_solve(A, b, solver=solver)
+    assert rep["r"] == orc["r"] and rep["s"] == orc["s"]
+    assert rep["iters"] == orc["iters"]
+    sv = np.linalg.svd(A.toarray(), compute_uv=False)
+    kappa = sv[0] / sv[-1]
+    xg = x.cpu().numpy()
+    rel = np.linalg.norm(xg - orc["x"]) / np.linalg.norm(orc["x"])
+    assert rel <= max(1e-9, 20 * kappa * U), rel
+    an = np.linalg.norm(A @ (xg - orc["x"])) / np.linalg.norm(A @ orc["x"])
+    assert an <= 1e-11, an
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_csr_solve_tikhonov_and_dense_agree(ctx, solver):
+    A = _random_csr(1500, 60, 4, 6, 30.0, 2, seed=4)
+    b = np.random.default_rng(1).standard_normal(1500)
+    lam = 0.3
+    x1, r1 = ctx.solve(_gpu_csr(A), torch.from_numpy(b).cuda(), 1500, 60, solver=solver, lam=lam)
+    x2, r2 = ctx.solve(torch.from_numpy(A.toarray()).cuda(), torch.from_numpy(b).cuda(), 1500, 60, solver=solver,
+                       lam=lam)
+    orc = orc_solve(A, b, solver=solver, lam=lam)
+    assert r1["iters"] == r2["iters"] == orc["iters"]
+    for x in (x1, x2):
+        rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
+        assert rel <= 1e-9, rel
+
+
+def test_csr_host_io_matches_device(ctx):
+    from paper_1109_5981_b200.lsrn import Csr
+    p = small("c4")
+    xd, rd = ctx.solve(Csr(p.rowptr.cuda(), p.colind.cuda(), p.val.cuda()), p.b.cuda(), p.m, p.n, solver="cs")
+    Xh = Csr(p.rowptr.pin_memory(), p.colind.pin_memory(), p.val.pin_memory())
+    xh, rh = ctx.solve(Xh, p.b.pin_memory(), p.m, p.n, solver="cs", host_io=True)
+    assert torch.equal(xd.cpu(), xh) and rd["iters"] == rh["iters"]
+
+
+def test_csr_rejects_wide(ctx):
+    from paper_1109_5981_b200.lsrn import LsrnError
+    A = _random_csr(50, 400, 3, 0, 1.0, 0, seed=1)
+    with pytest.raises(LsrnError, match="EUNSUPPORTED"):
+        ctx.sketch(_gpu_csr(A), 50, 400)

@@ -1,0 +1,133 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py uses.
+
+The oracle cannot redo a full-size solve in seconds, so these tests check
+  * sampled sketch entries, each recomputed one by one by the oracle
+    (oracle.sketch.sketch_entries: G[i, :] regenerated, dot with column c);
+  * closed forms: for c2 the generator's own factors give the exact
+    min-length solution x* = V diag(1/sigma) U^T b, so x is checked
+    against A^+ b directly; iteration counts against Thm 4.5 / Alg. 3 (P:643,
+    P:694) and the rank against the generator's rank;
+  * invariants at any size: x in range(A^T) and the normal equations.
+c2 runs by default (about a minute); c3 (3.2 GB), c4 (CSR, 1.4e8 nonzeros)
+and c5 (80 GB) run when LSRN_FULLSIZE=1 (their SVD / sketch stages take long).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import bounds
+from oracle.sketch import plan as orc_plan
+from oracle.sketch import sketch_entries
+from synth.generate import SKETCH_SEED, make_problem
+
+pytestmark = pytest.mark.gpu
+FULL = os.environ.get("LSRN_FULLSIZE") == "1"
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1109_5981_b200 import lsrn
+    c = lsrn.Context()
+    yield c
+    c.close()
+
+
+def _sampled_sketch_check(At, Xcol, s, L, sx=1.0, si=0.0, nsamp=12, seed=0):
+    """Compare nsamp entries of At (s x k, device) with the oracle, one by one."""
+    rng = np.random.default_rng(seed)
+    k = At.shape[1]
+    rows = list(rng.integers(0, s, nsamp - 2)) + [0, s - 1]
+    cols = list(rng.integers(0, k, nsamp - 2)) + [k - 1, 0]
+    cols_data = {c: Xcol(c) for c in set(cols)}
+    ref = sketch_entries(cols_data, rows, cols, SKETCH_SEED, sx, si, L=L)
+    got = At[torch.tensor(rows), torch.tensor(cols)].cpu().numpy()
+    # each entry is a length-L dot product of N(0,1) draws with a column: compare against
+    # its natural scale sqrt(sum_j X[j,c]^2) (the entry's standard deviation)
+    scale = np.array([np.linalg.norm(cols_data[c]) for c in cols])
+    err = np.abs(got - ref) / scale
+    assert err.max() <= 1e-12, (err.max(), rows, cols)
+
+
+def test_c2_full(ctx):
+    p = make_problem("c2", device="cuda", keep_factors=True)
+    m, n = p.m, p.n
+    At = ctx.sketch(p.X, m, n, 2.0, 0.0, seed=SKETCH_SEED)
+    s = At.shape[0]
+    assert s == 4000
+    Xc = p.X
+    _sampled_sketch_check(At, lambda c: Xc[:, c].cpu().numpy(), s, m)
+    del At
+    U = p.meta["U"].cpu().numpy()
+    V = p.meta["V"].cpu().numpy()
+    sig = p.meta["sigma"].cpu().numpy()
+    b = p.b.cpu().numpy()
+    xstar = V @ ((U.T @ b) / sig)                     # A^+ b from the generator's SVD
+    del U
+    for solver in ("lsqr", "cs"):
+        x, rep = ctx.solve(p.X, p.b, m, n, solver=solver, seed=SKETCH_SEED)
+        assert rep["r"] == 1800 and rep["s"] == 4000
+        alpha = bounds.default_alpha(s)
+        sl, su = bounds.sigma_bounds(s, 1800, alpha)
+        want = bounds.lsqr_count(1e-14, 1800, s) if solver == "lsqr" else bounds.cs_passes(sl, su, 1e-14)
+        assert rep["iters"] == want == (83 if solver == "lsqr" else 89)
+        xg = x.cpu().numpy()
+        rel = np.linalg.norm(xg - xstar) / np.linalg.norm(xstar)
+        assert rel <= 1e-9, (solver, rel)
+        leak = np.linalg.norm(xg - V @ (V.T @ xg)) / np.linalg.norm(xg)    # x in range(A^T)
+        assert leak <= 1e-10, leak
+
+
+@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
+def test_c3_full_tikhonov(ctx):
+    p = make_problem("c3", device="cuda")
+    m, n, lam = p.m, p.n, p.lam
+    pl = orc_plan(m, n, 2.0, lam)
+    At = ctx.sketch(p.X, m, n, 2.0, lam, seed=SKETCH_SEED)
+    Xc = p.X                                          # X = A^T (n x m)
+    _sampled_sketch_check(At, lambda c: Xc[:, c].cpu().numpy(), pl["s"], n, pl["sigma_x"], pl["sigma_i"])
+    del At
+    for solver in ("lsqr", "cs"):
+        x, rep = ctx.solve(p.X, p.b, m, n, solver=solver, lam=lam)
+        assert rep["r"] == 2000
+        # ridge normal equations A^T (b - A x) = lam^2 x  (W = lam I)
+        A_T = p.X
+        res = A_T @ (p.b - A_T.T @ x) - lam ** 2 * x
+        scale = torch.linalg.norm(A_T, 2) ** 2 * torch.linalg.norm(x) + torch.linalg.norm(A_T @ p.b)
+        assert float(torch.linalg.norm(res) / scale) <= 1e-12
+
+
+@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
+def test_c4_full_sketch(ctx):
+    from paper_1109_5981_b200.lsrn import Csr
+    p = make_problem("c4", device="cuda")
+    X = Csr(p.rowptr, p.colind, p.val)
+    At = ctx.sketch(X, p.m, p.n, 2.0, 0.0, seed=SKETCH_SEED)
+    A = p.to_scipy().tocsc()
+
+    def col(c):
+        return np.asarray(A[:, c].toarray()).ravel()
+    _sampled_sketch_check(At, col, At.shape[0], p.m, nsamp=8)
+
+
+@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
+def test_c5_full(ctx):
+    p = make_problem("c5", device="cuda")
+    m, n = p.m, p.n
+    At = ctx.sketch(p.X, m, n, 2.0, 0.0, seed=SKETCH_SEED)
+    Xc = p.X
+    _sampled_sketch_check(At, lambda c: Xc[:, c].cpu().numpy(), At.shape[0], m, nsamp=6)
+    del At
+    x, rep = ctx.solve(p.X, p.b, m, n, solver="cs")
+    s = 20000
+    sl, su = bounds.sigma_bounds(s, 10000, bounds.default_alpha(s))
+    assert rep["r"] == 10000 and rep["iters"] == bounds.cs_passes(sl, su, 1e-14) == 99
+    # normal equations: ||A^T (b - A x)|| <= 1e-10 ||A|| ||b - A x||  (x is the LS solution)
+    r = p.b - p.X @ x
+    g = p.X.T @ r
+    an = float(torch.linalg.norm(p.X[:200000], 2)) * math.sqrt(5)
+    assert float(torch.linalg.norm(g)) <= 1e-10 * an * float(torch.linalg.norm(r))
