@@ -71,9 +71,13 @@ LSRN_DEV double gaussian_lane(uint2 key, uint64_t q, uint64_t j, bool odd) {
 }  // namespace
 
 // ------------------------------------------------------------ CSC construction
-// cntc[chunk][c] = number of nonzeros of column c in rows [chunk*CH, (chunk+1)*CH)
+// cntc[chunk][c] = number of nonzeros of column c in rows [chunk*CH, (chunk+1)*CH).
+// Also validates the canonical-CSR contract (lsrn.h): column indices in [0, k)
+// (bad |= 1) and strictly increasing within each row (bad |= 2) -- the CSC
+// fill and the heavy-column accumulation rely on distinct columns per row.
 __global__ void csr_chunk_count_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
-                                       int64_t rows, int64_t k, int64_t CH, int* __restrict__ cntc) {
+                                       int64_t rows, int64_t k, int64_t CH, int* __restrict__ cntc,
+                                       int* __restrict__ bad) {
   extern __shared__ int hist[];
   const int64_t chunk = blockIdx.x;
   for (int64_t c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
@@ -81,7 +85,22 @@ __global__ void csr_chunk_count_kernel(const int64_t* __restrict__ rowptr, const
   const int64_t r0 = chunk * CH, r1 = min(rows, r0 + CH);
   const int64_t base = rowptr[0];
   const int64_t e0 = rowptr[r0] - base, e1 = rowptr[r1] - base;
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(&hist[colind[e]], 1);   // integer: exact
+  int flag = 0;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {     // row structure
+    const int64_t a0 = rowptr[r] - base, a1 = rowptr[r + 1] - base;
+    if (a1 < a0) flag |= 4;
+    for (int64_t e = a0 + 1; e < a1; ++e)
+      if (colind[e] <= colind[e - 1]) flag |= 2;
+  }
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int c = colind[e];
+    if (c < 0 || c >= k) {
+      flag |= 1;
+      continue;
+    }
+    atomicAdd(&hist[c], 1);   // integer: exact
+  }
+  if (flag) atomicOr(bad, flag);
   __syncthreads();
   int* out = cntc + chunk * k;
   for (int64_t c = threadIdx.x; c < k; c += blockDim.x) out[c] = hist[c];
@@ -294,7 +313,8 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
     double d = 0.0;
     for (int64_t e = e0 + lane; e < e1; e += 32) d = fma(val[e], __ldg(t + colind[e]), d);
     d = warp_sum(d);
-    const double un = fma(c1, u[r], c2 * d);
+    const double uo = __shfl_sync(0xffffffffu, lane == 0 ? u[r] : 0.0, 0);
+    const double un = fma(c1, uo, c2 * d);
     if (lane == 0) u[r] = un;
     nrm = fma(un, un, nrm);
     if (ND > 0) {
@@ -383,11 +403,13 @@ static unsigned grid_cap(int64_t n, int threads, int64_t cap) {
 cudaError_t launch_csr_build(const CsrBuildArgs& a, cudaStream_t st) {
   const int64_t nch = csr_nchunks(a.rows);
   const int64_t CH = csr_chunk_rows();
+  cudaError_t e0 = cudaMemsetAsync(a.bad, 0, sizeof(int), st);
+  if (e0 != cudaSuccess) return e0;
   if (nch > 0) {
     const size_t sh1 = sizeof(int) * (size_t)a.k;
     cudaError_t e = cudaFuncSetAttribute(csr_chunk_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh1);
     if (e != cudaSuccess) return e;
-    csr_chunk_count_kernel<<<(unsigned)nch, 512, sh1, st>>>(a.rowptr, a.colind, a.rows, a.k, CH, a.cntc);
+    csr_chunk_count_kernel<<<(unsigned)nch, 512, sh1, st>>>(a.rowptr, a.colind, a.rows, a.k, CH, a.cntc, a.bad);
   }
   csr_chunk_scan_kernel<<<grid_cap(a.k, 256, 4096), 256, 0, st>>>(a.cntc, nch, a.k, a.offs, a.total);
   return cudaGetLastError();

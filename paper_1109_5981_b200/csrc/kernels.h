@@ -18,7 +18,9 @@ struct SketchDenseArgs {
 };
 size_t sketch_dense_smem();
 void sketch_tile_counts(int64_t s, int64_t k, int64_t* mtiles, int64_t* ntiles, int64_t* bk);
-cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st);
+cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st);   // picks v2 when supported
+bool sketch_ws_supported(const SketchDenseArgs& a);
+cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_finish(const double* part, int nsplit, int64_t split_stride, int64_t s, int64_t k,
                                  double sx, double si, int64_t L, uint64_t seed, double* out, cudaStream_t st,
                                  int nsm);
@@ -106,13 +108,14 @@ struct CsrBuildArgs {
   double* cval;            // [nnz_light]
   double* D;               // [rows][ld_d] heavy block (nullable when no heavy column)
   int64_t ld_d;
+  int* bad;                // validation flags (zeroed by launch_csr_build): 1 column range, 2 order, 4 rowptr
 };
 int64_t csr_chunk_rows();
 int64_t csr_nchunks(int64_t rows);
 int csr_rowdot_blocks(int nsm);
 int csr_colgather_blocks(int64_t k);
 size_t csr_max_k();
-cudaError_t launch_csr_build(const CsrBuildArgs& a, cudaStream_t st);   // counts + per-column totals
+cudaError_t launch_csr_build(const CsrBuildArgs& a, cudaStream_t st);   // validate + counts + per-column totals
 cudaError_t launch_csr_fill(const CsrBuildArgs& a, cudaStream_t st);    // colptr + CSC + D (needs colmap)
 
 struct CsrSketchArgs {

@@ -192,6 +192,7 @@ constexpr int kMaxHeavy = 64;
 
 struct CsrWs {
   int* cntc;
+  int* bad;
   int64_t *offs, *total, *colptr;
   int *colmap, *heavy_cols;
   int32_t* rowidx;
@@ -209,6 +210,7 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
   const int64_t k = d.k;
   const int64_t nnz = std::max<int64_t>(A->nnz, 1);
   w.cntc = ar.take<int>((size_t)std::max<int64_t>(nch, 1) * k);
+  w.bad = ar.take<int>(4);
   w.offs = ar.take<int64_t>((size_t)std::max<int64_t>(nch, 1) * k);
   w.total = ar.take<int64_t>((size_t)k);
   w.colptr = ar.take<int64_t>((size_t)k + 1);
@@ -247,11 +249,18 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
   b.rowidx = w.rowidx;
   b.cval = w.cval;
   b.D = w.D;
+  b.bad = w.bad;
   LSRN_CUDA(launch_csr_build(b, st));
   c->launches += 2;
   std::vector<int64_t> tot((size_t)d.k);
+  int bad = 0;
   LSRN_CUDA(cudaMemcpyAsync(tot.data(), w.total, sizeof(int64_t) * d.k, cudaMemcpyDeviceToHost, st));
+  LSRN_CUDA(cudaMemcpyAsync(&bad, w.bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   LSRN_CUDA(cudaStreamSynchronize(st));
+  LSRN_REQUIRE(bad == 0, LSRN_EINVAL,
+               std::string("CSR A is not canonical:") + ((bad & 1) ? " column index outside [0, n);" : "") +
+                   ((bad & 2) ? " column indices not strictly increasing within a row;" : "") +
+                   ((bad & 4) ? " rowptr decreasing;" : ""));
   // heavy: density >= 1/32 of the shard's rows (then one generated G[i, j] serves
   // every heavy column of row j), at most kMaxHeavy, the densest first
   const int64_t thr = std::max<int64_t>(1, (d.cnt + 31) / 32);

@@ -33,38 +33,6 @@ namespace lsrn {
 
 namespace {
 
-LSRN_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-
-LSRN_DEV void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-LSRN_DEV void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-LSRN_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// 1-D bulk copy global -> this CTA's shared memory, completion on `bar`.
-LSRN_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 constexpr int THREADS = 256;
 constexpr int NWARP = THREADS / 32;
 constexpr int kMaxStages = 8;
@@ -103,7 +71,7 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
     const int64_t rb = r0 + tile * TR;
     const int nr = (int)min((int64_t)TR, r1 - rb);
     if (row_bytes == 0) {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&full[st])) : "memory");
+      mbar_arrive(&full[st]);
       return;
     }
     mbar_arrive_expect_tx(&full[st], row_bytes * (unsigned)nr);
@@ -113,10 +81,10 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
 
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mbar_fence_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {       // prime every stage; stage of tile t-1 is refilled after tile t's barrier
     for (int64_t t = 0; t < min((int64_t)nst, ntiles); ++t) issue(t);
   }
 
@@ -141,18 +109,21 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
     for (int tr = 0; tr < TR; ++tr) zo[tr] = (rb + tr < r1) ? a.z[rb + tr] : 0.0;
     mbar_wait(&full[st], parity);
 
-    double2 y[TR][P];
+    // phase 1: partial row dots from shared memory (rows past r1 are zero-weighted)
     double d[TR];
 #pragma unroll
     for (int tr = 0; tr < TR; ++tr) {
       const double* row = stage + ((int64_t)st * TR + tr) * stage_ld;
-      const bool rok = rb + tr < r1;
       double s = 0.0;
+      if (rb + tr < r1) {
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const int64_t cl = 2 * (tid + THREADS * p);
-        y[tr][p] = (rok && cl < ncol) ? *reinterpret_cast<const double2*>(row + cl) : make_double2(0.0, 0.0);
-        s = fma(y[tr][p].x, tv[p].x, fma(y[tr][p].y, tv[p].y, s));
+        for (int p = 0; p < P; ++p) {
+          const int64_t cl = 2 * (tid + THREADS * p);
+          if (cl < ncol) {
+            const double2 y = *reinterpret_cast<const double2*>(row + cl);
+            s = fma(y.x, tv[p].x, fma(y.y, tv[p].y, s));
+          }
+        }
       }
       d[tr] = s;
     }
@@ -161,8 +132,9 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
       const double s = warp_sum(d[tr]);
       if (lane == 0) red[buf][warp][tr] = s;
     }
-    __syncthreads();                       // stage st fully read; partial dots visible
-    if (tid == 0 && tile + nst < ntiles) issue(tile + nst);
+    __syncthreads();                       // partial dots visible; stage of tile-1 fully consumed
+    // refill the stage the previous tile used (its phase-2 reads finished before this barrier)
+    if (tid == 0 && tile >= 1 && tile - 1 + nst < ntiles) issue(tile - 1 + nst);
     double dot[TR];
     if (CL > 1) {
       cg::cluster_group cluster = cg::this_cluster();
@@ -188,22 +160,27 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
         dot[tr] = s;
       }
     }
+    // phase 2: new z entries, norm, and w += y z re-read from shared memory
 #pragma unroll
     for (int tr = 0; tr < TR; ++tr) {
       const int64_t row = rb + tr;
-      double zn = 0.0;
       if (row < r1) {
-        zn = fma(c1, zo[tr], c2 * dot[tr]);
+        const double zn = fma(c1, zo[tr], c2 * dot[tr]);
         norm = fma(zn, zn, norm);
         if (q == 0 && tid == 0) {
           a.z[row] = zn;
           if (a.acc != nullptr) a.acc[row] = fma(ca, zn, a.acc[row]);
         }
-      }
+        const double* rowp = stage + ((int64_t)st * TR + tr) * stage_ld;
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
-        wv[p].x = fma(y[tr][p].x, zn, wv[p].x);
-        wv[p].y = fma(y[tr][p].y, zn, wv[p].y);
+        for (int p = 0; p < P; ++p) {
+          const int64_t cl = 2 * (tid + THREADS * p);
+          if (cl < ncol) {
+            const double2 y = *reinterpret_cast<const double2*>(rowp + cl);
+            wv[p].x = fma(y.x, zn, wv[p].x);
+            wv[p].y = fma(y.y, zn, wv[p].y);
+          }
+        }
       }
     }
     buf ^= 1;
@@ -234,13 +211,13 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   cq = (cq + 1) & ~int64_t(1);
   int vpt = 1;
   while (512 * vpt < cq) vpt *= 2;
-  int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8 / vpt, 32768 / (cq * 8)));
+  int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8, 65536 / (cq * 8)));
   int t2 = 1;
   while (t2 * 2 <= tr) t2 *= 2;
   tr = t2;
   const size_t stage_bytes = (size_t)tr * cq * 8;
   int nst = (int)std::min<size_t>(kMaxStages, kStageBudget / stage_bytes);
-  if (nst < 2) return false;
+  if (nst < 3) return false;    // one stage being reduced, one waiting for its refill, >= 1 in flight
   int nclusters = nsm / cl;
   if (nclusters < 1) nclusters = 1;
   const int64_t tiles = (R + tr - 1) / tr;
@@ -282,14 +259,14 @@ static cudaError_t launch_bulk_t(const RowPassArgs& a, const RowPassPlan& p, cud
   return cudaLaunchKernelEx(&cfg, rowpass_bulk_kernel<P, TR>, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
 }
 
-// only P * TR <= 8 is planned (the row tile lives in registers: 2 P TR doubles per thread)
 template <int P>
 static cudaError_t launch_bulk_p(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
-  if constexpr (P * 8 <= 8) { if (p.tr == 8) return launch_bulk_t<P, 8>(a, p, st); }
-  if constexpr (P * 4 <= 8) { if (p.tr == 4) return launch_bulk_t<P, 4>(a, p, st); }
-  if constexpr (P * 2 <= 8) { if (p.tr == 2) return launch_bulk_t<P, 2>(a, p, st); }
-  if (p.tr == 1) return launch_bulk_t<P, 1>(a, p, st);
-  return cudaErrorInvalidValue;
+  switch (p.tr) {
+    case 1: return launch_bulk_t<P, 1>(a, p, st);
+    case 2: return launch_bulk_t<P, 2>(a, p, st);
+    case 4: return launch_bulk_t<P, 4>(a, p, st);
+    default: return launch_bulk_t<P, 8>(a, p, st);
+  }
 }
 
 cudaError_t launch_rowpass_bulk(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {

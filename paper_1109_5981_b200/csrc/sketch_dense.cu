@@ -201,6 +201,7 @@ size_t sketch_dense_smem() { return sk::SMEM_BYTES; }
 
 cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st) {
   using namespace sk;
+  if (sketch_ws_supported(a)) return launch_sketch_ws(a, st);   // warp-specialized K2 (sketch_ws.cu)
   dim3 grid((unsigned)((a.k + BN - 1) / BN), (unsigned)((a.s + BM - 1) / BM), (unsigned)a.nsplit);
   const bool vec2 = (a.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
   cudaError_t e;

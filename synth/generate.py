@@ -179,8 +179,10 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
         nd = min(cfg["dense_cols"], n - nr) if n > nr else 0
         pool = n - nd
         nnz_row = nr + nd
-        width = pool / nr
-        strata = torch.arange(nr, **f64) * width
+        # integer strata [floor(i pool / nr), floor((i+1) pool / nr)): one uniform draw in
+        # each, so the nr random columns of a row are distinct and sorted
+        edges = (torch.arange(nr + 1, device=device, dtype=torch.int64) * pool) // nr
+        lo_e, wid = edges[:-1], (edges[1:] - edges[:-1]).to(torch.float64)
         cols_d = torch.arange(pool, n, device=device, dtype=torch.int64)
         rows = hi - lo
         colind = torch.empty(rows, nnz_row, dtype=torch.int32, device=device)
@@ -190,7 +192,7 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
             g0, g1 = g * BLOCK, min(L, (g + 1) * BLOCK)
             gen = _block_gen(seed, g, device)
             u = torch.rand(g1 - g0, nr, generator=gen, **f64)
-            cr = torch.clamp((strata + u * width).floor().to(torch.int64), max=pool - 1)
+            cr = lo_e + torch.minimum((u * wid).floor().to(torch.int64), (wid - 1).to(torch.int64))
             # one draw per disjoint increasing stratum: distinct and sorted
             ci = torch.cat([cr, cols_d.expand(g1 - g0, nd)], dim=1).to(torch.int32)
             vv = torch.randn(g1 - g0, nnz_row, generator=gen, **f64)

@@ -151,3 +151,17 @@ def test_csr_rejects_wide(ctx):
     A = _random_csr(50, 400, 3, 0, 1.0, 0, seed=1)
     with pytest.raises(LsrnError, match="EUNSUPPORTED"):
         ctx.sketch(_gpu_csr(A), 50, 400)
+
+
+@pytest.mark.parametrize("bad", ["dup", "unsorted", "range"])
+def test_csr_rejects_non_canonical(ctx, bad):
+    from paper_1109_5981_b200.lsrn import Csr, LsrnError
+    rowptr = torch.tensor([0, 3, 5, 7, 8, 9, 10], dtype=torch.int64)          # 6 x 5, tall
+    good = [0, 2, 3, 1, 3, 0, 4, 1, 2, 4]
+    cols = {"dup": [0, 2, 2, 1, 3, 0, 4, 1, 2, 4], "unsorted": [0, 3, 2, 1, 3, 0, 4, 1, 2, 4],
+            "range": [0, 2, 5, 1, 3, 0, 4, 1, 2, 4]}[bad]
+    ones = torch.ones(10, dtype=torch.float64).cuda()
+    ctx.sketch(Csr(rowptr.cuda(), torch.tensor(good, dtype=torch.int32).cuda(), ones), 6, 5, 1.5)
+    X = Csr(rowptr.cuda(), torch.tensor(cols, dtype=torch.int32).cuda(), ones)
+    with pytest.raises(LsrnError, match="EINVAL"):
+        ctx.sketch(X, 6, 5, 1.5)
