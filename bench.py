@@ -30,6 +30,8 @@ UNIT = "s"
 FP64_PEAK_TFLOPS = 36.9     # DMMA.8x8x4 burst peak measured on this pool (profiles/fp64_peak.jsonl)
 FP64_PEAK_NOTE = ("fp64 DMMA peak measured by tools/microbench/fp64_peak.cu on this pool's B200 "
                   "(MEASURED_PEAKS.json has no fp64 entry); cuBLAS DGEMM 8192^3 measured 35.4")
+DFMA_PEAK_TFLOPS = 36.8     # DFMA (FP64 ALU) peak measured by the same microbenchmark
+DFMA_PEAK_NOTE = "fp64 DFMA peak measured by tools/microbench/fp64_peak.cu (profiles/r01_fp64_peak.jsonl)"
 
 
 def load_peaks():
@@ -107,7 +109,7 @@ def cpu_baseline(cfg_name, solver, m_sample):
     cfg = CONFIGS[cfg_name]
     p = make_problem(cfg_name, m=m_sample, n=cfg["n"]) if cfg["m"] >= cfg["n"] else \
         make_problem(cfg_name, m=cfg["m"], n=m_sample)
-    A = p.dense_A().numpy()
+    A = p.to_scipy() if p.kind == "csr" else p.dense_A().numpy()
     t0 = time.perf_counter()
     rep = orc_solve(A, p.b.numpy(), gamma=cfg["gamma"], lam=cfg["lam"], solver=solver, precise_g=False)
     wall = time.perf_counter() - t0
@@ -156,7 +158,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--solver", default="lsqr", choices=["lsqr", "cs"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -188,7 +190,9 @@ def main():
     L = max(m, n)
     lo, hi = lsrn_dist.shard_bounds(L, world, rank)
     p = make_problem(args.config, device=dev, shard=(lo, hi) if world > 1 else None)
-    X, b = p.X, p.b
+    csr = p.kind == "csr"
+    X = lsrn.Csr(p.rowptr, p.colind, p.val) if csr else p.X
+    b = p.b
     stream = torch.cuda.Stream(dev)
     torch.cuda.synchronize()
     ctx = lsrn_dist.context(stream=stream)
@@ -244,30 +248,47 @@ def main():
     s_ = reps[-1]["s"]
     k = min(m, n)
     cnt = hi - lo
-    sketch_flops = 2.0 * s_ * k * cnt
+    nnz = int(p.val.numel()) if csr else cnt * k
+    sketch_flops = 2.0 * s_ * nnz
     peaks, peak_src = load_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    lp_bytes = cnt * (8.0 * k + 16.0)            # per row: the row of A once + u_j read and write
+    # algorithmic bytes of one long pass, from the library: dense 8k+16 per row;
+    # CSR 12 per nonzero + 24 per row + 12 per light-CSC entry
+    lp_bytes = statistics.median(float(st["long_pass_bytes"]) for st in stats)
     sketch_tf = sketch_flops / (sk_ms * 1e-3) / 1e12
     lp_gbs = lp_bytes / (lp_ms * 1e-3) / 1e9 if lp_ms > 0 else None
     iters = reps[-1]["iters"]
     # dominant kernel by share of the step
     sketch_share = (sk_ms / 1e3) / (ms / 1e3)
     lp_share = (lp_ms / 1e3) * max(iters + 1, 1) / (ms / 1e3)
-    roof_sketch = {"kernel": "sketch_dense_kernel (K1+K2, DMMA)", "bound": "tensor", "achieved": sketch_tf,
-                   "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": sketch_tf / FP64_PEAK_TFLOPS,
-                   "traffic": None, "algorithmic": f"2*s*k*L = {sketch_flops:.4g} flop per launch",
-                   "peak_source": FP64_PEAK_NOTE, "share_of_step": sketch_share}
-    roof_lp = {"kernel": "rowpass_kernel long pass (K6)", "bound": "hbm", "achieved": lp_gbs, "peak": hbm_peak,
+    if csr:
+        roof_sketch = {"kernel": "csr_sketch_heavy/light (K4, FP64 FMA + in-kernel RNG)", "bound": "alu",
+                       "achieved": sketch_tf, "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                       "frac": sketch_tf / DFMA_PEAK_TFLOPS, "traffic": None,
+                       "algorithmic": f"2*s*nnz = {sketch_flops:.4g} flop per sketch (+ s*cnt normals, not counted)",
+                       "peak_source": DFMA_PEAK_NOTE, "share_of_step": sketch_share}
+    else:
+        roof_sketch = {"kernel": "sketch_ws_kernel (K1+K2, DMMA, warp-specialized)", "bound": "tensor",
+                       "achieved": sketch_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                       "frac": sketch_tf / FP64_PEAK_TFLOPS, "traffic": None,
+                       "algorithmic": f"2*s*k*L = {sketch_flops:.4g} flop per launch",
+                       "peak_source": FP64_PEAK_NOTE, "share_of_step": sketch_share}
+    roof_lp = {"kernel": "csr_rowdot + csr_colgather (K6-CSR)" if csr else "rowpass_bulk_kernel long pass (K6)",
+               "bound": "hbm", "achieved": lp_gbs, "peak": hbm_peak,
                "unit": "GB/s", "frac": (lp_gbs / hbm_peak) if lp_gbs else None, "traffic": None,
-               "algorithmic": f"rows*(8k+16) = {lp_bytes:.4g} B per launch",
+               "algorithmic": f"{lp_bytes:.4g} B per pass ({'12 nnz + 24 rows + 12 light-CSC' if csr else 'rows*(8k+16)'})",
                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", "share_of_step": lp_share}
     roofline = roof_sketch if sketch_share >= lp_share else roof_lp
 
     # ---- end to end through the C ABI with HOST buffers (H2D of A, b and D2H of x inside)
     e2e = None
     if not args.no_e2e:
-        Xh = X.cpu().pin_memory()
+        if csr:
+            Xh = lsrn.Csr(p.rowptr.cpu().pin_memory(), p.colind.cpu().pin_memory(), p.val.cpu().pin_memory())
+            h2d_A = int(p.rowptr.numel() * 8 + p.colind.numel() * 4 + p.val.numel() * 8)
+        else:
+            Xh = X.cpu().pin_memory()
+            h2d_A = int(Xh.numel() * 8)
         bh = b.cpu().pin_memory()
         nsteps = min(3, args.steps)
         barrier()
@@ -286,7 +307,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": float(te.item()) / 1e3, "unit": UNIT,
-               "h2d_bytes_per_step": int(Xh.numel() * 8 + bh.numel() * 8),
+               "h2d_bytes_per_step": h2d_A + int(bh.numel() * 8),
                "d2h_bytes_per_step": int(xh.numel() * 8),
                "steps": nsteps}
         del Xh, bh
@@ -306,7 +327,8 @@ def main():
             "config": {"workload": args.config, "shape": [m, n], "s": s_, "r": reps[-1]["r"],
                        "solver": args.solver, "iters": iters, "gamma": cfg["gamma"], "lambda": cfg["lam"],
                        "tol": 1e-14, "parallelism": f"row-shard x{world}" if m >= n else f"col-shard x{world}",
-                       "l2": "inputs larger than L2 (A = %.2f GB), no flush" % (cnt * k * 8 / 1e9)},
+                       "l2": "inputs larger than L2 (A = %.2f GB), no flush" % (
+                           (nnz * 12 + cnt * 8) / 1e9 if csr else cnt * k * 8 / 1e9)},
             "stages_s": {"sketch": t_sketch, "allreduce": t_ar, "svd": t_svd, "iterations": t_iter,
                          "hot_path_excl_svd": t_sketch + t_ar + t_iter},
             "sketch_tflops": sketch_tf, "matvec_gbs": lp_gbs,

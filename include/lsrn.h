@@ -128,11 +128,6 @@ lsrn_status lsrn_ctx_create(lsrn_ctx** ctx, void* stream, int nranks, int rank,
                             const void* nccl_id);
 lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
 
-/* Testing aid: split this rank's shard into `p` contiguous sub-shards that are
- * processed as if they were separate ranks (per-shard partial sums combined in
- * shard order where a real run would call NCCL).  p = 1 restores normal runs. */
-lsrn_status lsrn_ctx_set_virtual_shards(lsrn_ctx* ctx, int p);
-
 /* Record CUDA events around every long-pass (K6) launch of the next solves so
  * lsrn_last_stats reports its average duration (adds event nodes to the graph). */
 lsrn_status lsrn_ctx_set_profiling(lsrn_ctx* ctx, int on);

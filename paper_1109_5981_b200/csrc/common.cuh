@@ -15,6 +15,15 @@ LSRN_DEV double warp_sum(double v) {
   return v;
 }
 
+// Fixed-order warp sum of p[0..n) read through L2 (__ldcg: written by other CTAs
+// of the same grid): lane l adds p[l], p[l+32], ... in order, then a butterfly.
+// Deterministic for a given n; every lane returns the total.  Call with the full warp.
+LSRN_DEV double warp_sum_l2(const double* p, int64_t n) {
+  double v = 0.0;
+  for (int64_t i = threadIdx.x & 31; i < n; i += 32) v += __ldcg(p + i);
+  return warp_sum(v);
+}
+
 // cp.async 16 B global -> shared with zero fill of the bytes past src_bytes.
 LSRN_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

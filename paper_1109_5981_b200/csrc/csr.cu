@@ -378,13 +378,13 @@ csr_colgather_kernel(const int64_t* __restrict__ colptr, const int32_t* __restri
     last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && threadIdx.x < 32) {
     __threadfence();
-    double n = 0.0;
-    for (int g = 0; g < nparts; ++g) n += __ldcg(npart + g);
-    for (unsigned bb = 0; bb < gridDim.x; ++bb) n += __ldcg(blockpart + bb);
-    out[k] = n;
-    *counter = 0u;
+    const double n = warp_sum_l2(npart, nparts) + warp_sum_l2(blockpart, gridDim.x);
+    if (threadIdx.x == 0) {
+      out[k] = n;
+      *counter = 0u;
+    }
   }
 }
 

@@ -120,10 +120,10 @@ __global__ void lsqr_after_v_kernel(LsqrState* s, const double* comm, int64_t C,
     last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
-  if (!(last && threadIdx.x == 0)) return;
+  if (!(last && threadIdx.x < 32)) return;
   __threadfence();
-  double ynorm2 = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) ynorm2 += __ldcg(ypart + b);
+  const double ynorm2 = warp_sum_l2(ypart, gridDim.x);
+  if (threadIdx.x != 0) return;
   *counter = 0u;
   // publish the new scalars (single writer)
   s->alpha = alpha;

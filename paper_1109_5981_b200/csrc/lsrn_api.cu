@@ -688,12 +688,6 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* c) {
   return LSRN_OK;
 }
 
-lsrn_status lsrn_ctx_set_virtual_shards(lsrn_ctx* c, int p) {
-  if (!c) return set_error(LSRN_EINVAL, "ctx is NULL");
-  if (p == 1) return LSRN_OK;
-  return set_error(LSRN_EUNSUPPORTED, "virtual shards are not implemented in this build");
-}
-
 lsrn_status lsrn_ctx_set_profiling(lsrn_ctx* c, int on) {
   if (!c) return set_error(LSRN_EINVAL, "ctx is NULL");
   c->profile = on != 0;

@@ -167,49 +167,61 @@ rowpass_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL) {
 }
 
 // --------------------------------------------------------------- col reduce
-__global__ void colreduce_kernel(ColReduceArgs a) {
-  __shared__ double sh[256 / 32];
+// Block (32 columns) x (16 partial groups): thread (x, y) sums partials g = y,
+// y + 16, ... of column c = 32 blockIdx.x + x; the 16 group sums are added in
+// fixed order.  The last block to finish adds the norm partials (one warp, fixed
+// order).  Deterministic, and wide enough to hide L2 latency (the first version,
+// one thread per column looping over all partials, took ~28 us per call on c2).
+constexpr int CR_X = 32, CR_Y = 16;
+
+__global__ void __launch_bounds__(CR_X * CR_Y)
+colreduce_kernel(ColReduceArgs a) {
+  __shared__ double sh[CR_Y][CR_X + 1];
   __shared__ bool last;
   if (a.done != nullptr && *a.done != 0) return;
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  double nI = 0.0;
-  if (c < a.C) {
-    double w = 0.0;
-    for (int g = 0; g < a.nparts; ++g) w += a.wpart[(int64_t)g * a.C + c];
-    if (a.zI != nullptr) {
-      const double zn = fma(a.coef[0], a.zI[c], a.coef[1] * (a.sI * a.t[c]));
-      a.zI[c] = zn;
-      w = fma(a.sI, zn, w);
-      nI = zn * zn;
+  const int x = threadIdx.x, y = threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * CR_X + x;
+  double w = 0.0;
+  if (c < a.C)
+    for (int g = y; g < a.nparts; g += CR_Y) w += a.wpart[(int64_t)g * a.C + c];
+  sh[y][x] = w;
+  __syncthreads();
+  if (y == 0) {
+    double nI = 0.0;
+    if (c < a.C) {
+      double t = 0.0;
+#pragma unroll
+      for (int yy = 0; yy < CR_Y; ++yy) t += sh[yy][x];
+      if (a.zI != nullptr) {
+        const double zn = fma(a.coef[0], a.zI[c], a.coef[1] * (a.sI * a.t[c]));
+        a.zI[c] = zn;
+        t = fma(a.sI, zn, t);
+        nI = zn * zn;
+      }
+      a.out[c] = t;
     }
-    a.out[c] = w;
-  }
-  double s = warp_sum(nI);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += sh[w];
-    a.blockpart[blockIdx.x] = b;
-    __threadfence();
-    const unsigned ticket = atomicAdd(a.counter, 1u);
-    last = (ticket == gridDim.x - 1);
+    const double bsum = warp_sum(nI);
+    if (x == 0) {
+      a.blockpart[blockIdx.x] = bsum;
+      __threadfence();
+      last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+    }
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last && y == 0) {
     __threadfence();
-    double n = 0.0;
-    for (int g = 0; g < a.nparts; ++g) n += __ldcg(a.npart + g);
-    for (unsigned b = 0; b < gridDim.x; ++b) n += __ldcg(a.blockpart + b);
-    a.out[a.C] = n;
-    *a.counter = 0u;
+    const double n = warp_sum_l2(a.npart, a.nparts) + warp_sum_l2(a.blockpart, gridDim.x);
+    if (x == 0) {
+      a.out[a.C] = n;
+      *a.counter = 0u;
+    }
   }
 }
 
-int colreduce_blocks(int64_t C) { return (int)((C + 255) / 256); }
+int colreduce_blocks(int64_t C) { return (int)((C + CR_X - 1) / CR_X); }
 
 cudaError_t launch_colreduce(const ColReduceArgs& a, cudaStream_t st) {
-  colreduce_kernel<<<colreduce_blocks(a.C), 256, 0, st>>>(a);
+  colreduce_kernel<<<colreduce_blocks(a.C), dim3(CR_X, CR_Y), 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -14,8 +14,17 @@
 //     64 x 16 G tile of each k-block into a second ring (4 pairs per thread);
 //   warpgroups 1-2 (8 warps, setmaxnreg 200): DMMA.8x8x4 on 32 x 64 warp tiles,
 //     never touching RNG, released stage by stage with mbarriers.
-// The RNG still shares the FP64 pipe with DMMA (measured) but now
-// runs concurrently with it instead of in a separate phase.
+// The RNG shares the FP64 pipe with DMMA (measured), so each
+// normal must be generated as few times as possible: the CTAs of a cluster of
+// CL along N (same sketch rows, same k-range, different column tiles) need the
+// SAME G tile, so CTA q generates rows [q BM/CL, (q+1) BM/CL) of it into its own
+// ring and pushes that slice to the other CL-1 CTAs with async-proxy
+// shared->shared bulk copies (cp.async.bulk.shared::cluster.shared::cta) that
+// complete on the destination's `gfull` barrier; consumers release a G stage on
+// every CTA of the cluster with plain remote arrives.  RNG work per CTA drops by
+// CL.  (Without the sharing the consumers waited on the G ring 29 % of the time;
+// distributing with st.shared::cluster + release/acquire.cluster barriers cost
+// a MEMBAR.GPU / L1 invalidate per stage and ran 2x slower.)
 //
 // Requirements (else the caller uses sketch_dense_kernel): ld even, X 16-byte
 // aligned, k even (every bulk row segment is a multiple of 16 bytes).
@@ -37,6 +46,42 @@ constexpr int NCONS_WARPS = 8;
 constexpr size_t SMEM_BYTES = sizeof(double) * (size_t)(NSX * X_STAGE + NSG * G_STAGE) + 128;
 }  // namespace ws
 
+namespace {
+LSRN_DEV unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+LSRN_DEV unsigned map_rank(const void* p, unsigned rank) {     // shared::cluster address in CTA `rank`
+  unsigned a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+// remote arrive (default .release.cta semantics: only orders this thread's prior
+// shared-memory reads, which is all a consumer release needs)
+LSRN_DEV void mbar_arrive_remote(unsigned addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+// async-proxy copy of `bytes` from this CTA's shared memory into CTA-rank shared
+// memory (dst, bar: shared::cluster addresses), completing tx on the remote barrier
+LSRN_DEV void bulk_s2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "r"(smem_u32(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+LSRN_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+LSRN_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory"); }
+LSRN_DEV void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+LSRN_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+}  // namespace
+
+template <int CL>
 __global__ void __launch_bounds__(ws::THREADS, 1)
 sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
                  uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride) {
@@ -53,18 +98,24 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
   const int64_t r_end = min(rows, r_begin + rows_per_split);
   const int nk = (r_end > r_begin) ? (int)((r_end - r_begin + BK - 1) / BK) : 0;
 
+  const unsigned qrank = (CL > 1) ? cluster_rank() : 0u;
+  constexpr int SLICE_ROWS = BM / CL;                  // G rows generated by this CTA
+  constexpr unsigned SLICE_BYTES = (unsigned)(SLICE_ROWS * G_LD * sizeof(double));
   if (tid == 0) {
     for (int i = 0; i < NSX; ++i) {
       mbar_init(&xfull[i], 1);
       mbar_init(&xempty[i], NCONS_WARPS);
     }
     for (int i = 0; i < NSG; ++i) {
-      mbar_init(&gfull[i], 4);                          // one arrival per producer warp
-      mbar_init(&gempty[i], NCONS_WARPS);
+      mbar_init(&gfull[i], 1);                          // local producer leader (+ tx of CL-1 remote slices)
+      mbar_init(&gempty[i], NCONS_WARPS * CL);          // one per consumer warp of each CTA of the cluster
     }
     mbar_fence_init();
   }
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync_all();                                 // every CTA's barriers exist before remote traffic
+  else
+    __syncthreads();
 
   if (warp < 4) {
     // ------------------------------------------------------------ producers
@@ -91,21 +142,45 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
           for (int rr = 0; rr < nrow; ++rr) bulk_g2s(dst + rr * A_LD, X + (rbase + rr) * ld + n0, seg_bytes, &xfull[sx]);
         }
       }
-      // G tile: 64 x 16 normals = 512 Box-Muller pairs, 4 per producer thread
+      // G stage sg must be free on every CTA of the cluster, and (CL > 1) the bulk
+      // copies that last read our slice of it must have finished reading
       if (kb >= NSG) mbar_wait(&gempty[sg], pg);
+      if (CL > 1) {
+        if (ptid == 0) bulk_wait_read<NSG - 1>();
+        named_bar(1, 128);
+      }
       double* gdst = Gs + sg * G_STAGE;
       const int64_t jbase = lo + rbase;
+      constexpr int PAIRS = (SLICE_ROWS / 2) * BK;       // pairs per CTA per k-block
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < (PAIRS + 127) / 128; ++t) {
         const int p = ptid + 128 * t;
-        const int qp = p / BK, kk = p % BK;
-        double z0 = 0.0, z1 = 0.0;
-        if (kk < nrow) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), z0, z1);
-        gdst[(2 * qp) * G_LD + kk] = z0;
-        gdst[(2 * qp + 1) * G_LD + kk] = z1;
+        if (PAIRS % 128 == 0 || p < PAIRS) {
+          const int qp = (int)qrank * (SLICE_ROWS / 2) + p / BK, kk = p % BK;
+          double z0 = 0.0, z1 = 0.0;
+          if (kk < nrow) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), z0, z1);
+          gdst[(2 * qp) * G_LD + kk] = z0;
+          gdst[(2 * qp + 1) * G_LD + kk] = z1;
+        }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&gfull[sg]);           // release: this warp's G stores
+      if (CL > 1) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic -> async proxy
+      named_bar(1, 128);                                  // the whole slice is written
+      if (ptid == 0) {
+        mbar_arrive_expect_tx(&gfull[sg], SLICE_BYTES * (unsigned)(CL - 1));   // local slice: this arrive
+        if (CL > 1) {
+          const double* src = gdst + (int64_t)qrank * SLICE_ROWS * G_LD;
+#pragma unroll
+          for (unsigned r = 1; r < (unsigned)CL; ++r) {
+            const unsigned dr = (qrank + r) % (unsigned)CL;
+            bulk_s2s(map_rank(src, dr), src, SLICE_BYTES, map_rank(&gfull[sg], dr));
+          }
+          bulk_commit();
+        }
+      }
+    }
+    if (CL > 1) {
+      if (ptid == 0) bulk_wait_read<0>();
+      cluster_sync_all();                               // no CTA leaves while others may still signal it
     }
     return;
   }
@@ -141,7 +216,12 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(&xempty[sx]);
-      mbar_arrive(&gempty[sg]);
+      if (CL == 1) {
+        mbar_arrive(&gempty[sg]);
+      } else {
+#pragma unroll
+        for (unsigned r = 0; r < (unsigned)CL; ++r) mbar_arrive_remote(map_rank(&gempty[sg], r));
+      }
     }
   }
 
@@ -160,21 +240,51 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
       }
     }
   }
+  if (CL > 1) cluster_sync_all();
 }
 
 bool sketch_ws_supported(const SketchDenseArgs& a) {
   return (a.ld % 2 == 0) && (a.k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
 }
 
+template <int CL>
+static cudaError_t launch_ws_t(const SketchDenseArgs& a, dim3 grid, cudaStream_t st) {
+  using namespace ws;
+  cudaError_t e = cudaFuncSetAttribute(sketch_ws_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
+                            a.rows_per_split, a.out, a.out_split_stride);
+}
+
+int sketch_ws_cluster(int64_t k) {
+  const int64_t nt = (k + ws::BN - 1) / ws::BN;
+  for (int cl : {8, 4, 2})
+    if (nt % cl == 0) return cl;
+  return 1;
+}
+
 cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st) {
   using namespace ws;
   dim3 grid((unsigned)((a.k + BN - 1) / BN), (unsigned)((a.s + BM - 1) / BM), (unsigned)a.nsplit);
-  cudaError_t e = cudaFuncSetAttribute(sketch_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  sketch_ws_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed, a.rows_per_split,
-                                                      a.out, a.out_split_stride);
-  return cudaGetLastError();
+  switch (sketch_ws_cluster(a.k)) {
+    case 8: return launch_ws_t<8>(a, grid, st);
+    case 4: return launch_ws_t<4>(a, grid, st);
+    case 2: return launch_ws_t<2>(a, grid, st);
+    default: return launch_ws_t<1>(a, grid, st);
+  }
 }
 
 }  // namespace lsrn

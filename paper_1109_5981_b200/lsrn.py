@@ -22,7 +22,7 @@ STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE
 
 # every symbol include/lsrn.h declares
 EXPORTS = ["lsrn_last_error", "lsrn_version", "lsrn_nccl_unique_id", "lsrn_ctx_create", "lsrn_ctx_destroy",
-           "lsrn_ctx_set_virtual_shards", "lsrn_ctx_set_profiling", "lsrn_workspace_size", "lsrn_sketch",
+           "lsrn_ctx_set_profiling", "lsrn_workspace_size", "lsrn_sketch",
            "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_last_stats"]
 
 
@@ -74,7 +74,6 @@ def lib():
             "lsrn_nccl_unique_id": [vp],
             "lsrn_ctx_create": [ctypes.POINTER(vp), vp, i32, i32, vp],
             "lsrn_ctx_destroy": [vp],
-            "lsrn_ctx_set_virtual_shards": [vp, i32],
             "lsrn_ctx_set_profiling": [vp, i32],
             "lsrn_workspace_size": [vp, ctypes.POINTER(Matrix), ctypes.POINTER(Opts), ctypes.POINTER(sz)],
             "lsrn_sketch": [vp, ctypes.POINTER(Matrix), dbl, dbl, u64, vp, sz, vp, ctypes.POINTER(i64)],

@@ -59,6 +59,10 @@ def test_gaussian_entries(ctx):
     (1000, 33, 2.1, 0.0, 1),        # odd s = 70, ld = 34 padded ... ld even
     (1000, 33, 2.0, 0.0, 2),        # ld = 35 odd -> 8-byte path
     (3000, 64, 2.0, 0.25, 0),       # tall Tikhonov block
+    (1500, 512, 2.0, 0.0, 0),       # 2 N-tiles: G shared by a 2-CTA cluster
+    (1200, 1024, 1.5, 0.0, 0),      # 4 N-tiles: 4-CTA cluster
+    (2100, 2048, 1.2, 0.0, 2),      # 8 N-tiles: 8-CTA cluster, padded ld
+    (1601, 1536, 1.1, 0.5, 0),      # 6 N-tiles: 2-CTA clusters, Tikhonov block, ragged K
 ])
 def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad):
     g = torch.Generator().manual_seed(m * 7 + n)
