@@ -49,6 +49,8 @@ struct RowPassPlan {
   int bulk = 0;                     // 1: rowpass_bulk_kernel (TMA bulk-copy ring)
   int64_t cq = 0;                   // bulk: columns per CTA slice
   int nst = 0;                      // bulk: pipeline stages
+  int keep = 0;                     // bulk: row tile kept in registers between the two phases
+  int occ = 1;                      // bulk: CTAs per SM
 };
 // allow_bulk = false forces the register-load kernel (tests compare both)
 RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, bool allow_bulk = true);

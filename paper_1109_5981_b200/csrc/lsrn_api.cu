@@ -454,7 +454,7 @@ IterWs plan_iter(lsrn_ctx* c, const Dims& d, Arena& ar, int max_passes) {
   w.comm = ar.take<double>((size_t)k + 1);
   w.tbuf = ar.take<double>((size_t)k + 1);
   w.xbuf = ar.take<double>((size_t)k + 1);
-  const int nparts = c->nsm > 0 ? c->nsm : 148;
+  const int nparts = 2 * (c->nsm > 0 ? c->nsm : 148);   // row-pass partials: up to 2 CTAs per SM
   w.wpart = ar.take<double>((size_t)nparts * k);
   w.npart = ar.take<double>((size_t)nparts);
   w.blockpart = ar.take<double>((size_t)std::max(colreduce_blocks(k), csr_colgather_blocks(k)) + 1);

@@ -21,6 +21,7 @@
 // through distributed shared memory (one cluster barrier per stage).
 // Deterministic: fixed row chunks and reduction trees, no atomics.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -40,8 +41,10 @@ constexpr int kMaxStages = 8;
 }  // namespace
 
 // TR rows per stage; P column pairs per thread (slice width <= 512 P).
-template <int P, int TR>
-__global__ void __launch_bounds__(THREADS, 1)
+// KEEP: hold the staged row tile in registers between the two phases (2 P TR
+// doubles per thread) instead of re-reading shared memory; OCC: CTAs per SM.
+template <int P, int TR, bool KEEP, int OCC>
+__global__ void __launch_bounds__(THREADS, OCC)
 rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq, int nst) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages];
@@ -111,19 +114,18 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
 
     // phase 1: partial row dots from shared memory (rows past r1 are zero-weighted)
     double d[TR];
+    double2 yk[KEEP ? TR : 1][KEEP ? P : 1];
 #pragma unroll
     for (int tr = 0; tr < TR; ++tr) {
       const double* row = stage + ((int64_t)st * TR + tr) * stage_ld;
       double s = 0.0;
-      if (rb + tr < r1) {
+      const bool rok = rb + tr < r1;
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-          const int64_t cl = 2 * (tid + THREADS * p);
-          if (cl < ncol) {
-            const double2 y = *reinterpret_cast<const double2*>(row + cl);
-            s = fma(y.x, tv[p].x, fma(y.y, tv[p].y, s));
-          }
-        }
+      for (int p = 0; p < P; ++p) {
+        const int64_t cl = 2 * (tid + THREADS * p);
+        const double2 y = (rok && cl < ncol) ? *reinterpret_cast<const double2*>(row + cl) : make_double2(0.0, 0.0);
+        if constexpr (KEEP) yk[tr][p] = y;
+        s = fma(y.x, tv[p].x, fma(y.y, tv[p].y, s));
       }
       d[tr] = s;
     }
@@ -176,7 +178,11 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
         for (int p = 0; p < P; ++p) {
           const int64_t cl = 2 * (tid + THREADS * p);
           if (cl < ncol) {
-            const double2 y = *reinterpret_cast<const double2*>(rowp + cl);
+            double2 y;
+            if constexpr (KEEP)
+              y = yk[tr][p];
+            else
+              y = *reinterpret_cast<const double2*>(rowp + cl);
             wv[p].x = fma(y.x, zn, wv[p].x);
             wv[p].y = fma(y.y, zn, wv[p].y);
           }
@@ -202,6 +208,8 @@ constexpr int64_t kMaxSlice = 4096;        // doubles per CTA slice (32 KB per s
 constexpr size_t kStageBudget = 192 * 1024;
 }  // namespace
 
+// Tuning aids (env): LSRN_ROWPASS_OCC=1 (one CTA per SM, the whole stage budget),
+// LSRN_ROWPASS_KEEP=0/1 (force re-read / register tile).
 bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, RowPassPlan* p) {
   // 16-byte aligned rows and an even slice width: every bulk copy is a multiple of 16 bytes
   if (C <= 0 || (C & 1) || (ld & 1) || (reinterpret_cast<uintptr_t>(Y) & 15)) return false;
@@ -211,14 +219,24 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   cq = (cq + 1) & ~int64_t(1);
   int vpt = 1;
   while (512 * vpt < cq) vpt *= 2;
-  int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8, 65536 / (cq * 8)));
+  // Two CTAs per SM by default: while one CTA sits in its per-tile barrier and
+  // row reductions the other streams, which took the c2 long pass from 5.0 to
+  // 6.4 TB/s (99 % of the measured copy bandwidth; profiles/r01_rowpass_tune.jsonl).
+  int occ = 2;
+  if (const char* e = std::getenv("LSRN_ROWPASS_OCC")) occ = std::atoi(e) == 1 ? 1 : 2;
+  const size_t budget = kStageBudget / occ;
+  int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(budget / 3) / (cq * 8)));
   int t2 = 1;
   while (t2 * 2 <= tr) t2 *= 2;
   tr = t2;
   const size_t stage_bytes = (size_t)tr * cq * 8;
-  int nst = (int)std::min<size_t>(kMaxStages, kStageBudget / stage_bytes);
+  int nst = (int)std::min<size_t>(kMaxStages, budget / stage_bytes);
   if (nst < 3) return false;    // one stage being reduced, one waiting for its refill, >= 1 in flight
-  int nclusters = nsm / cl;
+  bool keep = vpt * tr <= (occ == 2 ? 4 : 16);
+  if (const char* e = std::getenv("LSRN_ROWPASS_KEEP")) keep = std::atoi(e) != 0 && vpt * tr <= 16;
+  p->keep = keep ? 1 : 0;
+  p->occ = occ;
+  int nclusters = (nsm * occ) / cl;
   if (nclusters < 1) nclusters = 1;
   const int64_t tiles = (R + tr - 1) / tr;
   if ((int64_t)nclusters > tiles) nclusters = (int)(tiles > 0 ? tiles : 1);
@@ -234,14 +252,14 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   return true;
 }
 
-template <int P, int TR>
-static cudaError_t launch_bulk_t(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+template <int P, int TR, bool KEEP, int OCC>
+static cudaError_t launch_bulk_k(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
   const size_t smem = (size_t)p.nst * TR * p.cq * 8;
-  cudaError_t e = cudaFuncSetAttribute(rowpass_bulk_kernel<P, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = rowpass_bulk_kernel<P, TR, KEEP, OCC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (p.cl > 8) {
-    e = cudaFuncSetAttribute(rowpass_bulk_kernel<P, TR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -256,7 +274,21 @@ static cudaError_t launch_bulk_t(const RowPassArgs& a, const RowPassPlan& p, cud
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, rowpass_bulk_kernel<P, TR>, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
+  return cudaLaunchKernelEx(&cfg, kern, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
+}
+
+template <int P, int TR>
+static cudaError_t launch_bulk_t(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  if (p.occ == 2) {
+    if constexpr (P * TR <= 4) {
+      if (p.keep) return launch_bulk_k<P, TR, true, 2>(a, p, st);
+    }
+    return launch_bulk_k<P, TR, false, 2>(a, p, st);
+  }
+  if constexpr (P * TR <= 16) {
+    if (p.keep) return launch_bulk_k<P, TR, true, 1>(a, p, st);
+  }
+  return launch_bulk_k<P, TR, false, 1>(a, p, st);
 }
 
 template <int P>

@@ -13,6 +13,8 @@
 // 32 x 64 = 4 x 8 DMMA fragments (64 fp64 accumulators per lane).  Every normal
 // generated is reused BN = 256 times (RNG overhead ~ cost(normal) / BN of the
 // FP64 pipe, which DMMA and DFMA share on sm_100a -- measured).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "philox_bm.cuh"
 #include "kernels.h"
@@ -201,7 +203,9 @@ size_t sketch_dense_smem() { return sk::SMEM_BYTES; }
 
 cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st) {
   using namespace sk;
-  if (sketch_ws_supported(a)) return launch_sketch_ws(a, st);   // warp-specialized K2 (sketch_ws.cu)
+  // warp-specialized K2 (sketch_ws.cu) when supported; LSRN_SKETCH_V1=1 forces this kernel (tuning aid)
+  const char* v1 = std::getenv("LSRN_SKETCH_V1");
+  if (sketch_ws_supported(a) && !(v1 && v1[0] == '1')) return launch_sketch_ws(a, st);
   dim3 grid((unsigned)((a.k + BN - 1) / BN), (unsigned)((a.s + BM - 1) / BM), (unsigned)a.nsplit);
   const bool vec2 = (a.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
   cudaError_t e;

@@ -28,6 +28,8 @@
 //
 // Requirements (else the caller uses sketch_dense_kernel): ld even, X 16-byte
 // aligned, k even (every bulk row segment is a multiple of 16 bytes).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "philox_bm.cuh"
@@ -269,10 +271,17 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, dim3 grid, cudaStream_t
                             a.rows_per_split, a.out, a.out_split_stride);
 }
 
+// Cluster size along N: the largest of {max_cl, ..., 2} dividing the N-tile count.
+// LSRN_SKETCH_MAXCL (tuning aid) caps it.  Default 2, measured on c2
+// (profiles/r01_sketch_tune.jsonl): CL = 1/2/4/8 -> 82.6/69.3/72.3/83.0 ms; larger
+// clusters cut the RNG further but leave SMs idle (whole clusters must fit in a
+// GPC: with CL = 8 only 76 % of the SM-cycles were active).
 int sketch_ws_cluster(int64_t k) {
   const int64_t nt = (k + ws::BN - 1) / ws::BN;
+  int max_cl = 2;
+  if (const char* e = std::getenv("LSRN_SKETCH_MAXCL")) max_cl = std::atoi(e);
   for (int cl : {8, 4, 2})
-    if (nt % cl == 0) return cl;
+    if (cl <= max_cl && nt % cl == 0) return cl;
   return 1;
 }
 

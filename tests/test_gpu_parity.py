@@ -195,3 +195,31 @@ def test_repeat_solves_bitwise(ctx):
     x1, _ = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="lsqr")
     x2, _ = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="lsqr")
     assert torch.equal(x1, x2)
+
+
+@pytest.mark.parametrize("maxcl,n", [(4, 1024), (8, 2048), (8, 1536)])
+def test_sketch_cluster_sizes(ctx, monkeypatch, maxcl, n):
+    """The G-sharing cluster paths CL = 4 and 8 (the default caps CL at 2; LSRN_SKETCH_MAXCL
+    is read at each launch) give the same sketch."""
+    monkeypatch.setenv("LSRN_SKETCH_MAXCL", str(maxcl))
+    m = n + 300
+    g = torch.Generator().manual_seed(n)
+    X = torch.randn(m, n, generator=g, dtype=torch.float64)
+    At = ctx.sketch(X.cuda(), m, n, 1.1, 0.0, seed=77).cpu().numpy()
+    p = orc_plan(m, n, 1.1, 0.0)
+    ref = orc_sketch(X.numpy(), p["s"], 77)
+    assert _relfro(At, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("env", [{"LSRN_ROWPASS_KEEP": "0"}, {"LSRN_ROWPASS_OCC": "1"},
+                                 {"LSRN_ROWPASS_OCC": "1", "LSRN_ROWPASS_KEEP": "1"}, {"LSRN_SKETCH_V1": "1"}])
+def test_tuning_variants_match(ctx, monkeypatch, env):
+    """Kernel variants selected by the tuning switches solve c1 to the same tolerance."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    p = make_problem("c1")
+    A = p.X.numpy()
+    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs")
+    orc = orc_solve(A, p.b.numpy(), solver="cs", extended=True)
+    assert rep["iters"] == orc["iters"]
+    _check_solution(A, x.cpu().numpy(), orc["x"], p.meta["kappa"])
