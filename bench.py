@@ -34,6 +34,16 @@ DFMA_PEAK_TFLOPS = 36.8     # DFMA (FP64 ALU) peak measured by the same microben
 DFMA_PEAK_NOTE = "fp64 DFMA peak measured by tools/microbench/fp64_peak.cu (profiles/r01_fp64_peak.jsonl)"
 
 
+def load_traffic(workload):
+    """DRAM bytes per launch of the dominant kernels from one committed ncu --set full
+    capture (profiles/traffic.json, written by tools/ncu_summary.py traffic); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload, {})
+    except Exception:
+        return {}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -278,6 +288,11 @@ def main():
                "unit": "GB/s", "frac": (lp_gbs / hbm_peak) if lp_gbs else None, "traffic": None,
                "algorithmic": f"{lp_bytes:.4g} B per pass ({'12 nnz + 24 rows + 12 light-CSC' if csr else 'rows*(8k+16)'})",
                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", "share_of_step": lp_share}
+    traffic = load_traffic(args.config)
+    roof_sketch["traffic"] = traffic.get("sketch")
+    roof_lp["traffic"] = traffic.get("long_pass")
+    if traffic:
+        roof_sketch["traffic_source"] = roof_lp["traffic_source"] = traffic.get("source")
     roofline = roof_sketch if sketch_share >= lp_share else roof_lp
 
     # ---- end to end through the C ABI with HOST buffers (H2D of A, b and D2H of x inside)

@@ -3,6 +3,7 @@
 
   python tools/ncu_summary.py launches <launches.csv>      # per-kernel counts, device time, share
   python tools/ncu_summary.py full <prof.ncu-rep> [...]     # key metrics of a --set full capture
+  python tools/ncu_summary.py traffic <workload> <sketch.ncu-rep> <longpass.ncu-rep>   # -> profiles/traffic.json
 """
 import collections
 import csv
@@ -73,9 +74,32 @@ def full(path):
     return res
 
 
+def traffic(workload, sketch_rep, lp_rep, out="profiles/traffic.json"):
+    """Record dram read+write bytes per launch of the sketch and long-pass kernels."""
+    def bytes_of(rep, kernel_re):
+        for d in full(rep):
+            if re.search(kernel_re, d["kernel"]):
+                tot = 0.0
+                for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, unit = d[key].split()
+                    tot += float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+                return tot
+        return None
+    try:
+        cur = json.load(open(out))
+    except Exception:
+        cur = {}
+    cur[workload] = {"sketch": bytes_of(sketch_rep, "sketch"), "long_pass": bytes_of(lp_rep, "rowpass|csr_rowdot"),
+                     "source": f"ncu --set full: {sketch_rep}, {lp_rep}"}
+    json.dump(cur, open(out, "w"), indent=1)
+    return cur
+
+
 if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
+    elif mode == "traffic":
+        print(json.dumps(traffic(sys.argv[2], sys.argv[3], sys.argv[4]), indent=1))
     else:
         print(json.dumps([full(p) for p in sys.argv[2:]], indent=1))
