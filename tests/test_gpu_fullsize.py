@@ -11,7 +11,6 @@ The oracle cannot redo a full-size solve in seconds, so these tests check
 c2 runs by default (about a minute); c3 (3.2 GB), c4 (CSR, 1.4e8 nonzeros)
 and c5 (80 GB) run when LSRN_FULLSIZE=1 (their SVD / sketch stages take long).
 """
-import math
 import os
 
 import numpy as np
@@ -97,7 +96,8 @@ def test_c3_full_tikhonov(ctx):
         # ridge normal equations A^T (b - A x) = lam^2 x  (W = lam I)
         A_T = p.X
         res = A_T @ (p.b - A_T.T @ x) - lam ** 2 * x
-        scale = torch.linalg.norm(A_T, 2) ** 2 * torch.linalg.norm(x) + torch.linalg.norm(A_T @ p.b)
+        fro = torch.linalg.norm(A_T)                   # ||A||_F >= ||A||_2: a looser, cheap scale
+        scale = fro ** 2 * torch.linalg.norm(x) + torch.linalg.norm(A_T @ p.b)
         assert float(torch.linalg.norm(res) / scale) <= 1e-12
 
 
@@ -126,8 +126,10 @@ def test_c5_full(ctx):
     s = 20000
     sl, su = bounds.sigma_bounds(s, 10000, bounds.default_alpha(s))
     assert rep["r"] == 10000 and rep["iters"] == bounds.cs_passes(sl, su, 1e-14) == 99
-    # normal equations: ||A^T (b - A x)|| <= 1e-10 ||A|| ||b - A x||  (x is the LS solution)
+    # normal equations A^T (b - A x) = 0 up to the iteration tolerance: Thm 4.5 bounds
+    # ||A(x - x*)|| by ~2 eps ||A x*||, so ||A^T r|| <~ ||A||_2 2 eps ||b||; checked with the
+    # cheaper ||A||_F >= ||A||_2 and a 10x margin
     r = p.b - p.X @ x
     g = p.X.T @ r
-    an = float(torch.linalg.norm(p.X[:200000], 2)) * math.sqrt(5)
-    assert float(torch.linalg.norm(g)) <= 1e-10 * an * float(torch.linalg.norm(r))
+    an = float(torch.linalg.norm(p.X))
+    assert float(torch.linalg.norm(g)) <= 10 * 2e-14 * an * float(torch.linalg.norm(p.b))
