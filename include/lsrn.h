@@ -71,7 +71,7 @@ typedef enum {
 
 enum { LSRN_DENSE = 0, LSRN_CSR = 1 };
 enum { LSRN_MODE_PREDICTABLE = 0, LSRN_MODE_ADAPTIVE = 1 };
-enum { LSRN_HOST_IO = 1 };
+enum { LSRN_HOST_IO = 1, LSRN_SKETCH_ONLY = 2 /* lsrn_workspace_size: size for lsrn_sketch only */ };
 
 typedef struct lsrn_ctx lsrn_ctx;
 
@@ -96,7 +96,7 @@ typedef struct {
   int32_t mode;          /* LSQR: LSRN_MODE_PREDICTABLE (Thm 4.5 count at alpha = 0, §8(c) C5)
                             or LSRN_MODE_ADAPTIVE (Paige-Saunders tests, capped) */
   int32_t max_iter;      /* adaptive cap; 0 = 2 x the Thm 4.5 count */
-  int32_t flags;         /* LSRN_HOST_IO */
+  int32_t flags;         /* LSRN_HOST_IO, LSRN_SKETCH_ONLY (workspace query) */
   int32_t pad_;
 } lsrn_opts;
 
@@ -170,6 +170,13 @@ lsrn_status lsrn_solve_cs(lsrn_ctx* ctx, const lsrn_matrix* A, const double* b,
  * (rows/cols/out device arrays), the in-kernel Philox + Box-Muller. */
 lsrn_status lsrn_debug_gaussian(lsrn_ctx* ctx, uint64_t seed, const int64_t* rows,
                                 const int64_t* cols, int64_t count, double* out);
+
+/* Testing aid (K1 parity on chosen Philox outputs): for t < count, the
+ * Box-Muller pair (z0, z1) of the four 32-bit Philox words words[4t .. 4t+3]
+ * (w0 = words[4t] | words[4t+1] << 32, w1 = words[4t+2] | words[4t+3] << 32,
+ * §8(c) C9) into out[2t], out[2t+1].  mode 0: the table-driven transform the
+ * kernels use; mode 1: CUDA libm (log, sqrt, sincospi).  Device arrays. */
+lsrn_status lsrn_debug_box_muller(lsrn_ctx* ctx, const uint32_t* words, int64_t count, int mode, double* out);
 
 /* Kernel statistics of the last lsrn_sketch / lsrn_solve_* call on ctx:
  * CUDA-event durations (ms) of the dominant kernels, averaged per launch, and

@@ -43,8 +43,13 @@ def uniforms(seed, q, j, tag=0):
     lo = (j & np.uint64(0xFFFFFFFF)).astype(np.uint64)
     hi = (j >> np.uint64(32)).astype(np.uint64)
     o = philox4x32_10(q, lo, hi, np.full(q.shape, tag, dtype=np.uint64), k0, k1)
-    w0 = o[0].astype(np.uint64) | (o[1].astype(np.uint64) << np.uint64(32))
-    w1 = o[2].astype(np.uint64) | (o[3].astype(np.uint64) << np.uint64(32))
+    return uniforms_from_words(o)
+
+
+def uniforms_from_words(o):
+    """(u1, u2) from the four uint32 Philox output words o = (x, y, z, w) (reading C9)."""
+    w0 = np.asarray(o[0]).astype(np.uint64) | (np.asarray(o[1]).astype(np.uint64) << np.uint64(32))
+    w1 = np.asarray(o[2]).astype(np.uint64) | (np.asarray(o[3]).astype(np.uint64) << np.uint64(32))
     # (w >> 11) < 2^53: exact in fp64; the scaling by 2^-53 is exact.
     u1 = ((w0 >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * TWO_M53
     u2 = (w1 >> np.uint64(11)).astype(np.float64) * TWO_M53

@@ -48,18 +48,15 @@ LSRN_DEV double block_sum(double v, double* sh) {
 
 // G[i, j] for the calling lane's sketch row i, lanes (2q, 2q+1) cooperating on
 // the pair.  All 32 lanes of the warp must call it (with their own i, j equal
-// within each lane pair).  Returns z_{i & 1}.
-LSRN_DEV double gaussian_lane(uint2 key, uint64_t q, uint64_t j, bool odd) {
-  const uint4 o = philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(j),
-                                           static_cast<uint32_t>(j >> 32), 0u), key);
+// within each lane pair).  Returns z_{i & 1}.  T: shared-memory Box-Muller table.
+LSRN_DEV double gaussian_lane(uint2 key, uint64_t q, uint64_t j, bool odd, const double* T) {
+  const uint4 o = philox_counter(key, q, j);
   double mine, other_cs = 0.0;
   if (!odd) {
-    const double u1 = u53_from_words(o.x, o.y) + 0x1.0p-53;
-    mine = sqrt(-2.0 * log(u1));                 // rho
+    mine = sqrt(-2.0 * bm_ln_u1(o.x, o.y, T));        // rho
   } else {
-    const double u2 = u53_from_words(o.z, o.w);
     double sn, cs;
-    sincospi(2.0 * u2, &sn, &cs);
+    bm_sincos_2pi(o.z, o.w, T, sn, cs);
     mine = sn;
     other_cs = cs;
   }
@@ -188,6 +185,8 @@ csr_sketch_heavy_kernel(const double* __restrict__ D, int64_t rows, int64_t lo, 
                         int64_t rows_per_split, double* __restrict__ part) {
   constexpr int JT = 32;                       // D rows staged per step
   __shared__ __align__(16) double Ds[JT][ND];
+  __shared__ double bmT[bm::TAB_SIZE];
+  bm_load_table(bmT);
   const uint2 key = philox_key(seed);
   const int64_t i = (int64_t)blockIdx.x * THR + threadIdx.x;
   const bool odd = (threadIdx.x & 1) != 0;
@@ -206,7 +205,7 @@ csr_sketch_heavy_kernel(const double* __restrict__ D, int64_t rows, int64_t lo, 
     }
     __syncthreads();
     for (int r = 0; r < nj; ++r) {
-      const double z = gaussian_lane(key, q, (uint64_t)(lo + jb + r), odd);
+      const double z = gaussian_lane(key, q, (uint64_t)(lo + jb + r), odd, bmT);
 #pragma unroll
       for (int h = 0; h < ND; h += 2) {
         const double2 d = *reinterpret_cast<const double2*>(&Ds[r][h]);
@@ -230,6 +229,9 @@ csr_sketch_light_kernel(const int64_t* __restrict__ colptr, const int32_t* __res
   constexpr int NT = 256;                      // nonzeros staged per step
   __shared__ int32_t js[NT];
   __shared__ double as[NT];
+  __shared__ double bmT[bm::TAB_SIZE];
+  bm_load_table(bmT);
+  __syncthreads();
   const uint2 key = philox_key(seed);
   const int64_t i = (int64_t)blockIdx.x * THR + threadIdx.x;
   const bool odd = (threadIdx.x & 1) != 0;
@@ -248,7 +250,7 @@ csr_sketch_light_kernel(const int64_t* __restrict__ colptr, const int32_t* __res
       }
       __syncthreads();
       for (int e = 0; e < ne; ++e) {
-        const double z = gaussian_lane(key, q, (uint64_t)(lo + js[e]), odd);
+        const double z = gaussian_lane(key, q, (uint64_t)(lo + js[e]), odd, bmT);
         acc = fma(z, as[e], acc);
       }
     }
@@ -271,13 +273,16 @@ __global__ void csr_heavy_finish_kernel(const double* __restrict__ part, int nsp
 // At[i][c] += si G[i, L + c]  (tall Tikhonov block, §5)
 __global__ void sketch_add_gblock_kernel(double* __restrict__ At, int64_t s, int64_t k, int64_t L, double si,
                                          uint64_t seed) {
+  __shared__ double bmT[bm::TAB_SIZE];
+  bm_load_table(bmT);
+  __syncthreads();
   const uint2 key = philox_key(seed);
   const int64_t npair = (s + 1) / 2;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npair * k;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t qq = e / k, c = e % k;
     double z0, z1;
-    gaussian_pair(key, (uint64_t)qq, (uint64_t)(L + c), z0, z1);
+    gaussian_pair(key, (uint64_t)qq, (uint64_t)(L + c), bmT, z0, z1);
     At[(2 * qq) * k + c] += si * z0;
     if (2 * qq + 1 < s) At[(2 * qq + 1) * k + c] += si * z1;
   }

@@ -24,6 +24,7 @@ cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_finish(const double* part, int nsplit, int64_t split_stride, int64_t s, int64_t k,
                                  double sx, double si, int64_t L, uint64_t seed, double* out, cudaStream_t st,
                                  int nsm);
+cudaError_t launch_debug_box_muller(const uint32_t* words, int64_t count, int mode, double* out, cudaStream_t st);
 cudaError_t launch_debug_gaussian(uint64_t seed, const int64_t* rows, const int64_t* cols, int64_t count,
                                   double* out, cudaStream_t st);
 
@@ -51,6 +52,7 @@ struct RowPassPlan {
   int nst = 0;                      // bulk: pipeline stages
   int keep = 0;                     // bulk: row tile kept in registers between the two phases
   int occ = 1;                      // bulk: CTAs per SM
+  int async_x = 0;                  // bulk, cl > 1: pipelined st.async partial-dot exchange
 };
 // allow_bulk = false forces the register-load kernel (tests compare both)
 RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, bool allow_bulk = true);

@@ -90,6 +90,8 @@ struct lsrn_ctx {
   cudaStream_t stream = nullptr;
   int nranks = 1, rank = 0, device = 0, nsm = 148;
   cusolverDnHandle_t solver = nullptr;
+  cusolverDnParams_t params = nullptr;
+  std::vector<char> host_ws;          // cuSOLVER 64-bit API host workspace
 #ifdef LSRN_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -372,25 +374,44 @@ void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
 // only the k largest eigenpairs.  Measured on the c2 shape (4000 x 2000, rank
 // 1800): 80 ms vs 231 ms for cuSOLVER gesvd with equal sigma / subspace
 // accuracy (profiles/r01_svd_options.jsonl).
+// cuSOLVER's symmetric eigensolvers accept n <= 32768, so for k > 16384 (c4,
+// k = 2e4) the SVD of R falls back to cuSOLVER gesvd (slower, same accuracy).
+constexpr int64_t kMaxJW = 32768;
+
 struct SvdWs {
-  double *W1, *tau, *JW, *S, *work, *Nt;
+  double *W1, *tau, *JW, *S, *Nt;   // JW: Jordan-Wielandt matrix, or [R | VT] in the gesvd fallback
+  void* work;
+  size_t work_bytes, host_bytes;
   int* info;
-  int lwork;
+  bool jw;
 };
 
+// 64-bit cuSOLVER API: the c4 shape (s x k = 4e4 x 2e4, JW 4e4 x 4e4) needs
+// workspaces beyond 2^31 elements.
 SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   SvdWs w{};
-  int l1 = 0, l2 = 0, meig = 0;
-  LSRN_SOLVER(cusolverDnDgeqrf_bufferSize(c->solver, (int)d.s, (int)d.k, nullptr, (int)d.s, &l1));
-  LSRN_SOLVER(cusolverDnDsyevdx_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
-                                           CUBLAS_FILL_MODE_LOWER, (int)(2 * d.k), nullptr, (int)(2 * d.k), 0.0, 0.0,
-                                           (int)d.k + 1, (int)(2 * d.k), &meig, nullptr, &l2));
-  w.lwork = l1 > l2 ? l1 : l2;
+  size_t d1 = 0, h1 = 0, d2 = 0, h2 = 0;
+  int64_t meig = 0;
+  double vl = 0.0, vu = 0.0;
+  LSRN_SOLVER(cusolverDnXgeqrf_bufferSize(c->solver, c->params, d.s, d.k, CUDA_R_64F, nullptr, d.s, CUDA_R_64F,
+                                          nullptr, CUDA_R_64F, &d1, &h1));
+  w.jw = 2 * d.k <= kMaxJW;
+  if (w.jw) {
+    LSRN_SOLVER(cusolverDnXsyevdx_bufferSize(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                             CUBLAS_FILL_MODE_LOWER, 2 * d.k, CUDA_R_64F, nullptr, 2 * d.k, &vl, &vu,
+                                             d.k + 1, 2 * d.k, &meig, CUDA_R_64F, nullptr, CUDA_R_64F, &d2, &h2));
+  } else {
+    LSRN_SOLVER(cusolverDnXgesvd_bufferSize(c->solver, c->params, 'N', 'A', d.k, d.k, CUDA_R_64F, nullptr, d.k,
+                                            CUDA_R_64F, nullptr, CUDA_R_64F, nullptr, 1, CUDA_R_64F, nullptr, d.k,
+                                            CUDA_R_64F, &d2, &h2));
+  }
+  w.work_bytes = std::max(d1, d2);
+  w.host_bytes = std::max(h1, h2);
   w.W1 = ar.take<double>((size_t)d.s * d.k);
   w.tau = ar.take<double>((size_t)d.k);
-  w.JW = ar.take<double>((size_t)4 * d.k * d.k);
+  w.JW = ar.take<double>((size_t)(w.jw ? 4 : 2) * d.k * d.k);
   w.S = ar.take<double>((size_t)2 * d.k);
-  w.work = ar.take<double>((size_t)w.lwork);
+  w.work = ar.take<char>(w.work_bytes + 16);
   w.Nt = ar.take<double>((size_t)d.k * d.k);
   w.info = ar.take<int>(4);
   return w;
@@ -402,23 +423,37 @@ int64_t run_svd(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, st
   const int64_t k = d.k;
   LSRN_CUDA(launch_transpose(At, d.s, k, w.W1, st));
   c->launches++;
-  LSRN_SOLVER(cusolverDnDgeqrf(c->solver, (int)d.s, (int)k, w.W1, (int)d.s, w.tau, w.work, w.lwork, w.info));
-  LSRN_CUDA(launch_build_jw(w.W1, d.s, k, w.JW, st));
-  c->launches++;
-  int meig = 0;
-  LSRN_SOLVER(cusolverDnDsyevdx(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER,
-                                (int)(2 * k), w.JW, (int)(2 * k), 0.0, 0.0, (int)k + 1, (int)(2 * k), &meig, w.S,
-                                w.work, w.lwork, w.info + 1));
+  if (c->host_ws.size() < w.host_bytes + 16) c->host_ws.resize(w.host_bytes + 16);
+  LSRN_SOLVER(cusolverDnXgeqrf(c->solver, c->params, d.s, k, CUDA_R_64F, w.W1, d.s, CUDA_R_64F, w.tau, CUDA_R_64F,
+                               w.work, w.work_bytes, c->host_ws.data(), w.host_bytes, w.info));
+  int64_t meig = k;
   std::vector<double> ev((size_t)k, 0.0);
   int info[2] = {0, 0};
+  double* R = w.JW;                 // gesvd fallback: R (k x k) then VT (k x k)
+  double* VT = w.JW + (size_t)k * k;
+  if (w.jw) {
+    LSRN_CUDA(launch_build_jw(w.W1, d.s, k, w.JW, st));
+    c->launches++;
+    double vl = 0.0, vu = 0.0;
+    LSRN_SOLVER(cusolverDnXsyevdx(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                  CUBLAS_FILL_MODE_LOWER, 2 * k, CUDA_R_64F, w.JW, 2 * k, &vl, &vu, k + 1, 2 * k, &meig,
+                                  CUDA_R_64F, w.S, CUDA_R_64F, w.work, w.work_bytes, c->host_ws.data(), w.host_bytes,
+                                  w.info + 1));
+  } else {
+    LSRN_CUDA(launch_extract_r(w.W1, d.s, k, R, st));
+    c->launches++;
+    LSRN_SOLVER(cusolverDnXgesvd(c->solver, c->params, 'N', 'A', k, k, CUDA_R_64F, R, k, CUDA_R_64F, w.S, CUDA_R_64F,
+                                 nullptr, 1, CUDA_R_64F, VT, k, CUDA_R_64F, w.work, w.work_bytes, c->host_ws.data(),
+                                 w.host_bytes, w.info + 1));
+  }
   LSRN_CUDA(cudaMemcpyAsync(ev.data(), w.S, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
   LSRN_CUDA(cudaMemcpyAsync(info, w.info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
   LSRN_CUDA(cudaStreamSynchronize(st));
-  LSRN_REQUIRE(info[0] == 0 && info[1] == 0 && meig == (int)k, LSRN_ESVD,
-               "cuSOLVER geqrf/syevdx info = " + std::to_string(info[0]) + "/" + std::to_string(info[1]) +
-                   ", eigenpairs " + std::to_string(meig));
+  LSRN_REQUIRE(info[0] == 0 && info[1] == 0 && meig == k, LSRN_ESVD,
+               std::string("cuSOLVER geqrf/") + (w.jw ? "syevdx" : "gesvd") + " info = " + std::to_string(info[0]) +
+                   "/" + std::to_string(info[1]) + ", eigenpairs " + std::to_string(meig));
   S_host.assign((size_t)k, 0.0);
-  for (int64_t i = 0; i < k; ++i) S_host[i] = std::max(0.0, ev[k - 1 - i]);
+  for (int64_t i = 0; i < k; ++i) S_host[i] = std::max(0.0, w.jw ? ev[k - 1 - i] : ev[i]);
   // rank rule (reading C4): r = #{sigma_i > max(s, k) 2^-52 sigma_1}
   const double tau = (double)std::max(d.s, k) * std::ldexp(1.0, -52) * S_host[0];
   int64_t r = 0;
@@ -426,7 +461,10 @@ int64_t run_svd(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, st
     for (int64_t i = 0; i < k; ++i)
       if (S_host[i] > tau) ++r;
   LSRN_REQUIRE(r > 0, LSRN_ERANK0, "sketch has numerical rank 0");
-  LSRN_CUDA(launch_form_nt_jw(w.JW, 2 * k, w.S, k, r, w.Nt, st));
+  if (w.jw)
+    LSRN_CUDA(launch_form_nt_jw(w.JW, 2 * k, w.S, k, r, w.Nt, st));
+  else
+    LSRN_CUDA(launch_form_nt(VT, w.S, k, r, w.Nt, st));
   c->launches++;
   return r;
 }
@@ -652,6 +690,7 @@ lsrn_status lsrn_ctx_create(lsrn_ctx** out, void* stream, int nranks, int rank, 
     LSRN_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device));
     LSRN_SOLVER(cusolverDnCreate(&c->solver));
     LSRN_SOLVER(cusolverDnSetStream(c->solver, c->stream));
+    LSRN_SOLVER(cusolverDnCreateParams(&c->params));
     for (auto& e : c->ev) LSRN_CUDA(cudaEventCreate(&e));
     if (nranks > 1) {
 #ifdef LSRN_WITH_NCCL
@@ -680,6 +719,7 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->pass_ev)
     if (e) cudaEventDestroy(e);
+  if (c->params) cusolverDnDestroyParams(c->params);
   if (c->solver) cusolverDnDestroy(c->solver);
 #ifdef LSRN_WITH_NCCL
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1103,7 +1143,7 @@ lsrn_status lsrn_workspace_size(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_op
     validate_opts(o);
     Arena ar(nullptr);
     Plan PL;
-    *bytes = plan_all(c, A, o, ar, PL, true) + 256;
+    *bytes = plan_all(c, A, o, ar, PL, true, (o->flags & LSRN_SKETCH_ONLY) == 0) + 256;
     return LSRN_OK;
   } catch (const Fail& f) {
     return f.code;
@@ -1152,6 +1192,15 @@ lsrn_status lsrn_solve_lsqr(lsrn_ctx* c, const lsrn_matrix* A, const double* b, 
 lsrn_status lsrn_solve_cs(lsrn_ctx* c, const lsrn_matrix* A, const double* b, const lsrn_opts* o, void* ws,
                           size_t ws_bytes, double* x, lsrn_report* rep) {
   return solve_impl(c, A, b, o, ws, ws_bytes, x, rep, SOLVER_CS);
+}
+
+lsrn_status lsrn_debug_box_muller(lsrn_ctx* c, const uint32_t* words, int64_t count, int mode, double* out) {
+  if (!c || !words || !out) return set_error(LSRN_EINVAL, "NULL argument");
+  if (mode != 0 && mode != 1) return set_error(LSRN_EINVAL, "mode must be 0 (table) or 1 (libm)");
+  if (count <= 0) return LSRN_OK;
+  cudaError_t e = launch_debug_box_muller(words, count, mode, out, c->stream);
+  if (e != cudaSuccess) return set_error(LSRN_ECUDA, cudaGetErrorString(e));
+  return LSRN_OK;
 }
 
 lsrn_status lsrn_debug_gaussian(lsrn_ctx* c, uint64_t seed, const int64_t* rows, const int64_t* cols, int64_t count,

@@ -11,6 +11,7 @@
 // counter-based stream lets every CTA (and every GPU) regenerate exactly the
 // tile it needs from (seed, i, j), so the sketch is tiling- and shard-invariant.
 #pragma once
+#include "bm_tables.h"
 #include "common.cuh"
 
 namespace lsrn {
@@ -44,8 +45,10 @@ LSRN_DEV double u53_from_words(uint32_t lo, uint32_t hi) {
   return (hi & 0x80000000u) ? half_plus : (half_plus - 0.5);
 }
 
-// Box-Muller pair for Philox output o.
-LSRN_DEV void box_muller(uint4 o, double& z0, double& z1) {
+// Box-Muller pair for Philox output o with CUDA's libm (log, sqrt, sincospi):
+// about 77 FP64-pipe instructions per pair on sm_100a.  Kept as the reference
+// implementation for lsrn_debug_box_muller (tests compare the two).
+LSRN_DEV void box_muller_libm(uint4 o, double& z0, double& z1) {
   const double u2 = u53_from_words(o.z, o.w);
   const double u1 = u53_from_words(o.x, o.y) + 0x1.0p-53;   // ((w0>>11)+1) 2^-53, exact
   const double rho = sqrt(-2.0 * log(u1));
@@ -55,11 +58,96 @@ LSRN_DEV void box_muller(uint4 o, double& z0, double& z1) {
   z1 = rho * sn;
 }
 
-// The normal pair (G[2q, j], G[2q+1, j]).
-LSRN_DEV void gaussian_pair(uint2 key, uint64_t q, uint64_t j, double& z0, double& z1) {
-  const uint4 o = philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(j),
-                                           static_cast<uint32_t>(j >> 32), 0u), key);
-  box_muller(o, z0, z1);
+// ---- table-driven Box-Muller (K1 v2) -------------------------------------------
+// The same transform in ~40 FP64 instructions instead of ~77: the RNG shares the
+// FP64 pipe with DMMA in the dense sketch and is the whole cost of the CSR
+// sketch.  Tables and coefficients: bm_tables.h (tools/gen_bm_tables.py); the
+// caller stages bm::kTable (4 KB) in shared memory (bm_load_table) and passes it.
+//
+// ln u1, u1 = n 2^-53, n = (w0 >> 11) + 1 in [1, 2^53]:  n = 2^e m, m in [1, 2);
+//   i = top 7 bits of m's fraction; r = m invc_i - 1 is exact (invc_i has 9
+//   significant bits, |r| < 2^-7); ln u1 = (e - 53) ln2 - ln(invc_i) + log1p(r),
+//   with ln2 and -ln(invc_i) as 42-bit heads + tails so the head sum is exact;
+//   invc_127 = 1/2 makes u1 -> 1 come out as log1p(r) with no cancellation.
+// sin / cos (2 pi u2): 4 u2 = k + f (quadrant k, f exact), f = j / 64 + d / 64;
+//   table sin / cos (pi/2 j/64), polynomials in d for (pi/128) d, angle addition,
+//   quadrant rotation.
+// Accuracy (host model of the same operations vs 40-digit references over 3e4
+// random and edge words): ln u1 within 1.4e-16 relative, sin / cos within 1.5e-16,
+// normals within 4.5e-16 max(1, |z|).
+
+LSRN_DEV void bm_load_table(double* Ts) {
+  for (int i = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); i < bm::TAB_SIZE;
+       i += blockDim.x * blockDim.y * blockDim.z)
+    Ts[i] = bm::kTable[i];
+}
+
+LSRN_DEV double bm_ln_u1(uint32_t lo, uint32_t hi, const double* T) {
+  const uint64_t w0 = (static_cast<uint64_t>(hi) << 32) | lo;
+  const uint64_t n1 = (w0 >> 11) + 1ull;                        // 1 .. 2^53
+  const int e = 63 - __clzll(static_cast<long long>(n1));      // 0 .. 53
+  const uint64_t mant = (e <= 52) ? ((n1 << (52 - e)) & 0xFFFFFFFFFFFFFull) : 0ull;
+  const double m = __longlong_as_double(static_cast<long long>(0x3FF0000000000000ull | mant));
+  const int i = static_cast<int>(mant >> 45);
+  const double r = fma(m, T[i], -1.0);
+  double p = bm::LOG1P_C8;
+  p = fma(p, r, bm::LOG1P_C7);
+  p = fma(p, r, bm::LOG1P_C6);
+  p = fma(p, r, bm::LOG1P_C5);
+  p = fma(p, r, bm::LOG1P_C4);
+  p = fma(p, r, bm::LOG1P_C3);
+  p = fma(p, r, bm::LOG1P_C2);
+  const double poly = fma(r * r, p, r);
+  const double E = static_cast<double>(e - 53);
+  const double thi = fma(E, bm::LN2_HI, T[128 + i]);
+  const double tlo = fma(E, bm::LN2_LO, T[256 + i]);
+  return thi + (tlo + poly);
+}
+
+LSRN_DEV void bm_sincos_2pi(uint32_t lo, uint32_t hi, const double* T, double& sn, double& cs) {
+  const uint64_t w1 = (static_cast<uint64_t>(hi) << 32) | lo;
+  const uint64_t n2 = w1 >> 11;                                 // u2 = n2 2^-53
+  const int k = static_cast<int>(n2 >> 51);
+  const int j = static_cast<int>((n2 >> 45) & 63);
+  const uint64_t dm = n2 & ((1ull << 45) - 1);
+  const double d = __longlong_as_double(static_cast<long long>(0x3FF0000000000000ull | (dm << 7))) - 1.0;
+  const double d2 = d * d;
+  double sp = bm::SIN_C9;
+  sp = fma(sp, d2, bm::SIN_C7);
+  sp = fma(sp, d2, bm::SIN_C5);
+  sp = fma(sp, d2, bm::SIN_C3);
+  sp = fma(sp, d2, bm::SIN_C1);
+  const double sb = sp * d;
+  double cp = bm::COS_C10;
+  cp = fma(cp, d2, bm::COS_C8);
+  cp = fma(cp, d2, bm::COS_C6);
+  cp = fma(cp, d2, bm::COS_C4);
+  cp = fma(cp, d2, bm::COS_C2);
+  const double cb = fma(cp, d2, 1.0);
+  const double sa = T[384 + j], ca = T[448 + j];
+  const double s = fma(sa, cb, ca * sb);
+  const double c = fma(ca, cb, -(sa * sb));
+  // rotate by k quarter turns
+  sn = (k == 0) ? s : (k == 1) ? c : (k == 2) ? -s : -c;
+  cs = (k == 0) ? c : (k == 1) ? -s : (k == 2) ? -c : s;
+}
+
+LSRN_DEV void box_muller_tab(uint4 o, const double* T, double& z0, double& z1) {
+  const double rho = sqrt(-2.0 * bm_ln_u1(o.x, o.y, T));
+  double sn, cs;
+  bm_sincos_2pi(o.z, o.w, T, sn, cs);
+  z0 = rho * cs;
+  z1 = rho * sn;
+}
+
+LSRN_DEV uint4 philox_counter(uint2 key, uint64_t q, uint64_t j) {
+  return philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(j),
+                                  static_cast<uint32_t>(j >> 32), 0u), key);
+}
+
+// The normal pair (G[2q, j], G[2q+1, j]); T = shared-memory copy of bm::kTable.
+LSRN_DEV void gaussian_pair(uint2 key, uint64_t q, uint64_t j, const double* T, double& z0, double& z1) {
+  box_muller_tab(philox_counter(key, q, j), T, z0, z1);
 }
 
 }  // namespace lsrn

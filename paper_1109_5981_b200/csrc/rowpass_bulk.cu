@@ -202,6 +202,183 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
   if (CL > 1) cg::this_cluster().sync();   // keep smem alive until remote stores land
 }
 
+// ----------------------------------------------------------- wide rows (CL > 1)
+// Rows wider than one CTA slice are split over a cluster of CL CTAs that must
+// exchange partial row dots.  With one cluster barrier per tile the c5 long pass
+// (k = 1e4, 3-CTA clusters, one 80 KB row per tile) ran at 1.8 TB/s.  Here the
+// exchange is asynchronous and software-pipelined: after the block reduction of
+// tile t each CTA pushes its TR partials into every peer's `xs` slot with
+// st.async (completing on the peer's `xbar` mbarrier) and goes on to finish tile
+// t-1, whose peer partials were sent one tile earlier.  Four exchange slots: a
+// peer sends tile t only after finishing tile t-2, which needs our tile t-2
+// partials, which we send after our wait on tile t-4 and after reading tile
+// t-3's slot -- so slot t % 4 (and its barrier phase) is free when t arrives.
+namespace {
+LSRN_DEV unsigned cl_map(const void* p, unsigned rank) {
+  unsigned a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+LSRN_DEV void st_async_f64(unsigned addr, double v, unsigned bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(addr), "d"(v),
+               "r"(bar)
+               : "memory");
+}
+LSRN_DEV void cluster_sync_all2() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+}  // namespace
+
+template <int P, int TR, int OCC>
+__global__ void __launch_bounds__(THREADS, OCC)
+rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq, int nst) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kMaxStages];
+  __shared__ uint64_t xbar[4];
+  __shared__ double red[2][NWARP][TR];
+  __shared__ double xs[4][16][TR];
+  __shared__ double zs[4][TR];                       // old z of the tile, read before the exchange
+  if (a.done != nullptr && *a.done != 0) return;     // uniform over the grid
+
+  const unsigned q = cg::this_cluster().block_rank();
+  const int64_t g = blockIdx.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t C = a.C;
+  const int64_t c0 = (int64_t)q * Cq;
+  const int64_t ncol = max((int64_t)0, min(Cq, C - c0));
+  const unsigned row_bytes = (unsigned)(ncol * 8);
+  const int64_t stage_ld = Cq;
+  double* stage = reinterpret_cast<double*>(smem_raw);           // [nst][TR][stage_ld]
+  const double c1 = a.coef[0], c2 = a.coef[1] * a.sx;
+  const double ca = (a.acc != nullptr) ? a.coef[2] : 0.0;
+  const int64_t r0 = g * rows_per_cluster;
+  const int64_t r1 = min(a.R, r0 + rows_per_cluster);
+  const int64_t ntiles = (r1 > r0) ? (r1 - r0 + TR - 1) / TR : 0;
+
+  auto issue = [&](int64_t tile) {
+    const int st = (int)(tile % nst);
+    const int64_t rb = r0 + tile * TR;
+    const int nr = (int)min((int64_t)TR, r1 - rb);
+    if (row_bytes == 0) {
+      mbar_arrive(&full[st]);
+      return;
+    }
+    mbar_arrive_expect_tx(&full[st], row_bytes * (unsigned)nr);
+    for (int tr = 0; tr < nr; ++tr)
+      bulk_g2s(stage + ((int64_t)st * TR + tr) * stage_ld, a.Y + (rb + tr) * a.ld + c0, row_bytes, &full[st]);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < 4; ++s) mbar_init(&xbar[s], 1);
+    mbar_fence_init();
+  }
+  cluster_sync_all2();                       // peers' xbar exist before any st.async
+  if (tid == 0)
+    for (int64_t t = 0; t < min((int64_t)nst, ntiles); ++t) issue(t);
+
+  double2 tv[P], wv[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int64_t cl = 2 * (tid + THREADS * p);
+    tv[p].x = (cl < ncol) ? a.t[c0 + cl] : 0.0;
+    tv[p].y = (cl + 1 < ncol) ? a.t[c0 + cl + 1] : 0.0;
+    wv[p] = make_double2(0.0, 0.0);
+  }
+  double norm = 0.0;
+
+  // phase 1 of `tile`: partial dots, block reduction, push to every CTA of the cluster
+  auto phase1 = [&](int64_t tile) {
+    const int st = (int)(tile % nst);
+    const int64_t rb = r0 + tile * TR;
+    mbar_wait(&full[st], (unsigned)((tile / nst) & 1));
+    double d[TR];
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr) {
+      const double* row = stage + ((int64_t)st * TR + tr) * stage_ld;
+      const bool rok = rb + tr < r1;
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int64_t cl = 2 * (tid + THREADS * p);
+        if (rok && cl < ncol) {
+          const double2 y = *reinterpret_cast<const double2*>(row + cl);
+          s = fma(y.x, tv[p].x, fma(y.y, tv[p].y, s));
+        }
+      }
+      d[tr] = s;
+    }
+    const int rb2 = (int)(tile & 1), xb = (int)(tile & 3);
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr) {
+      const double s = warp_sum(d[tr]);
+      if (lane == 0) red[rb2][warp][tr] = s;
+    }
+    __syncthreads();
+    if (tid == 0) mbar_arrive_expect_tx(&xbar[xb], (unsigned)(CL * TR * 8));
+    if (tid < TR) {
+      // the old z of this row is read (and consumed) before our partial leaves: CTA 0
+      // of the cluster overwrites z only after receiving every CTA's partial
+      zs[xb][tid] = (rb + tid < r1) ? a.z[rb + tid] : 0.0;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) s += red[rb2][w][tid];
+      for (int rr = 0; rr < CL; ++rr)
+        st_async_f64(cl_map(&xs[xb][q][tid], (unsigned)rr), s, cl_map(&xbar[xb], (unsigned)rr));
+    }
+  };
+  // phase 2 of `tile`: totals from the exchange slot, new z, norm, w += y z (y re-read)
+  auto phase2 = [&](int64_t tile) {
+    const int st = (int)(tile % nst);
+    const int64_t rb = r0 + tile * TR;
+    const int xb = (int)(tile & 3);
+    mbar_wait(&xbar[xb], (unsigned)((tile >> 2) & 1));
+#pragma unroll
+    for (int tr = 0; tr < TR; ++tr) {
+      const int64_t row = rb + tr;
+      if (row >= r1) continue;
+      double dot = 0.0;
+      for (int qq = 0; qq < CL; ++qq) dot += xs[xb][qq][tr];
+      const double zn = fma(c1, zs[xb][tr], c2 * dot);
+      norm = fma(zn, zn, norm);
+      if (q == 0 && tid == 0) {
+        a.z[row] = zn;
+        if (a.acc != nullptr) a.acc[row] = fma(ca, zn, a.acc[row]);
+      }
+      const double* rowp = stage + ((int64_t)st * TR + tr) * stage_ld;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int64_t cl = 2 * (tid + THREADS * p);
+        if (cl < ncol) {
+          const double2 y = *reinterpret_cast<const double2*>(rowp + cl);
+          wv[p].x = fma(y.x, zn, wv[p].x);
+          wv[p].y = fma(y.y, zn, wv[p].y);
+        }
+      }
+    }
+  };
+
+  for (int64_t tile = 0; tile < ntiles; ++tile) {
+    phase1(tile);
+    if (tile >= 1) {
+      phase2(tile - 1);
+      __syncthreads();                       // stage of tile-1 fully read by every thread
+      if (tid == 0 && tile - 1 + nst < ntiles) issue(tile - 1 + nst);
+    }
+  }
+  if (ntiles >= 1) phase2(ntiles - 1);
+
+  double* wp = a.wpart + g * C;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int64_t cl = 2 * (tid + THREADS * p);
+    if (cl < ncol) wp[c0 + cl] = a.sx * wv[p].x;
+    if (cl + 1 < ncol) wp[c0 + cl + 1] = a.sx * wv[p].y;
+  }
+  if (q == 0 && tid == 0) a.npart[g] = norm;
+  cluster_sync_all2();                       // no CTA exits while peers may still address it
+}
+
 // ------------------------------------------------------------------ planning
 namespace {
 constexpr int64_t kMaxSlice = 4096;        // doubles per CTA slice (32 KB per staged row)
@@ -236,6 +413,9 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   if (const char* e = std::getenv("LSRN_ROWPASS_KEEP")) keep = std::atoi(e) != 0 && vpt * tr <= 16;
   p->keep = keep ? 1 : 0;
   p->occ = occ;
+  // wide rows: pipelined asynchronous partial-dot exchange (LSRN_ROWPASS_ASYNCX=0: cluster barrier per tile)
+  p->async_x = 1;
+  if (const char* e = std::getenv("LSRN_ROWPASS_ASYNCX")) p->async_x = std::atoi(e) != 0;
   int nclusters = (nsm * occ) / cl;
   if (nclusters < 1) nclusters = 1;
   const int64_t tiles = (R + tr - 1) / tr;
@@ -277,8 +457,37 @@ static cudaError_t launch_bulk_k(const RowPassArgs& a, const RowPassPlan& p, cud
   return cudaLaunchKernelEx(&cfg, kern, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
 }
 
+template <int P, int TR, int OCC>
+static cudaError_t launch_cluster_k(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  const size_t smem = (size_t)p.nst * TR * p.cq * 8;
+  auto kern = rowpass_cluster_kernel<P, TR, OCC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (p.cl > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.nclusters * p.cl));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)p.cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
+}
+
 template <int P, int TR>
 static cudaError_t launch_bulk_t(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  if (p.cl > 1 && p.async_x) {
+    if (p.occ == 2) return launch_cluster_k<P, TR, 2>(a, p, st);
+    return launch_cluster_k<P, TR, 1>(a, p, st);
+  }
   if (p.occ == 2) {
     if constexpr (P * TR <= 4) {
       if (p.keep) return launch_bulk_k<P, TR, true, 2>(a, p, st);

@@ -38,6 +38,7 @@ sketch_dense_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int6
                     double* __restrict__ out, int64_t out_split_stride) {
   using namespace sk;
   extern __shared__ __align__(16) double smem[];
+  __shared__ double bmT[bm::TAB_SIZE];       // Box-Muller tables (philox_bm.cuh)
   double* As = smem;                         // [STAGES][BK][A_LD]
   double* Gs = smem + STAGES * A_STAGE;      // [2][BM][G_LD]
 
@@ -89,7 +90,7 @@ sketch_dense_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int6
       const int p = tid + t * THREADS;
       const int qp = p / BK, kk = p % BK;
       double z0, z1;
-      gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), z0, z1);
+      gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z0, z1);
       dst[(2 * qp) * G_LD + kk] = z0;
       dst[(2 * qp + 1) * G_LD + kk] = z1;
     }
@@ -101,6 +102,8 @@ sketch_dense_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int6
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  bm_load_table(bmT);
+  __syncthreads();
   if (nk > 0) {
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
@@ -162,6 +165,9 @@ sketch_dense_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int6
 __global__ void sketch_finish_kernel(const double* __restrict__ part, int nsplit, int64_t split_stride,
                                      int64_t s, int64_t k, double sx, double si, int64_t L,
                                      uint64_t seed, double* __restrict__ out) {
+  __shared__ double bmT[bm::TAB_SIZE];
+  bm_load_table(bmT);
+  __syncthreads();
   const int64_t npair = (s + 1) / 2;
   const uint2 key = philox_key(seed);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npair * k;
@@ -177,7 +183,7 @@ __global__ void sketch_finish_kernel(const double* __restrict__ part, int nsplit
     v1 *= sx;
     if (si != 0.0) {
       double z0, z1;
-      gaussian_pair(key, (uint64_t)q, (uint64_t)(L + c), z0, z1);
+      gaussian_pair(key, (uint64_t)q, (uint64_t)(L + c), bmT, z0, z1);
       v0 += si * z0;
       v1 += si * z1;
     }
@@ -189,12 +195,34 @@ __global__ void sketch_finish_kernel(const double* __restrict__ part, int nsplit
 __global__ void debug_gaussian_kernel(uint64_t seed, const int64_t* __restrict__ rows,
                                       const int64_t* __restrict__ cols, int64_t count,
                                       double* __restrict__ out) {
+  __shared__ double bmT[bm::TAB_SIZE];
+  bm_load_table(bmT);
+  __syncthreads();
   const uint2 key = philox_key(seed);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
        t += (int64_t)gridDim.x * blockDim.x) {
     double z0, z1;
-    gaussian_pair(key, (uint64_t)(rows[t] >> 1), (uint64_t)cols[t], z0, z1);
+    gaussian_pair(key, (uint64_t)(rows[t] >> 1), (uint64_t)cols[t], bmT, z0, z1);
     out[t] = (rows[t] & 1) ? z1 : z0;
+  }
+}
+
+// Box-Muller on given Philox words (4 per entry): mode 0 table-driven, 1 libm.
+__global__ void debug_box_muller_kernel(const uint32_t* __restrict__ words, int64_t count, int mode,
+                                        double* __restrict__ out) {
+  __shared__ double bmT[bm::TAB_SIZE];
+  bm_load_table(bmT);
+  __syncthreads();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 o = make_uint4(words[4 * t], words[4 * t + 1], words[4 * t + 2], words[4 * t + 3]);
+    double z0, z1;
+    if (mode == 0)
+      box_muller_tab(o, bmT, z0, z1);
+    else
+      box_muller_libm(o, z0, z1);
+    out[2 * t] = z0;
+    out[2 * t + 1] = z1;
   }
 }
 
@@ -240,6 +268,14 @@ cudaError_t launch_debug_gaussian(uint64_t seed, const int64_t* rows, const int6
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) blocks = 1;
   debug_gaussian_kernel<<<(unsigned)blocks, 256, 0, st>>>(seed, rows, cols, count, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_box_muller(const uint32_t* words, int64_t count, int mode, double* out, cudaStream_t st) {
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  debug_box_muller_kernel<<<(unsigned)blocks, 256, 0, st>>>(words, count, mode, out);
   return cudaGetLastError();
 }
 

@@ -92,6 +92,7 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
   double* Xs = smem;                                   // [NSX][BK][A_LD]
   double* Gs = smem + NSX * X_STAGE;                   // [NSG][BM][G_LD]
   __shared__ uint64_t xfull[NSX], xempty[NSX], gfull[NSG], gempty[NSG];
+  __shared__ double bmT[bm::TAB_SIZE];                 // Box-Muller tables (producers)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n0 = (int64_t)blockIdx.x * BN;
@@ -124,6 +125,8 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n");
     const uint2 key = philox_key(seed);
     const int ptid = tid;                                // 0..127
+    for (int i = ptid; i < bm::TAB_SIZE; i += 128) bmT[i] = bm::kTable[i];
+    named_bar(1, 128);
     const int64_t ncols = min((int64_t)BN, k - n0);      // even (k even, n0 multiple of BN)
     const unsigned seg_bytes = (unsigned)(ncols * 8);
     for (int kb = 0; kb < nk; ++kb) {
@@ -160,7 +163,7 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
         if (PAIRS % 128 == 0 || p < PAIRS) {
           const int qp = (int)qrank * (SLICE_ROWS / 2) + p / BK, kk = p % BK;
           double z0 = 0.0, z1 = 0.0;
-          if (kk < nrow) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), z0, z1);
+          if (kk < nrow) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z0, z1);
           gdst[(2 * qp) * G_LD + kk] = z0;
           gdst[(2 * qp + 1) * G_LD + kk] = z1;
         }

@@ -17,13 +17,14 @@ LSRN_OK = 0
 LSRN_DENSE, LSRN_CSR = 0, 1
 MODE_PREDICTABLE, MODE_ADAPTIVE = 0, 1
 HOST_IO = 1
+SKETCH_ONLY = 2
 STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE", -4: "LSRN_ERANK0",
           -5: "LSRN_ESVD", -6: "LSRN_ENOMEM", -7: "LSRN_ECUDA", -8: "LSRN_ENCCL", -9: "LSRN_EUNSUPPORTED"}
 
 # every symbol include/lsrn.h declares
 EXPORTS = ["lsrn_last_error", "lsrn_version", "lsrn_nccl_unique_id", "lsrn_ctx_create", "lsrn_ctx_destroy",
            "lsrn_ctx_set_profiling", "lsrn_workspace_size", "lsrn_sketch",
-           "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_last_stats"]
+           "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_debug_box_muller", "lsrn_last_stats"]
 
 
 class LsrnError(RuntimeError):
@@ -82,6 +83,7 @@ def lib():
             "lsrn_solve_cs": [vp, ctypes.POINTER(Matrix), vp, ctypes.POINTER(Opts), vp, sz, vp,
                               ctypes.POINTER(Report)],
             "lsrn_debug_gaussian": [vp, u64, vp, vp, i64, vp],
+            "lsrn_debug_box_muller": [vp, vp, i64, i32, vp],
             "lsrn_last_stats": [vp, ctypes.POINTER(ctypes.c_double), i32],
         }
         for name, args in sigs.items():
@@ -216,7 +218,7 @@ class Context:
         k = min(m, n)
         s = int(torch.tensor(gamma * k, dtype=torch.float64).ceil().item())
         At = torch.empty(s, k, dtype=torch.float64, device=self.device)
-        opts = Opts(gamma=gamma, lambda_=lam, tol=0.5, alpha=-1.0, seed=seed)
+        opts = Opts(gamma=gamma, lambda_=lam, tol=0.5, alpha=-1.0, seed=seed, flags=SKETCH_ONLY)
         ws = self.workspace(self.workspace_size(mat, opts))
         s_out = ctypes.c_int64()
         cur = self._enter()
@@ -255,6 +257,16 @@ class Context:
                   ctypes.byref(rep)))
         self._leave(cur)
         return x_out, rep.as_dict()
+
+    def debug_box_muller(self, words, mode=0):
+        """(count, 2) normals of the Box-Muller transform of (count, 4) uint32 Philox words."""
+        w = torch.as_tensor(words).to(torch.int64).to(torch.int32).contiguous().to(self.device)
+        n = w.shape[0]
+        out = torch.empty(n, 2, dtype=torch.float64, device=self.device)
+        cur = self._enter()
+        _check(lib().lsrn_debug_box_muller(self.h, _ptr(w), n, mode, _ptr(out)))
+        self._leave(cur)
+        return out
 
     def debug_gaussian(self, seed, rows, cols):
         rows = rows.to(self.device, torch.int64).contiguous()

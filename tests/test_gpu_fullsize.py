@@ -45,9 +45,9 @@ def _sampled_sketch_check(At, Xcol, s, L, sx=1.0, si=0.0, nsamp=12, seed=0):
     cols_data = {c: Xcol(c) for c in set(cols)}
     ref = sketch_entries(cols_data, rows, cols, SKETCH_SEED, sx, si, L=L)
     got = At[torch.tensor(rows), torch.tensor(cols)].cpu().numpy()
-    # each entry is a length-L dot product of N(0,1) draws with a column: compare against
-    # its natural scale sqrt(sum_j X[j,c]^2) (the entry's standard deviation)
-    scale = np.array([np.linalg.norm(cols_data[c]) for c in cols])
+    # each entry is sx * (length-L dot product of N(0,1) draws with a column) + si * G: compare
+    # against its natural scale sx * sqrt(sum_j X[j,c]^2) + si (the entry's standard deviation)
+    scale = np.array([sx * np.linalg.norm(cols_data[c]) + si for c in cols])
     err = np.abs(got - ref) / scale
     assert err.max() <= 1e-12, (err.max(), rows, cols)
 

@@ -223,3 +223,67 @@ def test_tuning_variants_match(ctx, monkeypatch, env):
     orc = orc_solve(A, p.b.numpy(), solver="cs", extended=True)
     assert rep["iters"] == orc["iters"]
     _check_solution(A, x.cpu().numpy(), orc["x"], p.meta["kappa"])
+
+
+@pytest.mark.parametrize("asyncx", ["1", "0"])
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_wide_rows_cluster_pass_vs_pseudoinverse(ctx, monkeypatch, asyncx, solver):
+    """k > 4096: each row of A is split over a 2-CTA cluster in the long pass (partial dots
+    exchanged with st.async, or with a cluster barrier when LSRN_ROWPASS_ASYNCX=0).  The
+    generator's factors give x* = V diag(1/sigma) U^T b exactly."""
+    monkeypatch.setenv("LSRN_ROWPASS_ASYNCX", asyncx)
+    p = make_problem("c1", m=6000, n=4100, keep_factors=True)
+    U, V, sig = p.meta["U"].numpy(), p.meta["V"].numpy(), p.meta["sigma"].numpy()
+    b = p.b.numpy()
+    xstar = V @ ((U.T @ b) / sig)
+    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver=solver, gamma=1.5)
+    assert rep["r"] == 4100
+    dx = x.cpu().numpy() - xstar
+    # Thm 4.5's A-norm form (P:656-662) is kappa-free; the 2-norm carries the fp64
+    # floor ~ kappa u sqrt(n) of any two implementations (DESIGN.md C18), here n = 4100
+    an = np.linalg.norm(sig * (V.T @ dx)) / np.linalg.norm(sig * (V.T @ xstar))
+    assert an <= 1e-11, an
+    rel = np.linalg.norm(dx) / np.linalg.norm(xstar)
+    assert rel <= 1e-8, rel
+
+
+def _edge_words(rng, n):
+    """Philox-word edge cases for the Box-Muller transform: u1 -> 1 and u1 -> 0 (ln u1
+    near 0 / large), u2 at quadrant and table-interval boundaries, plus random words."""
+    w = rng.integers(0, 2 ** 32, size=(n, 4), dtype=np.uint64)
+    top = np.uint64(0xFFFFFFFF)
+    k = 0
+    for t in range(40):                       # w0 = 2^64 - 1 - small  ->  u1 = 1 - tiny
+        small = int(rng.integers(0, 2 ** min(t + 1, 62)))
+        w0 = (2 ** 64 - 1) - small
+        w[k, 0], w[k, 1] = w0 & 0xFFFFFFFF, w0 >> 32
+        k += 1
+    for t in range(40):                       # w0 small  ->  u1 = (w0 >> 11 + 1) 2^-53 tiny
+        w0 = int(rng.integers(0, 2 ** (t + 1)))
+        w[k, 0], w[k, 1] = w0 & 0xFFFFFFFF, w0 >> 32
+        k += 1
+    for quad in range(4):                     # u2 at / just around quadrant and 1/256 boundaries
+        for j in (0, 1, 31, 63):
+            for delta in (0, 1, 2 ** 11, -(2 ** 11)):
+                n2 = (quad << 51) + (j << 45)
+                w1 = ((n2 << 11) + delta) % (2 ** 64)
+                w[k, 2], w[k, 3] = w1 & 0xFFFFFFFF, w1 >> 32
+                k += 1
+    w[k, :] = 0
+    w[k + 1, :] = top
+    return w.astype(np.uint32)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_box_muller_words_vs_oracle(ctx, mode):
+    """K1's transform (mode 0: table-driven, the kernels' path; 1: CUDA libm) on chosen
+    Philox words against the oracle's long-double Box-Muller (reading C9)."""
+    from oracle.gaussian import box_muller, uniforms_from_words
+    rng = np.random.default_rng(17)
+    w = _edge_words(rng, 20000)
+    got = ctx.debug_box_muller(torch.from_numpy(w.astype(np.int64)), mode).cpu().numpy()
+    u1, u2 = uniforms_from_words(w.T.astype(np.uint64))
+    z0, z1 = box_muller(u1, u2, precise=True)
+    for col, ref in ((0, z0), (1, z1)):
+        err = np.abs(got[:, col] - ref) / np.maximum(1.0, np.abs(ref))
+        assert err.max() <= 2e-15, (col, err.max(), int(err.argmax()))
