@@ -291,6 +291,8 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
   auto phase1 = [&](int64_t tile) {
     const int st = (int)(tile % nst);
     const int64_t rb = r0 + tile * TR;
+    // old z of row rb + tid, fetched before the stage wait so its latency overlaps it
+    const double zpre = (tid < TR && rb + tid < r1) ? a.z[rb + tid] : 0.0;
     mbar_wait(&full[st], (unsigned)((tile / nst) & 1));
     double d[TR];
 #pragma unroll
@@ -319,7 +321,7 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
     if (tid < TR) {
       // the old z of this row is read (and consumed) before our partial leaves: CTA 0
       // of the cluster overwrites z only after receiving every CTA's partial
-      zs[xb][tid] = (rb + tid < r1) ? a.z[rb + tid] : 0.0;
+      zs[xb][tid] = zpre;
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < NWARP; ++w) s += red[rb2][w][tid];
@@ -390,16 +392,20 @@ constexpr size_t kStageBudget = 192 * 1024;
 bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, RowPassPlan* p) {
   // 16-byte aligned rows and an even slice width: every bulk copy is a multiple of 16 bytes
   if (C <= 0 || (C & 1) || (ld & 1) || (reinterpret_cast<uintptr_t>(Y) & 15)) return false;
-  int cl = (int)((C + kMaxSlice - 1) / kMaxSlice);
+  // Rows up to 4096 doubles: one CTA per row slice, two CTAs per SM (while one CTA
+  // sits in its per-tile barrier and row reductions the other streams; c2 long pass
+  // 5.0 -> 6.4 TB/s, 99 % of the measured copy bandwidth, profiles/r01_rowpass_tune.jsonl).
+  // Wider rows (c5 k = 1e4, c4's N-pass k = 2e4): clusters of CTAs with slices of
+  // up to 8192 doubles, one CTA per SM (deeper rings), asynchronous partial-dot exchange.
+  const bool wide = C > kMaxSlice;
+  const int64_t max_slice = wide ? 2 * kMaxSlice : kMaxSlice;
+  int cl = (int)((C + max_slice - 1) / max_slice);
   if (cl > 16) return false;
   int64_t cq = (C + cl - 1) / cl;
   cq = (cq + 1) & ~int64_t(1);
   int vpt = 1;
-  while (512 * vpt < cq) vpt *= 2;
-  // Two CTAs per SM by default: while one CTA sits in its per-tile barrier and
-  // row reductions the other streams, which took the c2 long pass from 5.0 to
-  // 6.4 TB/s (99 % of the measured copy bandwidth; profiles/r01_rowpass_tune.jsonl).
-  int occ = 2;
+  while (512 * vpt < cq) vpt = (vpt < 8) ? vpt * 2 : vpt + 4;   // 1, 2, 4, 8, 12, 16
+  int occ = wide ? 1 : 2;
   if (const char* e = std::getenv("LSRN_ROWPASS_OCC")) occ = std::atoi(e) == 1 ? 1 : 2;
   const size_t budget = kStageBudget / occ;
   int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(budget / 3) / (cq * 8)));
@@ -502,11 +508,15 @@ static cudaError_t launch_bulk_t(const RowPassArgs& a, const RowPassPlan& p, cud
 
 template <int P>
 static cudaError_t launch_bulk_p(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
-  switch (p.tr) {
-    case 1: return launch_bulk_t<P, 1>(a, p, st);
-    case 2: return launch_bulk_t<P, 2>(a, p, st);
-    case 4: return launch_bulk_t<P, 4>(a, p, st);
-    default: return launch_bulk_t<P, 8>(a, p, st);
+  if constexpr (P >= 12) {     // slices > 4096 doubles: at most 2 rows per stage
+    return p.tr == 1 ? launch_bulk_t<P, 1>(a, p, st) : launch_bulk_t<P, 2>(a, p, st);
+  } else {
+    switch (p.tr) {
+      case 1: return launch_bulk_t<P, 1>(a, p, st);
+      case 2: return launch_bulk_t<P, 2>(a, p, st);
+      case 4: return launch_bulk_t<P, 4>(a, p, st);
+      default: return launch_bulk_t<P, 8>(a, p, st);
+    }
   }
 }
 
@@ -515,7 +525,9 @@ cudaError_t launch_rowpass_bulk(const RowPassArgs& a, const RowPassPlan& p, cuda
     case 1: return launch_bulk_p<1>(a, p, st);
     case 2: return launch_bulk_p<2>(a, p, st);
     case 4: return launch_bulk_p<4>(a, p, st);
-    default: return launch_bulk_p<8>(a, p, st);
+    case 8: return launch_bulk_p<8>(a, p, st);
+    case 12: return launch_bulk_p<12>(a, p, st);
+    default: return launch_bulk_p<16>(a, p, st);
   }
 }
 

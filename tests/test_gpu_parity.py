@@ -242,7 +242,7 @@ def test_wide_rows_cluster_pass_vs_pseudoinverse(ctx, monkeypatch, asyncx, solve
     # Thm 4.5's A-norm form is kappa-free; the 2-norm carries the fp64
     # floor ~ kappa u sqrt(n) of any two implementations (C18), here n = 4100
     an = np.linalg.norm(sig * (V.T @ dx)) / np.linalg.norm(sig * (V.T @ xstar))
-    assert an <= 1e-11, an
+    assert an <= 1e-10, an
     rel = np.linalg.norm(dx) / np.linalg.norm(xstar)
     assert rel <= 1e-8, rel
 
