@@ -86,7 +86,8 @@ LSRN_DEV void cluster_sync_all() {
 template <int CL>
 __global__ void __launch_bounds__(ws::THREADS, 1)
 sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
-                 uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride) {
+                 uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride,
+                 int diag) {
   using namespace ws;
   extern __shared__ __align__(128) double smem[];
   double* Xs = smem;                                   // [NSX][BK][A_LD]
@@ -163,7 +164,7 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
         if (PAIRS % 128 == 0 || p < PAIRS) {
           const int qp = (int)qrank * (SLICE_ROWS / 2) + p / BK, kk = p % BK;
           double z0 = 0.0, z1 = 0.0;
-          if (kk < nrow) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z0, z1);
+          if (kk < nrow && !(diag & 1)) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z0, z1);
           gdst[(2 * qp) * G_LD + kk] = z0;
           gdst[(2 * qp + 1) * G_LD + kk] = z1;
         }
@@ -270,8 +271,11 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, dim3 grid, cudaStream_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // LSRN_SKETCH_DIAG (timing experiments only, results are wrong): 1 = skip the RNG
+  int diag = 0;
+  if (const char* e = std::getenv("LSRN_SKETCH_DIAG")) diag = std::atoi(e);
   return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
-                            a.rows_per_split, a.out, a.out_split_stride);
+                            a.rows_per_split, a.out, a.out_split_stride, diag);
 }
 
 // Cluster size along N: the largest of {max_cl, ..., 2} dividing the N-tile count.
