@@ -20,6 +20,8 @@ size_t sketch_dense_smem();
 void sketch_tile_counts(int64_t s, int64_t k, int64_t* mtiles, int64_t* ntiles, int64_t* bk);
 cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st);   // picks v2 when supported
 bool sketch_ws_supported(const SketchDenseArgs& a);
+bool sketch_batch_supported(const SketchDenseArgs& a);
+cudaError_t launch_sketch_batch(const SketchDenseArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_finish(const double* part, int nsplit, int64_t split_stride, int64_t s, int64_t k,
                                  double sx, double si, int64_t L, uint64_t seed, double* out, cudaStream_t st,

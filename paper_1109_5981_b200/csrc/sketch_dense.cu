@@ -14,6 +14,7 @@
 // generated is reused BN = 256 times (RNG overhead ~ cost(normal) / BN of the
 // FP64 pipe, which DMMA and DFMA share on sm_100a -- measured).
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "philox_bm.cuh"
@@ -231,9 +232,15 @@ size_t sketch_dense_smem() { return sk::SMEM_BYTES; }
 
 cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st) {
   using namespace sk;
-  // warp-specialized K2 (sketch_ws.cu) when supported; LSRN_SKETCH_V1=1 forces this kernel (tuning aid)
+  // Variant (tuning aid LSRN_SKETCH_IMPL = ws | batch | v1; LSRN_SKETCH_V1=1 = v1):
+  // ws = warp-specialized (sketch_ws.cu), batch = batched RNG phases (sketch_batch.cu),
+  // v1 = this kernel (also the path for unaligned X / odd ld).
+  const char* impl = std::getenv("LSRN_SKETCH_IMPL");
   const char* v1 = std::getenv("LSRN_SKETCH_V1");
-  if (sketch_ws_supported(a) && !(v1 && v1[0] == '1')) return launch_sketch_ws(a, st);
+  std::string which = impl ? impl : "ws";
+  if (v1 && v1[0] == '1') which = "v1";
+  if (which == "batch" && sketch_batch_supported(a)) return launch_sketch_batch(a, st);
+  if (which == "ws" && sketch_ws_supported(a)) return launch_sketch_ws(a, st);
   dim3 grid((unsigned)((a.k + BN - 1) / BN), (unsigned)((a.s + BM - 1) / BM), (unsigned)a.nsplit);
   const bool vec2 = (a.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
   cudaError_t e;

@@ -43,7 +43,8 @@ constexpr int A_LD = BN + 8;                // padded smem row (doubles)
 constexpr int G_LD = BK + 4;
 constexpr int X_STAGE = BK * A_LD;          // doubles
 constexpr int G_STAGE = BM * G_LD;
-constexpr int THREADS = 384;
+constexpr int NPROD = 256;                 // producer threads (2 warpgroups)
+constexpr int THREADS = NPROD + 256;
 constexpr int NCONS_WARPS = 8;
 constexpr size_t SMEM_BYTES = sizeof(double) * (size_t)(NSX * X_STAGE + NSG * G_STAGE) + 128;
 }  // namespace ws
@@ -121,13 +122,13 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
   else
     __syncthreads();
 
-  if (warp < 4) {
+  if (warp < NPROD / 32) {
     // ------------------------------------------------------------ producers
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
     const uint2 key = philox_key(seed);
     const int ptid = tid;                                // 0..127
-    for (int i = ptid; i < bm::TAB_SIZE; i += 128) bmT[i] = bm::kTable[i];
-    named_bar(1, 128);
+    for (int i = ptid; i < bm::TAB_SIZE; i += NPROD) bmT[i] = bm::kTable[i];
+    named_bar(1, NPROD);
     const int64_t ncols = min((int64_t)BN, k - n0);      // even (k even, n0 multiple of BN)
     const unsigned seg_bytes = (unsigned)(ncols * 8);
     for (int kb = 0; kb < nk; ++kb) {
@@ -153,15 +154,15 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
       if (kb >= NSG) mbar_wait(&gempty[sg], pg);
       if (CL > 1) {
         if (ptid == 0) bulk_wait_read<NSG - 1>();
-        named_bar(1, 128);
+        named_bar(1, NPROD);
       }
       double* gdst = Gs + sg * G_STAGE;
       const int64_t jbase = lo + rbase;
       constexpr int PAIRS = (SLICE_ROWS / 2) * BK;       // pairs per CTA per k-block
 #pragma unroll
-      for (int t = 0; t < (PAIRS + 127) / 128; ++t) {
-        const int p = ptid + 128 * t;
-        if (PAIRS % 128 == 0 || p < PAIRS) {
+      for (int t = 0; t < (PAIRS + NPROD - 1) / NPROD; ++t) {
+        const int p = ptid + NPROD * t;
+        if (PAIRS % NPROD == 0 || p < PAIRS) {
           const int qp = (int)qrank * (SLICE_ROWS / 2) + p / BK, kk = p % BK;
           double z0 = 0.0, z1 = 0.0;
           if (kk < nrow && !(diag & 1)) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z0, z1);
@@ -170,7 +171,7 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
         }
       }
       if (CL > 1) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic -> async proxy
-      named_bar(1, 128);                                  // the whole slice is written
+      named_bar(1, NPROD);                                // the whole slice is written
       if (ptid == 0) {
         mbar_arrive_expect_tx(&gfull[sg], SLICE_BYTES * (unsigned)(CL - 1));   // local slice: this arrive
         if (CL > 1) {
@@ -193,7 +194,7 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
 
   // -------------------------------------------------------------- consumers
   asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n");
-  const int cw = warp - 4;                               // 0..7
+  const int cw = warp - NPROD / 32;                      // 0..7
   const int wm = cw >> 2, wn = cw & 3;                   // 2 x 4 warps
   double acc[4][8][2];
 #pragma unroll

@@ -197,11 +197,14 @@ def test_repeat_solves_bitwise(ctx):
     assert torch.equal(x1, x2)
 
 
-@pytest.mark.parametrize("maxcl,n", [(4, 1024), (8, 2048), (8, 1536)])
+@pytest.mark.parametrize("maxcl,n", [(4, 1024), (8, 2048), (8, 1536), ("batch", 1000), ("batch", 2048)])
 def test_sketch_cluster_sizes(ctx, monkeypatch, maxcl, n):
     """The G-sharing cluster paths CL = 4 and 8 (the default caps CL at 2; LSRN_SKETCH_MAXCL
     is read at each launch) give the same sketch."""
-    monkeypatch.setenv("LSRN_SKETCH_MAXCL", str(maxcl))
+    if maxcl == "batch":
+        monkeypatch.setenv("LSRN_SKETCH_IMPL", "batch")
+    else:
+        monkeypatch.setenv("LSRN_SKETCH_MAXCL", str(maxcl))
     m = n + 300
     g = torch.Generator().manual_seed(n)
     X = torch.randn(m, n, generator=g, dtype=torch.float64)
@@ -212,7 +215,8 @@ def test_sketch_cluster_sizes(ctx, monkeypatch, maxcl, n):
 
 
 @pytest.mark.parametrize("env", [{"LSRN_ROWPASS_KEEP": "0"}, {"LSRN_ROWPASS_OCC": "1"},
-                                 {"LSRN_ROWPASS_OCC": "1", "LSRN_ROWPASS_KEEP": "1"}, {"LSRN_SKETCH_V1": "1"}])
+                                 {"LSRN_ROWPASS_OCC": "1", "LSRN_ROWPASS_KEEP": "1"}, {"LSRN_SKETCH_V1": "1"},
+                                 {"LSRN_SKETCH_IMPL": "batch"}, {"LSRN_SKETCH_IMPL": "ws"}])
 def test_tuning_variants_match(ctx, monkeypatch, env):
     """Kernel variants selected by the tuning switches solve c1 to the same tolerance."""
     for k_, v_ in env.items():
