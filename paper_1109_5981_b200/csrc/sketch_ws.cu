@@ -9,11 +9,19 @@
 // DMMA, one __syncthreads per k-block) kept the tensor pipe 62 % active on c2
 // (profiles/r01_ncu_full_sketch_rowpass.json): after each barrier all warps sat
 // in the latency-bound Box-Muller phase together.  Here the roles are split:
-//   warpgroup 0 (4 warps, setmaxnreg 96): one lane streams X tiles into a
-//     shared-memory ring with 1-D TMA bulk copies; all 128 threads generate the
-//     64 x 16 G tile of each k-block into a second ring (4 pairs per thread);
-//   warpgroups 1-2 (8 warps, setmaxnreg 200): DMMA.8x8x4 on 32 x 64 warp tiles,
-//     never touching RNG, released stage by stage with mbarriers.
+//   warpgroups 0-1 (8 producer warps, setmaxnreg 56): one lane streams X tiles
+//     into a shared-memory ring with 1-D TMA bulk copies; all 256 threads
+//     generate the 64 x 16 G tile of each k-block into a second ring;
+//   warpgroups 2-3 (8 consumer warps, setmaxnreg 200): DMMA.8x8x4 on 32 x 64
+//     warp tiles, never touching RNG, released stage by stage with mbarriers.
+// Measured on c2 (profiles/r01_sketch_tune*.jsonl): with the RNG switched off the
+// consumers reach 33.8 TFLOP/s (92 % of the DMMA peak); with it, 25.5 TFLOP/s.
+// The Box-Muller FP64 instructions cost far more than their issue count: each
+// competes with the consumers' DMMAs for the shared FP64 pipe.  Variants tried
+// and rejected: 4 producer warps (66 ms vs 62.7), producers batching 4-8 pairs
+// per thread (register-starved), X streamed by a consumer warp (serialises the
+// consumers), batched RNG phases in a non-specialized kernel (sketch_batch.cu,
+// 73.9 ms).
 // The RNG shares the FP64 pipe with DMMA (measured), so each
 // normal must be generated as few times as possible: the CTAs of a cluster of
 // CL along N (same sketch rows, same k-range, different column tiles) need the
