@@ -71,7 +71,17 @@ typedef enum {
 
 enum { LSRN_DENSE = 0, LSRN_CSR = 1 };
 enum { LSRN_MODE_PREDICTABLE = 0, LSRN_MODE_ADAPTIVE = 1 };
-enum { LSRN_HOST_IO = 1, LSRN_SKETCH_ONLY = 2 /* lsrn_workspace_size: size for lsrn_sketch only */ };
+enum {
+  LSRN_HOST_IO = 1,
+  LSRN_SKETCH_ONLY = 2,    /* lsrn_workspace_size: size for lsrn_sketch only */
+  /* λ-path reuse (§5: "we can reuse GA and only re-sketch W"):
+   * skip the sketch of A and its allreduce and reuse the raw sketch G·A that
+   * the previous call on this context left in this workspace.  Valid only if
+   * A (the same pointers and values), its shard, gamma and seed are unchanged;
+   * pointer / shard / gamma / seed / workspace mismatches return LSRN_EINVAL.
+   * lambda may change: only the Tikhonov block depends on it. */
+  LSRN_REUSE_SKETCH = 4
+};
 
 typedef struct lsrn_ctx lsrn_ctx;
 
@@ -96,7 +106,7 @@ typedef struct {
   int32_t mode;          /* LSQR: LSRN_MODE_PREDICTABLE (Thm 4.5 count at alpha = 0, §8(c) C5)
                             or LSRN_MODE_ADAPTIVE (Paige-Saunders tests, capped) */
   int32_t max_iter;      /* adaptive cap; 0 = 2 x the Thm 4.5 count */
-  int32_t flags;         /* LSRN_HOST_IO, LSRN_SKETCH_ONLY (workspace query) */
+  int32_t flags;         /* LSRN_HOST_IO, LSRN_SKETCH_ONLY (workspace query), LSRN_REUSE_SKETCH */
   int32_t pad_;
 } lsrn_opts;
 

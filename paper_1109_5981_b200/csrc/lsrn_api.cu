@@ -92,6 +92,9 @@ struct lsrn_ctx {
   cusolverDnHandle_t solver = nullptr;
   cusolverDnParams_t params = nullptr;
   std::vector<char> host_ws;          // cuSOLVER 64-bit API host workspace
+  // raw sketch cache (λ-path reuse): key of the sketch held in the workspace
+  bool sketch_cached = false;
+  unsigned char sketch_key[160] = {};
 #ifdef LSRN_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -184,7 +187,8 @@ SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_fla
   int64_t rps = (d.cnt + w.nsplit - 1) / w.nsplit;
   rps = (rps + 15) / 16 * 16;
   w.rows_per_split = rps > 0 ? rps : 16;
-  const bool direct = (w.nsplit == 1) && (d.sx == 1.0) && !d.has_I && !need_finish_flag;
+  const bool direct = (w.nsplit == 1);
+  (void)need_finish_flag;
   w.part = direct ? nullptr : ar.take<double>((size_t)w.nsplit * d.s * d.k);
   return w;
 }
@@ -289,6 +293,7 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
   LSRN_CUDA(cudaStreamSynchronize(st));   // host vectors above are pageable: keep them alive until copied
 }
 
+// Raw sketch S0 = G[:, lo:lo+cnt] X_shard (no scaling, no Tikhonov block) of a CSR shard.
 void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double* At) {
   CsrSketchArgs a{};
   a.D = w.D;
@@ -310,12 +315,9 @@ void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double*
   a.At = At;
   LSRN_CUDA(launch_csr_sketch(a, c->stream, c->nsm));
   c->launches += (w.nd > 0 ? 3 : 1);
-  if (d.has_I) {
-    LSRN_CUDA(launch_sketch_add_gblock(At, d.s, d.k, d.L, d.si, seed, c->stream, c->nsm));
-    c->launches++;
-  }
 }
 
+// Raw sketch S0 = G[:, lo:lo+cnt] X_shard of a dense shard (split-K partials summed in fixed order).
 void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed, const SketchWs& w, double* At) {
   cudaStream_t st = c->stream;
   if (d.cnt > 0) {
@@ -342,10 +344,56 @@ void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed,
       LSRN_CUDA(launch_fill(w.part, 0.0, (int64_t)w.nsplit * d.s * d.k, st));
       c->launches++;
     }
-    LSRN_CUDA(launch_sketch_finish(w.part, w.nsplit, d.s * d.k, d.s, d.k, d.sx, d.has_I ? d.si : 0.0, d.L, seed,
-                                   At, st, c->nsm));
+    LSRN_CUDA(launch_sketch_finish(w.part, w.nsplit, d.s * d.k, d.s, d.k, 1.0, 0.0, d.L, seed, At, st, c->nsm));
     c->launches++;
   }
+}
+
+void allreduce(lsrn_ctx* c, double* buf, int64_t count);
+
+// Alg. 1/2 step 3 with the §5 blocks, from the raw (allreduced) sketch S0:
+//   At = sigma_X S0 + sigma_I G[:, L:L+k]   (every rank; G is deterministic)
+void finish_sketch(lsrn_ctx* c, const Dims& d, uint64_t seed, const double* S0, double* At) {
+  LSRN_CUDA(launch_copy_scale(At, S0, d.sx, d.s * d.k, c->stream));
+  c->launches++;
+  if (d.si != 0.0) {
+    LSRN_CUDA(launch_sketch_add_gblock(At, d.s, d.k, d.L, d.si, seed, c->stream, c->nsm));
+    c->launches++;
+  }
+}
+
+// The raw sketch of the last call is kept in the workspace (Plan::S0); a later
+// call with LSRN_REUSE_SKETCH and the same A, shard, gamma, seed and workspace
+// skips the sketch of A and its allreduce -- the λ-path reuse of §5:
+// only the Tikhonov block G_W (tall) / G_I (wide) depends on λ.
+struct SketchKey {
+  const void* val = nullptr;
+  const void* rowptr = nullptr;
+  const void* colind = nullptr;
+  int64_t m = 0, n = 0, lo = 0, cnt = 0, ld = 0, nnz = 0, s = 0;
+  int kind = -1;
+  uint64_t seed = 0;
+  const void* ws = nullptr;
+};
+static_assert(sizeof(SketchKey) <= 160, "sketch key must fit lsrn_ctx::sketch_key");
+
+SketchKey make_key(const lsrn_matrix* A_user, const Dims& d, uint64_t seed, const void* ws) {
+  SketchKey k;
+  std::memset(static_cast<void*>(&k), 0, sizeof(k));   // padding takes part in the comparison
+  k.val = A_user->val;
+  k.rowptr = A_user->rowptr;
+  k.colind = A_user->colind;
+  k.m = A_user->m;
+  k.n = A_user->n;
+  k.lo = A_user->lo;
+  k.cnt = A_user->cnt;
+  k.ld = A_user->ld;
+  k.nnz = A_user->nnz;
+  k.s = d.s;
+  k.kind = A_user->kind;
+  k.seed = seed;
+  k.ws = ws;
+  return k;
 }
 
 void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
@@ -758,6 +806,7 @@ struct Plan {
   SvdWs vw;
   IterWs iw;
   double* At = nullptr;
+  double* S0 = nullptr;
   // LSRN_HOST_IO staging (dense: A rows; CSR: rowptr / colind / val)
   double* Astage = nullptr;
   int64_t* rpstage = nullptr;
@@ -787,6 +836,7 @@ size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar
       P.xstage = ar.take<double>((size_t)(d.tall ? d.n : d.cnt));
     }
   }
+  P.S0 = ar.take<double>((size_t)d.s * d.k);   // raw sketch (kept for LSRN_REUSE_SKETCH)
   if (solve) P.At = ar.take<double>((size_t)d.s * d.k);
   if (P.csr)
     P.cw = plan_csr(c, d, A, ar);
@@ -799,6 +849,37 @@ size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar
     P.iw = plan_iter(c, d, ar, max_passes);
   }
   return ar.off;
+}
+
+// Alg. 1/2 step 3 (+ §5 blocks) into At: raw sketch S0 of the shard (skipped with
+// LSRN_REUSE_SKETCH when the cached S0 matches), its allreduce, then
+// At = sigma_X S0 + sigma_I G_block.  Events ev[1..3] bracket sketch / allreduce.
+void sketch_stage(lsrn_ctx* c, const lsrn_matrix* A_user, const lsrn_matrix* A, Plan& P, uint64_t seed, int flags,
+                  const void* ws, double* At) {
+  cudaStream_t st = c->stream;
+  const Dims& d = P.d;
+  const SketchKey key = make_key(A_user, d, seed, ws);
+  const bool reuse = (flags & LSRN_REUSE_SKETCH) != 0;
+  const bool hit = c->sketch_cached && std::memcmp(c->sketch_key, &key, sizeof(key)) == 0;
+  LSRN_REQUIRE(!reuse || hit, LSRN_EINVAL,
+               "LSRN_REUSE_SKETCH: this context holds no sketch of this A (pointers, shard, gamma, seed) in this workspace");
+  if (P.csr) csr_prepare(c, A, d, P.cw);   // CSC copy + heavy block (format conversion; also used by the iterations)
+  LSRN_CUDA(cudaEventRecord(c->ev[1], st));
+  if (!reuse) {
+    c->sketch_cached = false;
+    if (P.csr)
+      run_sketch_csr(c, d, seed, P.cw, P.S0);
+    else
+      run_sketch(c, A, d, seed, P.sw, P.S0);
+  }
+  LSRN_CUDA(cudaEventRecord(c->ev[2], st));
+  if (!reuse) {
+    allreduce(c, P.S0, d.s * d.k);
+    std::memcpy(c->sketch_key, &key, sizeof(key));
+    c->sketch_cached = true;
+  }
+  LSRN_CUDA(cudaEventRecord(c->ev[3], st));
+  finish_sketch(c, d, seed, P.S0, At);
 }
 
 // Stage host inputs (LSRN_HOST_IO) and return the device view of A.
@@ -875,16 +956,8 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
       b = PL.bstage;
       x = xstage;
     }
-    // ---- sketch (Alg. 1/2 step 3)
-    if (PL.csr) csr_prepare(c, &A, d, PL.cw);   // CSC copy + heavy block (format conversion)
-    LSRN_CUDA(cudaEventRecord(c->ev[1], st));
-    if (PL.csr)
-      run_sketch_csr(c, d, o->seed, PL.cw, At);
-    else
-      run_sketch(c, &A, d, o->seed, sw, At);
-    LSRN_CUDA(cudaEventRecord(c->ev[2], st));
-    allreduce(c, At, d.s * d.k);
-    LSRN_CUDA(cudaEventRecord(c->ev[3], st));
+    // ---- sketch (Alg. 1/2 step 3; §5 blocks)
+    sketch_stage(c, A_in, &A, PL, o->seed, o->flags, ws, At);
     // ---- SVD + N (steps 4-5), outside the hot path
     std::vector<double> S;
     const int64_t r = run_svd(c, d, At, vw, S);
@@ -1166,15 +1239,7 @@ lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double 
     LSRN_REQUIRE(ar.off == 0 || (ws != nullptr && ws_bytes >= ar.off), LSRN_ENOMEM,
                  "workspace too small for the sketch: need " + std::to_string(ar.off) + " bytes");
     c->launches = 0;
-    if (PL.csr) csr_prepare(c, A, d, PL.cw);
-    LSRN_CUDA(cudaEventRecord(c->ev[1], c->stream));
-    if (PL.csr)
-      run_sketch_csr(c, d, seed, PL.cw, At);
-    else
-      run_sketch(c, A, d, seed, PL.sw, At);
-    LSRN_CUDA(cudaEventRecord(c->ev[2], c->stream));
-    allreduce(c, At, d.s * d.k);
-    LSRN_CUDA(cudaEventRecord(c->ev[3], c->stream));
+    sketch_stage(c, A, A, PL, seed, 0, ws, At);
     LSRN_CUDA(cudaGetLastError());
     c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
     if (s_out) *s_out = d.s;

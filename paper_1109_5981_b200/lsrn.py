@@ -18,6 +18,7 @@ LSRN_DENSE, LSRN_CSR = 0, 1
 MODE_PREDICTABLE, MODE_ADAPTIVE = 0, 1
 HOST_IO = 1
 SKETCH_ONLY = 2
+REUSE_SKETCH = 4
 STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE", -4: "LSRN_ERANK0",
           -5: "LSRN_ESVD", -6: "LSRN_ENOMEM", -7: "LSRN_ECUDA", -8: "LSRN_ENCCL", -9: "LSRN_EUNSUPPORTED"}
 
@@ -229,7 +230,7 @@ class Context:
         return At
 
     def solve(self, X, b, m, n, solver="lsqr", gamma=2.0, lam=0.0, tol=1e-14, seed=5981, alpha=-1.0,
-              mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False):
+              mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False, reuse_sketch=False):
         """LSRN solve; X a long-index-major dense shard or a Csr row shard (device, or pinned host with host_io)."""
         if host_io and not isinstance(X, Csr):
             if X.dim() != 2 or X.stride(1) != 1:
@@ -246,7 +247,7 @@ class Context:
                                 pin_memory=bool(host_io))
         opts = Opts(gamma=gamma, lambda_=lam, tol=tol, alpha=alpha, seed=seed,
                     mode=MODE_ADAPTIVE if mode == "adaptive" else MODE_PREDICTABLE, max_iter=max_iter,
-                    flags=HOST_IO if host_io else 0)
+                    flags=(HOST_IO if host_io else 0) | (REUSE_SKETCH if reuse_sketch else 0))
         ws = self.workspace(self.workspace_size(mat, opts))
         rep = Report()
         fn = lib().lsrn_solve_lsqr if solver == "lsqr" else lib().lsrn_solve_cs
@@ -257,6 +258,15 @@ class Context:
                   ctypes.byref(rep)))
         self._leave(cur)
         return x_out, rep.as_dict()
+
+    def solve_path(self, X, b, m, n, lambdas, **kw):
+        """Solve for a sequence of Tikhonov lambdas, sketching A once (§5):
+        the first solve computes G A, the others reuse it (LSRN_REUSE_SKETCH)."""
+        out = []
+        for i, lam in enumerate(lambdas):
+            x, rep = self.solve(X, b, m, n, lam=lam, reuse_sketch=(i > 0), **kw)
+            out.append((x.clone(), rep))
+        return out
 
     def debug_box_muller(self, words, mode=0):
         """(count, 2) normals of the Box-Muller transform of (count, 4) uint32 Philox words."""

@@ -291,3 +291,27 @@ def test_box_muller_words_vs_oracle(ctx, mode):
     for col, ref in ((0, z0), (1, z1)):
         err = np.abs(got[:, col] - ref) / np.maximum(1.0, np.abs(ref))
         assert err.max() <= 2e-15, (col, err.max(), int(err.argmax()))
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+@pytest.mark.parametrize("shape", [(3000, 40), (40, 3000)])
+def test_lambda_path_reuses_the_sketch(ctx, solver, shape):
+    """NEXT-1, §5 (P:883-891): for a sequence of lambdas the sketch G A is computed once;
+    each solve on the path equals a fresh solve bit for bit and matches the ridge oracle."""
+    from paper_1109_5981_b200.lsrn import LsrnError
+    rng = np.random.default_rng(8)
+    m, n = shape
+    A = rng.standard_normal((m, n)) * np.logspace(0, -2, n if m >= n else m)[None, :] if m >= n else \
+        rng.standard_normal((m, n)) * np.logspace(0, -2, m)[:, None]
+    b = rng.standard_normal(m)
+    X = torch.from_numpy(A if m >= n else np.ascontiguousarray(A.T)).cuda()
+    bd = torch.from_numpy(b).cuda()
+    lams = [1e-1, 3e-2, 1e-3]
+    path = ctx.solve_path(X, bd, m, n, lams, solver=solver)
+    for lam, (x, rep) in zip(lams, path):
+        fresh, rep2 = ctx.solve(X, bd, m, n, solver=solver, lam=lam)
+        assert torch.equal(x, fresh) and rep["iters"] == rep2["iters"]
+        ref = brute.ridge(A, b, lam)
+        assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-9 * np.linalg.norm(ref)
+    with pytest.raises(LsrnError, match="EINVAL"):        # a different seed has no cached sketch
+        ctx.solve(X, bd, m, n, solver=solver, lam=0.5, seed=1, reuse_sketch=True)
