@@ -398,7 +398,9 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   // Wider rows (c5 k = 1e4, c4's N-pass k = 2e4): clusters of CTAs with slices of
   // up to 8192 doubles, one CTA per SM (deeper rings), asynchronous partial-dot exchange.
   const bool wide = C > kMaxSlice;
-  const int64_t max_slice = wide ? 2 * kMaxSlice : kMaxSlice;
+  int64_t max_slice = wide ? 2 * kMaxSlice : kMaxSlice;
+  if (const char* e = std::getenv("LSRN_ROWPASS_WIDE_SLICE"))   // tuning aid
+    if (wide) max_slice = std::max<int64_t>(512, std::atoll(e));
   int cl = (int)((C + max_slice - 1) / max_slice);
   if (cl > 16) return false;
   int64_t cq = (C + cl - 1) / cl;
