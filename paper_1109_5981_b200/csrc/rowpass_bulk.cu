@@ -407,6 +407,7 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   cq = (cq + 1) & ~int64_t(1);
   int vpt = 1;
   while (512 * vpt < cq) vpt = (vpt < 8) ? vpt * 2 : vpt + 4;   // 1, 2, 4, 8, 12, 16
+  if (vpt > 16) return false;                                     // no kernel instance: fallback
   int occ = wide ? 1 : 2;
   if (const char* e = std::getenv("LSRN_ROWPASS_OCC")) occ = std::atoi(e) == 1 ? 1 : 2;
   const size_t budget = kStageBudget / occ;
