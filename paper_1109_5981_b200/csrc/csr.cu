@@ -14,9 +14,9 @@
 //     ND heavy columns of row j;
 //   * the remaining nonzeros are sketched column-stationary from a CSC copy
 //     (csr_sketch_light): thread = sketch row i, one G[i, j] per nonzero.
-// The two threads of a Box-Muller pair (rows 2q, 2q+1, C9) split its
-// work: the even lane computes rho = sqrt(-2 ln u1), the odd lane sincospi(2 u2),
-// and they swap halves with one shuffle.
+// The two lanes of a Box-Muller pair (rows 2q, 2q+1, C9) take two
+// columns at a time: each evaluates one full pair (Philox + Box-Muller) for its
+// own column and one shuffle swaps the halves (gaussian_lane2).
 //
 // The CSC copy is built deterministically (per-chunk counts, exclusive scans,
 // in-order fill), so the sketch and the iterations are bitwise reproducible.
@@ -46,24 +46,22 @@ LSRN_DEV double block_sum(double v, double* sh) {
   return t;   // valid in thread 0
 }
 
-// G[i, j] for the calling lane's sketch row i, lanes (2q, 2q+1) cooperating on
-// the pair.  All 32 lanes of the warp must call it (with their own i, j equal
-// within each lane pair).  Returns z_{i & 1}.  T: shared-memory Box-Muller table.
-LSRN_DEV double gaussian_lane(uint2 key, uint64_t q, uint64_t j, bool odd, const double* T) {
-  const uint4 o = philox_counter(key, q, j);
-  double mine, other_cs = 0.0;
-  if (!odd) {
-    mine = sqrt(-2.0 * bm_ln_u1(o.x, o.y, T));        // rho
-  } else {
-    double sn, cs;
-    bm_sincos_2pi(o.z, o.w, T, sn, cs);
-    mine = sn;
-    other_cs = cs;
-  }
-  // even lane needs cos from its odd partner; odd lane needs rho from its even partner
-  const double send = odd ? other_cs : mine;
-  const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
-  return odd ? recv * mine : mine * recv;        // z1 = rho sin, z0 = rho cos
+// Two columns at once: G[i, ja] and G[i, jb] for the calling lane's sketch row i.
+// Lane 2q evaluates the whole pair (G[2q, ja], G[2q+1, ja]), lane 2q+1 the pair
+// (G[2q, jb], G[2q+1, jb]); one shuffle hands each lane the value it lacks.  Per
+// normal this is half a Philox call and half a Box-Muller pair with every lane
+// busy -- gaussian_lane (both lanes of a pair run the same Philox call) spends
+// twice the integer work (the first version did that: the c4 sketch took 13.9 s,
+// Philox-bound in the light part).
+LSRN_DEV void gaussian_lane2(uint2 key, uint64_t q, uint64_t ja, uint64_t jb, bool odd, const double* T,
+                             double& za, double& zb) {
+  double z0, z1;
+  box_muller_tab(philox_counter(key, q, odd ? jb : ja), T, z0, z1);
+  // even lane owns row 2q: keeps z0(ja), needs z0(jb) from the odd lane;
+  // odd lane owns row 2q+1: keeps z1(jb), needs z1(ja) from the even lane
+  const double recv = __shfl_xor_sync(0xffffffffu, odd ? z0 : z1, 1);
+  za = odd ? recv : z0;
+  zb = odd ? z1 : recv;
 }
 }  // namespace
 
@@ -204,13 +202,15 @@ csr_sketch_heavy_kernel(const double* __restrict__ D, int64_t rows, int64_t lo, 
       Ds[r][h] = (r < nj) ? D[(jb + r) * ND + h] : 0.0;
     }
     __syncthreads();
-    for (int r = 0; r < nj; ++r) {
-      const double z = gaussian_lane(key, q, (uint64_t)(lo + jb + r), odd, bmT);
+    for (int r = 0; r < nj; r += 2) {            // rows r, r+1 (Ds row nj is zero when nj is odd)
+      double za, zb;
+      gaussian_lane2(key, q, (uint64_t)(lo + jb + r), (uint64_t)(lo + jb + r + 1), odd, bmT, za, zb);
 #pragma unroll
       for (int h = 0; h < ND; h += 2) {
         const double2 d = *reinterpret_cast<const double2*>(&Ds[r][h]);
-        acc[h] = fma(z, d.x, acc[h]);
-        acc[h + 1] = fma(z, d.y, acc[h + 1]);
+        const double2 e = *reinterpret_cast<const double2*>(&Ds[r + 1][h]);
+        acc[h] = fma(zb, e.x, fma(za, d.x, acc[h]));
+        acc[h + 1] = fma(zb, e.y, fma(za, d.y, acc[h + 1]));
       }
     }
   }
@@ -249,9 +249,12 @@ csr_sketch_light_kernel(const int64_t* __restrict__ colptr, const int32_t* __res
         as[threadIdx.x] = cval[eb + threadIdx.x];
       }
       __syncthreads();
-      for (int e = 0; e < ne; ++e) {
-        const double z = gaussian_lane(key, q, (uint64_t)(lo + js[e]), odd, bmT);
-        acc = fma(z, as[e], acc);
+      for (int e = 0; e < ne; e += 2) {           // nonzeros e, e+1 (a = 0 past the end)
+        const bool two = e + 1 < ne;
+        double za, zb;
+        gaussian_lane2(key, q, (uint64_t)(lo + js[e]), (uint64_t)(lo + js[two ? e + 1 : e]), odd, bmT, za, zb);
+        acc = fma(za, as[e], acc);
+        if (two) acc = fma(zb, as[e + 1], acc);
       }
     }
     if (i < s) At[i * k + c] = acc;
