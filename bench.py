@@ -117,10 +117,11 @@ def cpu_baseline(cfg_name, solver, m_sample):
     from oracle.lsrn import solve as orc_solve
     from synth.generate import CONFIGS, make_problem
     cfg = CONFIGS[cfg_name]
-    if cfg["kind"] == "csr":
+    if min(cfg["m"], cfg["n"]) > 4096:
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                "unavailable": "c4: the oracle's 4e4 x 2e4 SVD alone exceeds the bench's few-minute budget; "
-                               "a row sample with m < n would change the problem"}
+                "unavailable": f"{cfg_name}: the oracle's SVD of the {2 * min(cfg['m'], cfg['n'])} x "
+                               f"{min(cfg['m'], cfg['n'])} sketch alone exceeds the bench's few-minute budget; "
+                               "shrinking the short dimension would change the problem"}
     p = make_problem(cfg_name, m=m_sample, n=cfg["n"]) if cfg["m"] >= cfg["n"] else \
         make_problem(cfg_name, m=cfg["m"], n=m_sample)
     A = p.to_scipy() if p.kind == "csr" else p.dense_A().numpy()
@@ -172,7 +173,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "t4"])
     ap.add_argument("--solver", default="lsqr", choices=["lsqr", "cs"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -24,12 +24,13 @@
  *     i.e. the library always sees X = A (tall) or X = A^T (wide) as a
  *     row-major L x k matrix, L = max(m, n), k = min(m, n).  ld >= k, and the
  *     fast (16-byte vector) paths need ld even and val 16-byte aligned.
- *   - CSR A (kind LSRN_CSR, tall only): rows [lo, lo+cnt) of A; rowptr has
+ *   - CSR (kind LSRN_CSR): the long-index-major X in CSR -- X = A for m >= n,
+ *     X = A^T for m < n (i.e. a wide A given in CSC).  Rows [lo, lo+cnt) of X; rowptr has
  *     cnt+1 entries (rowptr[0] may be non-zero: entry e of local row r is
- *     colind/val[rowptr[r] - rowptr[0] + e]), colind int32 in [0, n) and
- *     strictly increasing within each row (canonical CSR: sorted, no
- *     duplicates), val fp64.  A violation returns LSRN_EINVAL.  n <= 24576
- *     (the CSC build keeps one cursor per column in shared memory).
+ *     colind/val[rowptr[r] - rowptr[0] + e]), colind int32 in [0, k),
+ *     k = min(m, n), strictly increasing within each row (canonical CSR:
+ *     sorted, no duplicates), val fp64.  A violation returns LSRN_EINVAL.
+ *     k <= 24576 (the CSC build keeps one cursor per column in shared memory).
  *   - Multi-GPU: every rank calls with the SAME opts/seed; A is sharded along
  *     the long index (rows of a tall A, columns of a wide A): rank p holds
  *     [lo, lo + cnt).  b is the rank's shard of b (tall) or the full b (wide).

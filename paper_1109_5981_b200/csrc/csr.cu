@@ -1,4 +1,5 @@
-// K4 (CSR sketch) and the CSR long pass (K6-CSR) for sparse tall A.
+// K4 (CSR sketch) and the CSR long pass (K6-CSR) for sparse A in the tall form:
+// X = A (m >= n) as CSR, or X = A^T (m < n) as CSR of A^T, i.e. A in CSC.
 //
 // The paper notes that LSRN "automatically speeds up when A is sparse" because
 // it only touches A through products (Abstract; §4.1) and
@@ -300,8 +301,9 @@ template <int ND>
 __global__ void __launch_bounds__(THR)
 csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
                   const double* __restrict__ val, int64_t rows, const double* __restrict__ t,
-                  const int* __restrict__ colmap, const double* __restrict__ coef, double* __restrict__ u,
-                  double* __restrict__ npart, double* __restrict__ wpart, const int* __restrict__ done) {
+                  const int* __restrict__ colmap, const double* __restrict__ coef, double sx, double* __restrict__ u,
+                  double* __restrict__ acc, double* __restrict__ npart, double* __restrict__ wpart,
+                  const int* __restrict__ done) {
   __shared__ double sh[THR / 32];
   __shared__ double wd[THR / 32][ND > 0 ? ND : 1];
   if (done != nullptr && *done != 0) return;
@@ -311,7 +313,8 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
   if (ND > 0)
     for (int h = lane; h < ND; h += 32) wd[wib][h] = 0.0;
   __syncwarp();
-  const double c1 = coef[0], c2 = coef[1];
+  const double c1 = coef[0], c2 = coef[1] * sx;
+  const double ca = (acc != nullptr) ? coef[2] : 0.0;
   const int64_t base = rowptr[0];
   double nrm = 0.0;
   const int64_t per = (rows + nwarps - 1) / nwarps;
@@ -323,7 +326,10 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
     d = warp_sum(d);
     const double uo = __shfl_sync(0xffffffffu, lane == 0 ? u[r] : 0.0, 0);
     const double un = fma(c1, uo, c2 * d);
-    if (lane == 0) u[r] = un;
+    if (lane == 0) {
+      u[r] = un;
+      if (acc != nullptr) acc[r] = fma(ca, un, acc[r]);   // CS, Alg. 2 form: x += alpha v on the long side
+    }
     nrm = fma(un, un, nrm);
     if (ND > 0) {
       for (int64_t e = e0 + lane; e < e1; e += 32) {
@@ -340,7 +346,7 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
     for (int h = threadIdx.x; h < ND; h += THR) {
       double v = 0.0;
       for (int w = 0; w < THR / 32; ++w) v += wd[w][h];
-      wpart[(int64_t)blockIdx.x * ND + h] = v;
+      wpart[(int64_t)blockIdx.x * ND + h] = sx * v;
     }
   }
 }
@@ -350,7 +356,7 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
 // Tikhonov block and ||u||^2 as in colreduce_kernel: out = [w ; ||u||^2 + ||zI||^2].
 __global__ void __launch_bounds__(THR)
 csr_colgather_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
-                     const double* __restrict__ cval, int64_t k, const double* __restrict__ u,
+                     const double* __restrict__ cval, int64_t k, double sx, const double* __restrict__ u,
                      const int* __restrict__ colmap, const double* __restrict__ wpart, int ND,
                      const double* __restrict__ npart, int nparts, double* __restrict__ zI,
                      const double* __restrict__ t, const double* __restrict__ coef, double sI,
@@ -369,6 +375,7 @@ csr_colgather_kernel(const int64_t* __restrict__ colptr, const int32_t* __restri
       for (int g = lane; g < nparts; g += 32) w += wpart[(int64_t)g * ND + h];
     } else {
       for (int64_t e = colptr[c] + lane; e < colptr[c + 1]; e += 32) w = fma(cval[e], u[rowidx[e]], w);
+      w *= sx;
     }
     w = warp_sum(w);
     if (zI != nullptr) {
@@ -476,7 +483,7 @@ cudaError_t launch_sketch_add_gblock(double* At, int64_t s, int64_t k, int64_t L
 cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st) {
   const unsigned nb = (unsigned)a.nblocks;
 #define LSRN_ROWDOT(ND_) csr_rowdot_kernel<ND_><<<nb, THR, 0, st>>>(a.rowptr, a.colind, a.val, a.rows, a.t, \
-      a.colmap, a.coef, a.u, a.npart, a.wpart, a.done)
+      a.colmap, a.coef, a.sx, a.u, a.acc, a.npart, a.wpart, a.done)
   switch (a.ND) {
     case 0: LSRN_ROWDOT(0); break;
     case 16: LSRN_ROWDOT(16); break;
@@ -489,7 +496,7 @@ cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st) {
 
 cudaError_t launch_csr_colgather(const CsrGatherArgs& a, cudaStream_t st) {
   csr_colgather_kernel<<<(unsigned)csr_colgather_blocks(a.k), THR, 0, st>>>(
-      a.colptr, a.rowidx, a.cval, a.k, a.u, a.colmap, a.wpart, a.ND, a.npart, a.nparts, a.zI, a.t, a.coef, a.sI,
+      a.colptr, a.rowidx, a.cval, a.k, a.sx, a.u, a.colmap, a.wpart, a.ND, a.npart, a.nparts, a.zI, a.t, a.coef, a.sI,
       a.out, a.blockpart,
       a.counter, a.done);
   return cudaGetLastError();

@@ -149,8 +149,10 @@ struct CsrRowdotArgs {
   int64_t rows;
   const double* t;
   const int* colmap;
-  const double* coef;
+  const double* coef;      // {c1, c2, ca}
+  double sx;               // sigma_X (1/lambda for the wide Tikhonov form)
   double* u;
+  double* acc;             // nullable: acc_j += ca u_j (CS, wide form)
   double* npart;           // [nblocks]
   double* wpart;           // [nblocks][ND]
   const int* done;
@@ -163,6 +165,7 @@ struct CsrGatherArgs {
   const int32_t* rowidx;
   const double* cval;
   int64_t k;
+  double sx;
   const double* u;
   const int* colmap;
   const double* wpart;

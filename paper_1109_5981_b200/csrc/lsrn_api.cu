@@ -142,9 +142,9 @@ Dims make_dims(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, b
     LSRN_REQUIRE(A->ld >= d.k, LSRN_EDIM, "leading dimension ld must be >= min(m, n)");
     LSRN_REQUIRE(A->val != nullptr || d.cnt == 0, LSRN_EINVAL, "A->val is NULL");
   } else if (A->kind == LSRN_CSR) {
-    LSRN_REQUIRE(d.tall, LSRN_EUNSUPPORTED, "CSR A must be tall (m >= n); pass a wide sparse A as its transpose");
+    // X is always the long-index-major matrix: CSR of A (m >= n) or CSR of A^T (m < n, i.e. A in CSC)
     LSRN_REQUIRE((size_t)d.k <= csr_max_k(), LSRN_EUNSUPPORTED,
-                 "CSR path supports n <= " + std::to_string(csr_max_k()) + " columns");
+                 "CSR path supports min(m, n) <= " + std::to_string(csr_max_k()));
     LSRN_REQUIRE(A->nnz >= 0, LSRN_EDIM, "nnz must be >= 0");
     LSRN_REQUIRE(d.cnt == 0 || A->rowptr != nullptr, LSRN_EINVAL, "A->rowptr is NULL");
     LSRN_REQUIRE(A->nnz == 0 || (A->colind != nullptr && A->val != nullptr), LSRN_EINVAL,
@@ -564,7 +564,7 @@ struct Pass {
   const CsrWs* cw = nullptr;   // CSR A: rowdot + colgather instead of the dense row pass
 
   // CSR long pass (tall only): z <- c1 z + c2 A t ; out = [A^T z (+ I block) ; ||z||^2]
-  void long_pass_csr(double* z, const double* t, const double* coef, const int* done, double* out) {
+  void long_pass_csr(double* z, const double* t, const double* coef, double* acc, const int* done, double* out) {
     cudaStream_t st = c->stream;
     const int idx = c->n_pass_ev;
     const bool prof = c->profile && idx + 2 <= (int)c->pass_ev.size();
@@ -577,7 +577,9 @@ struct Pass {
     a.t = t;
     a.colmap = cw->colmap;
     a.coef = coef;
+    a.sx = d.sx;
     a.u = z;
+    a.acc = acc;
     a.npart = cw->npart;
     a.wpart = cw->wpart;
     a.done = done;
@@ -589,6 +591,7 @@ struct Pass {
     g.rowidx = cw->rowidx;
     g.cval = cw->cval;
     g.k = d.k;
+    g.sx = d.sx;
     g.u = z;
     g.colmap = cw->colmap;
     g.wpart = cw->wpart;
@@ -615,7 +618,7 @@ struct Pass {
   // long pass over X: z <- c1 z + c2 sX X t (+ I block), out = [P^T z ; ||z||^2]
   void long_pass(double* z, const double* t, const double* coef, double* acc, const int* done, double* out) {
     if (cw != nullptr) {
-      long_pass_csr(z, t, coef, done, out);
+      long_pass_csr(z, t, coef, acc, done, out);
       return;
     }
     cudaStream_t st = c->stream;

@@ -39,6 +39,11 @@ CONFIGS = {
                nnz_random=20, dense_cols=50, dense_scale=1e3, rhs="randn"),
     "c5": dict(num=5, kind="dense", m=1_000_000, n=10_000, gamma=2.0, lam=0.0,
                spectrum="colscale", log_range=5.0, rhs="model"),
+    # NEXT-2: the shape of the paper's cluster workload tnimg_4 (Table 3,
+    # P:1207-1219): 1024 x 4e6, ~21 nonzeros per column; the real
+    # TinyImages data is not available, so columns get 21 distinct uniform rows, N(0,1).
+    "t4": dict(num=6, kind="csr", m=1024, n=4_000_000, gamma=2.0, lam=0.0,
+               nnz_random=21, dense_cols=0, dense_scale=1.0, rhs="randn"),
 }
 
 
@@ -66,16 +71,20 @@ class Problem:
         """A itself (a view for dense; materialised for CSR)."""
         if self.kind == "dense":
             return self.X if self.tall else self.X.T
-        A = torch.zeros(self.m, self.n, dtype=torch.float64, device=self.val.device)
-        rows = torch.repeat_interleave(torch.arange(self.m, device=self.val.device),
+        L, k = max(self.m, self.n), min(self.m, self.n)
+        X = torch.zeros(L, k, dtype=torch.float64, device=self.val.device)
+        rows = torch.repeat_interleave(torch.arange(L, device=self.val.device),
                                        self.rowptr[1:] - self.rowptr[:-1])
-        A[rows, self.colind.long()] = self.val
-        return A
+        X[rows, self.colind.long()] = self.val
+        return X if self.tall else X.T
 
     def to_scipy(self):
+        """A itself as scipy CSR (for a wide A the stored CSR is that of A^T)."""
         import scipy.sparse as sp
-        return sp.csr_matrix((self.val.cpu().numpy(), self.colind.cpu().numpy(),
-                              self.rowptr.cpu().numpy()), shape=(self.m, self.n))
+        L, k = max(self.m, self.n), min(self.m, self.n)
+        X = sp.csr_matrix((self.val.cpu().numpy(), self.colind.cpu().numpy(),
+                           self.rowptr.cpu().numpy()), shape=(L, k))
+        return X if self.tall else X.T.tocsr()
 
 
 def _haar(L, r, gen, device):
@@ -176,14 +185,14 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
 
     if kind == "csr":
         nr = cfg["nnz_random"]
-        nd = min(cfg["dense_cols"], n - nr) if n > nr else 0
-        pool = n - nd
+        nd = min(cfg["dense_cols"], k - nr) if k > nr else 0   # columns of X (k = min(m, n))
+        pool = k - nd
         nnz_row = nr + nd
         # integer strata [floor(i pool / nr), floor((i+1) pool / nr)): one uniform draw in
         # each, so the nr random columns of a row are distinct and sorted
         edges = (torch.arange(nr + 1, device=device, dtype=torch.int64) * pool) // nr
         lo_e, wid = edges[:-1], (edges[1:] - edges[:-1]).to(torch.float64)
-        cols_d = torch.arange(pool, n, device=device, dtype=torch.int64)
+        cols_d = torch.arange(pool, k, device=device, dtype=torch.int64)
         rows = hi - lo
         colind = torch.empty(rows, nnz_row, dtype=torch.int32, device=device)
         val = torch.empty(rows, nnz_row, **f64)
@@ -204,6 +213,8 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
             b[a0 - lo:a1 - lo] = bb[a0 - g0:a1 - g0]
         rowptr = torch.arange(rows + 1, device=device, dtype=torch.int64) * nnz_row
         meta.update(nnz=rows * nnz_row, dense_cols=nd)
+        if m < n:             # wide: X = A^T in CSR (A in CSC); b is short (length m), replicated
+            b = torch.randn(m, generator=gx, **f64)
         return Problem(name, m, n, "csr", cfg["gamma"], cfg["lam"], b, rowptr=rowptr,
                        colind=colind.reshape(-1), val=val.reshape(-1), meta=meta)
     raise ValueError(f"unknown spectrum/kind for {name}")
@@ -212,11 +223,13 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
 def small(name, device="cpu"):
     """Scaled-down instances used by CPU tests (same recipe, oracle-fast sizes)."""
     shapes = {"c1": (2000, 100), "c2": (3000, 120), "c3": (60, 3000),
-              "c4": (6000, 200), "c5": (4000, 150)}
+              "c4": (6000, 200), "c5": (4000, 150), "t4": (64, 6000)}
     m, n = shapes[name]
     over = {}
     if name == "c4":
         over = dict(nnz_random=8, dense_cols=6)
+    if name == "t4":
+        over = dict(nnz_random=5)
     return make_problem(name, device=device, m=m, n=n, **over)
 
 

@@ -146,11 +146,34 @@ def test_csr_host_io_matches_device(ctx):
     assert torch.equal(xd.cpu(), xh) and rd["iters"] == rh["iters"]
 
 
-def test_csr_rejects_wide(ctx):
-    from paper_1109_5981_b200.lsrn import LsrnError
-    A = _random_csr(50, 400, 3, 0, 1.0, 0, seed=1)
-    with pytest.raises(LsrnError, match="EUNSUPPORTED"):
-        ctx.sketch(_gpu_csr(A), 50, 400)
+@pytest.mark.parametrize("lam", [0.0, 0.05])
+def test_csr_wide_sketch_vs_oracle(ctx, lam):
+    """Wide sparse A (m < n) given as the CSR of A^T (Alg. 2; §5 wide form)."""
+    AT = _random_csr(3000, 60, 4, 3, 10.0, 2, seed=21)          # X = A^T: 3000 x 60, A: 60 x 3000
+    m, n = 60, 3000
+    At = ctx.sketch(_gpu_csr(AT), m, n, 2.0, lam, seed=5981).cpu().numpy()
+    p = orc_plan(m, n, 2.0, lam)
+    ref = orc_sketch(AT, p["s"], 5981, p["sigma_x"], p["sigma_i"])
+    assert _relfro(At, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+@pytest.mark.parametrize("lam", [0.0, 0.05])
+def test_csr_wide_solve_vs_oracle_and_dense(ctx, solver, lam):
+    """Wide CSR solves (NEXT-2 shape: few rows, many sparse columns) against the oracle and the
+    dense wide path on the same matrix."""
+    AT = _random_csr(2500, 50, 5, 2, 5.0, 0, seed=33)
+    A = AT.T.tocsr()
+    m, n = 50, 2500
+    b = np.random.default_rng(2).standard_normal(m)
+    x1, r1 = ctx.solve(_gpu_csr(AT), torch.from_numpy(b).cuda(), m, n, solver=solver, lam=lam)
+    x2, r2 = ctx.solve(torch.from_numpy(AT.toarray()).cuda(), torch.from_numpy(b).cuda(), m, n, solver=solver,
+                       lam=lam)
+    orc = orc_solve(A, b, solver=solver, lam=lam)
+    assert r1["iters"] == r2["iters"] == orc["iters"] and r1["r"] == orc["r"]
+    for x in (x1, x2):
+        rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
+        assert rel <= 1e-9, rel
 
 
 @pytest.mark.parametrize("bad", ["dup", "unsorted", "range"])
@@ -165,3 +188,17 @@ def test_csr_rejects_non_canonical(ctx, bad):
     X = Csr(rowptr.cuda(), torch.tensor(cols, dtype=torch.int32).cuda(), ones)
     with pytest.raises(LsrnError, match="EINVAL"):
         ctx.sketch(X, 6, 5, 1.5)
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_csr_small_t4_vs_oracle(ctx, solver):
+    """NEXT-2 recipe (tnimg-shaped: few rows, ~21 nonzeros per column) at test size."""
+    from paper_1109_5981_b200.lsrn import Csr
+    p = small("t4")
+    A = p.to_scipy()
+    b = p.b.numpy()
+    x, rep = ctx.solve(Csr(p.rowptr.cuda(), p.colind.cuda(), p.val.cuda()), p.b.cuda(), p.m, p.n, solver=solver)
+    orc = orc_solve(A, b, solver=solver)
+    assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
+    rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
+    assert rel <= 1e-9, rel

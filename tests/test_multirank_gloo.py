@@ -130,10 +130,11 @@ def test_sharded_chebyshev_allreduce_equals_single_process():
     _run(_cs_shards)
 
 
-def test_c4_recipe_rows_are_canonical_csr():
-    """The CSR generator honours lsrn.h's contract: sorted, distinct columns per row."""
+@pytest.mark.parametrize("name", ["c4", "t4"])
+def test_csr_recipes_are_canonical(name):
+    """The CSR generators honour lsrn.h's contract: sorted, distinct columns per row of X."""
     from synth.generate import small
-    p = small("c4")
+    p = small(name)
     rp, ci = p.rowptr.numpy(), p.colind.numpy()
     assert all(np.all(np.diff(ci[rp[i]:rp[i + 1]]) > 0) for i in range(p.m))
-    assert ci.min() >= 0 and ci.max() < p.n
+    assert ci.min() >= 0 and ci.max() < min(p.m, p.n)

@@ -22,7 +22,7 @@ from synth.generate import CONFIGS, make_problem, small
 
 
 def test_plan_configs():
-    exp_s = {"c1": 200, "c2": 4000, "c3": 4000, "c4": 40000, "c5": 20000}
+    exp_s = {"c1": 200, "c2": 4000, "c3": 4000, "c4": 40000, "c5": 20000, "t4": 2048}   # Table 3: s = 2048
     for c, cfg in CONFIGS.items():
         p = plan(cfg["m"], cfg["n"], cfg["gamma"], cfg["lam"])
         assert p["s"] == exp_s[c]
