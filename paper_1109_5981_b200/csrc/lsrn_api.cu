@@ -353,10 +353,13 @@ void allreduce(lsrn_ctx* c, double* buf, int64_t count);
 
 // Alg. 1/2 step 3 with the §5 blocks, from the raw (allreduced) sketch S0:
 //   At = sigma_X S0 + sigma_I G[:, L:L+k]   (every rank; G is deterministic)
+// With one rank and a partial shard (lo > 0: a testing / manual-reduction use of
+// lsrn_sketch) the block belongs to the shard that starts the long index, so
+// that partial sketches still sum to the full one.
 void finish_sketch(lsrn_ctx* c, const Dims& d, uint64_t seed, const double* S0, double* At) {
   LSRN_CUDA(launch_copy_scale(At, S0, d.sx, d.s * d.k, c->stream));
   c->launches++;
-  if (d.si != 0.0) {
+  if (d.si != 0.0 && (c->nranks > 1 || d.lo == 0)) {
     LSRN_CUDA(launch_sketch_add_gblock(At, d.s, d.k, d.L, d.si, seed, c->stream, c->nsm));
     c->launches++;
   }
