@@ -291,7 +291,7 @@ def main():
     roof_lp = {"kernel": "csr_rowdot + csr_colgather (K6-CSR)" if csr else "rowpass_bulk_kernel long pass (K6)",
                "bound": "hbm", "achieved": lp_gbs, "peak": hbm_peak,
                "unit": "GB/s", "frac": (lp_gbs / hbm_peak) if lp_gbs else None, "traffic": None,
-               "algorithmic": f"{lp_bytes:.4g} B per pass ({'12 nnz + 24 rows + 12 light-CSC' if csr else 'rows*(8k+16)'})",
+               "algorithmic": f"{lp_bytes:.4g} B per pass ({'12 nnz + 24 rows (+ 12 light-CSC if k > 2048)' if csr else 'rows*(8k+16)'})",
                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", "share_of_step": lp_share}
     traffic = load_traffic(args.config)
     roof_sketch["traffic"] = traffic.get("sketch")

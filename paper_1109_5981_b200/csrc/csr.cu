@@ -351,6 +351,91 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
   }
 }
 
+// Single-pass CSR long pass for short rows of w (k <= csr_rowdot_all_max_k()):
+// the same u update as csr_rowdot_kernel, and w = sx X^T u accumulated for ALL
+// columns in per-warp shared-memory copies (the columns of one row are distinct,
+// so lanes never collide), reduced over the block's warps in fixed order into
+// wpart[block][k]; colreduce_kernel then sums the blocks and adds the norm.  X is
+// read once per pass and no CSC gather is needed (the paper's t4 shape has
+// k = 1024 columns of 82 000 nonzeros each: a warp-per-column gather had only
+// 1024 warps of work and ran at 0.97 TB/s).
+__global__ void __launch_bounds__(THR)
+csr_rowdot_all_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                      const double* __restrict__ val, int64_t rows, int64_t k, const double* __restrict__ t,
+                      const double* __restrict__ coef, double sx, double* __restrict__ u, double* __restrict__ acc,
+                      double* __restrict__ npart, double* __restrict__ wpart, const int* __restrict__ done) {
+  extern __shared__ double wsh[];            // [THR / 32][k]
+  __shared__ double sh[THR / 32];
+  if (done != nullptr && *done != 0) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* wd = wsh + (int64_t)wib * k;
+  for (int64_t c = lane; c < k; c += 32) wd[c] = 0.0;
+  __syncwarp();
+  const int64_t warp = ((int64_t)blockIdx.x * THR + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * THR) >> 5;
+  const double c1 = coef[0], c2 = coef[1] * sx;
+  const double ca = (acc != nullptr) ? coef[2] : 0.0;
+  const int64_t base = rowptr[0];
+  double nrm = 0.0;
+  const int64_t per = (rows + nwarps - 1) / nwarps;
+  const int64_t r0 = warp * per, r1 = min(rows, r0 + per);
+  // two rows per step (independent loads and reductions in flight); rows of <= 32
+  // entries (the common sparse case) keep (c, a) in registers for the w update.
+  // (Four rows of eight lanes each ran slower: 0.81 vs 1.27 TB/s on t4.)
+  for (int64_t r = r0; r < r1; r += 2) {
+    const bool has2 = r + 1 < r1;
+    const int64_t ea0 = rowptr[r] - base, ea1 = rowptr[r + 1] - base;
+    const int64_t eb1 = has2 ? rowptr[r + 2] - base : ea1;
+    int ca_ = 0, cb_ = 0;
+    double aa = 0.0, ab = 0.0, da = 0.0, db = 0.0;
+    if (ea0 + lane < ea1) {
+      ca_ = colind[ea0 + lane];
+      aa = ldg_stream1(val + ea0 + lane);
+      da = aa * __ldg(t + ca_);
+    }
+    if (ea1 + lane < eb1) {
+      cb_ = colind[ea1 + lane];
+      ab = ldg_stream1(val + ea1 + lane);
+      db = ab * __ldg(t + cb_);
+    }
+    for (int64_t e = ea0 + 32 + lane; e < ea1; e += 32) da = fma(val[e], __ldg(t + colind[e]), da);
+    for (int64_t e = ea1 + 32 + lane; e < eb1; e += 32) db = fma(val[e], __ldg(t + colind[e]), db);
+    const double uoa = lane == 0 ? u[r] : 0.0;
+    const double uob = (lane == 0 && has2) ? u[r + 1] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      da += __shfl_xor_sync(0xffffffffu, da, o);
+      db += __shfl_xor_sync(0xffffffffu, db, o);
+    }
+    const double una = fma(c1, __shfl_sync(0xffffffffu, uoa, 0), c2 * da);
+    const double unb = fma(c1, __shfl_sync(0xffffffffu, uob, 0), c2 * db);
+    if (lane == 0) {
+      u[r] = una;
+      if (acc != nullptr) acc[r] = fma(ca, una, acc[r]);
+      nrm = fma(una, una, nrm);
+      if (has2) {
+        u[r + 1] = unb;
+        if (acc != nullptr) acc[r + 1] = fma(ca, unb, acc[r + 1]);
+        nrm = fma(unb, unb, nrm);
+      }
+    }
+    if (ea0 + lane < ea1) wd[ca_] = fma(aa, una, wd[ca_]);
+    for (int64_t e = ea0 + 32 + lane; e < ea1; e += 32) wd[colind[e]] = fma(val[e], una, wd[colind[e]]);
+    __syncwarp();                           // row b may share columns with row a
+    if (ea1 + lane < eb1) wd[cb_] = fma(ab, unb, wd[cb_]);
+    for (int64_t e = ea1 + 32 + lane; e < eb1; e += 32) wd[colind[e]] = fma(val[e], unb, wd[colind[e]]);
+    __syncwarp();
+  }
+  const double b = block_sum(nrm, sh);     // contains __syncthreads: every warp's wd complete
+  if (threadIdx.x == 0) npart[blockIdx.x] = b;
+  for (int64_t c = threadIdx.x; c < k; c += THR) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < THR / 32; ++w) v += wsh[(int64_t)w * k + c];
+    wpart[(int64_t)blockIdx.x * k + c] = sx * v;
+  }
+}
+
 // w_c = sum_{(j,a) in col c} a u_j (light columns: warp per column, lanes stride
 // the CSC column; heavy columns: the row pass's block partials);
 // Tikhonov block and ||u||^2 as in colreduce_kernel: out = [w ; ||u||^2 + ||zI||^2].
@@ -407,6 +492,21 @@ csr_colgather_kernel(const int64_t* __restrict__ colptr, const int32_t* __restri
 int64_t csr_chunk_rows() { return 8192; }
 int64_t csr_nchunks(int64_t rows) { return rows > 0 ? (rows + csr_chunk_rows() - 1) / csr_chunk_rows() : 0; }
 int csr_rowdot_blocks(int nsm) { return nsm * 8; }
+int64_t csr_rowdot_all_max_k() { return 2048; }      // 8 warps x k doubles of shared memory (128 KB)
+// CTAs of 8 warps, as many per SM as the per-warp w copies (8 k doubles) allow
+int csr_rowdot_all_blocks(int nsm, int64_t k) {
+  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (200 * 1024) / (64 * k)));
+  return (int)(nsm * per_sm);
+}
+
+cudaError_t launch_csr_rowdot_all(const CsrRowdotArgs& a, int64_t k, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)(THR / 32) * (size_t)k;
+  cudaError_t e = cudaFuncSetAttribute(csr_rowdot_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  csr_rowdot_all_kernel<<<(unsigned)a.nblocks, THR, smem, st>>>(a.rowptr, a.colind, a.val, a.rows, k, a.t, a.coef,
+                                                                 a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
+  return cudaGetLastError();
+}
 int csr_colgather_blocks(int64_t k) { return (int)((k * 32 + THR - 1) / THR); }
 size_t csr_max_k() { return 24 * 1024; }     // CSC cursors (int64) of a chunk live in shared memory
 

@@ -159,6 +159,10 @@ struct CsrRowdotArgs {
   int ND, nblocks;
 };
 cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st);
+// single-pass variant for k <= csr_rowdot_all_max_k(): wpart[nblocks][k], then colreduce
+int64_t csr_rowdot_all_max_k();
+int csr_rowdot_all_blocks(int nsm, int64_t k);
+cudaError_t launch_csr_rowdot_all(const CsrRowdotArgs& a, int64_t k, cudaStream_t st);
 
 struct CsrGatherArgs {
   const int64_t* colptr;

@@ -232,8 +232,10 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
   w.nsplit = nsplit;
   w.rows_per_split = std::max<int64_t>(1, (d.cnt + nsplit - 1) / nsplit);
   w.part = ar.take<double>((size_t)nsplit * d.s * kMaxHeavy);
-  w.npart = ar.take<double>((size_t)csr_rowdot_blocks(c->nsm));
-  w.wpart = ar.take<double>((size_t)csr_rowdot_blocks(c->nsm) * kMaxHeavy);
+  w.npart = ar.take<double>((size_t)std::max(csr_rowdot_blocks(c->nsm), csr_rowdot_all_blocks(c->nsm, d.k)));
+  const size_t wp_heavy = (size_t)csr_rowdot_blocks(c->nsm) * kMaxHeavy;
+  const size_t wp_all = d.k <= csr_rowdot_all_max_k() ? (size_t)csr_rowdot_all_blocks(c->nsm, d.k) * d.k : 0;
+  w.wpart = ar.take<double>(std::max(wp_heavy, wp_all));
   return w;
 }
 
@@ -587,6 +589,32 @@ struct Pass {
     a.wpart = cw->wpart;
     a.done = done;
     a.ND = cw->ND;
+    if (d.k <= csr_rowdot_all_max_k()) {
+      // single pass: w for every column accumulated in shared memory, then the fixed-order block sum
+      a.nblocks = csr_rowdot_all_blocks(c->nsm, d.k);
+      LSRN_CUDA(launch_csr_rowdot_all(a, d.k, st));
+      ColReduceArgs r{};
+      r.wpart = cw->wpart;
+      r.npart = cw->npart;
+      r.nparts = a.nblocks;
+      r.C = d.k;
+      r.zI = d.has_I ? z + d.cnt : nullptr;
+      r.t = t;
+      r.coef = coef;
+      r.sI = d.si;
+      r.out = out;
+      r.blockpart = w.blockpart;
+      r.counter = w.counters;
+      r.done = done;
+      LSRN_CUDA(launch_colreduce(r, st));
+      if (prof) {
+        LSRN_CUDA(cudaEventRecordWithFlags(c->pass_ev[idx + 1], st, cudaEventRecordExternal));
+        c->n_pass_ev += 2;
+      }
+      c->launches += 2;
+      allreduce(c, out, d.k + 1);
+      return;
+    }
     a.nblocks = csr_rowdot_blocks(c->nsm);
     LSRN_CUDA(launch_csr_rowdot(a, st));
     CsrGatherArgs g{};
@@ -1192,7 +1220,9 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     c->stats[4] = (double)nlp;
     // algorithmic bytes of one long pass: dense rows (8k + 16 per row);
     // CSR: the CSR stream (12 B per nonzero + 8 B rowptr + 16 B u per row) + the light CSC (12 B per entry)
-    c->stats[5] = PL.csr ? (12.0 * (double)A_in->nnz + 24.0 * (double)d.cnt + 12.0 * (double)PL.cw.nnz_light)
+    // (k <= 2048: single pass over the CSR, no CSC read in the iterations)
+    const double csc_bytes = d.k <= csr_rowdot_all_max_k() ? 0.0 : 12.0 * (double)PL.cw.nnz_light;
+    c->stats[5] = PL.csr ? (12.0 * (double)A_in->nnz + 24.0 * (double)d.cnt + csc_bytes)
                          : (double)d.cnt * ((double)d.k * 8.0 + 16.0);
     c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
     c->stats[7] = (double)graph_launches;

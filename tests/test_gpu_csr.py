@@ -202,3 +202,16 @@ def test_csr_small_t4_vs_oracle(ctx, solver):
     assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
     rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
     assert rel <= 1e-9, rel
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_csr_solve_wide_k_uses_csc_gather(ctx, solver):
+    """k > 2048: the CSR long pass gathers w = A^T u from the CSC copy (light columns) and the
+    heavy block (for k <= 2048 it accumulates w in shared memory in one pass)."""
+    A = _random_csr(4400, 2100, 4, 3, 20.0, 0, seed=41)
+    b = np.random.default_rng(3).standard_normal(4400)
+    x, rep = ctx.solve(_gpu_csr(A), torch.from_numpy(b).cuda(), 4400, 2100, solver=solver, gamma=1.5)
+    orc = orc_solve(A, b, solver=solver, gamma=1.5, precise_g=False)
+    assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
+    rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
+    assert rel <= 1e-9, rel
