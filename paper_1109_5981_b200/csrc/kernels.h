@@ -15,6 +15,7 @@ struct SketchDenseArgs {
   int nsplit;
   double* out;       // [nsplit][s][k]
   int64_t out_split_stride;
+  int accumulate = 0;   // 1: out += partial (stream-ordered chunks of A, host-IO streaming)
 };
 size_t sketch_dense_smem();
 void sketch_tile_counts(int64_t s, int64_t k, int64_t* mtiles, int64_t* ntiles, int64_t* bk);

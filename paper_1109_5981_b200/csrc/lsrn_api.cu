@@ -92,6 +92,10 @@ struct lsrn_ctx {
   cusolverDnHandle_t solver = nullptr;
   cusolverDnParams_t params = nullptr;
   std::vector<char> host_ws;          // cuSOLVER 64-bit API host workspace
+  // host-IO streaming of A: copy stream + per-chunk events
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ev[16] = {};
+  cudaEvent_t io_ev = nullptr;
   // raw sketch cache (λ-path reuse): key of the sketch held in the workspace
   bool sketch_cached = false;
   unsigned char sketch_key[160] = {};
@@ -176,13 +180,39 @@ int choose_nsplit(int64_t s, int64_t k, int64_t rows, int nsm) {
 }
 
 struct SketchWs {
-  int nsplit;
-  int64_t rows_per_split;
-  double* part;   // nullptr if direct
+  int nsplit = 1;
+  int64_t rows_per_split = 0;
+  double* part = nullptr;   // nullptr if direct
+  // LSRN_HOST_IO streaming: A arrives in nchunk H2D chunks; chunk i is sketched (split-K
+  // nsplit inside the chunk) as soon as it lands and accumulated into the nsplit partials
+  int nchunk = 0;
+  int64_t rows_per_chunk = 0;
 };
 
-SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_flag) {
+// Host-IO streaming: A is copied in chunks of >= 128 MB on a second stream and
+// each chunk is sketched as soon as it has landed, so the H2D copy of A
+// overlaps the sketch (one split-K slot per chunk, summed in fixed order).
+int stream_chunks(const Dims& d, int64_t ld) {
+  const double bytes = 8.0 * (double)d.cnt * (double)ld;
+  static const double chunk_mb = [] {
+    const char* e = std::getenv("LSRN_HOSTIO_CHUNK_MB");   // test / tuning knob
+    return (e && std::atof(e) > 0.0) ? std::atof(e) : 128.0;
+  }();
+  const int n = (int)std::ceil(bytes / (chunk_mb * 1024 * 1024));
+  return std::max(1, std::min(16, std::min(n, (int)std::max<int64_t>(1, d.cnt / 256))));
+}
+
+SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_flag, int force_chunks = 0) {
   SketchWs w{};
+  if (force_chunks > 1) {
+    const int64_t rpc = (d.cnt + force_chunks - 1) / force_chunks;
+    w.rows_per_chunk = std::max<int64_t>(16, (rpc + 15) / 16 * 16);
+    w.nchunk = (int)((d.cnt + w.rows_per_chunk - 1) / w.rows_per_chunk);
+    w.nsplit = choose_nsplit(d.s, d.k, w.rows_per_chunk, c->nsm);
+    w.rows_per_split = (w.rows_per_chunk + w.nsplit - 1) / w.nsplit;
+    w.part = ar.take<double>((size_t)w.nsplit * d.s * d.k);
+    return w;
+  }
   w.nsplit = choose_nsplit(d.s, d.k, d.cnt, c->nsm);
   int64_t rps = (d.cnt + w.nsplit - 1) / w.nsplit;
   rps = (rps + 15) / 16 * 16;
@@ -322,6 +352,31 @@ void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double*
 // Raw sketch S0 = G[:, lo:lo+cnt] X_shard of a dense shard (split-K partials summed in fixed order).
 void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed, const SketchWs& w, double* At) {
   cudaStream_t st = c->stream;
+  if (w.nchunk > 1) {          // one launch per H2D chunk, each after its copy event
+    for (int i = 0; i < w.nchunk; ++i) {
+      const int64_t r0 = (int64_t)i * w.rows_per_chunk;
+      const int64_t nr = std::min(w.rows_per_chunk, d.cnt - r0);
+      LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[i], 0));
+      SketchDenseArgs a{};
+      a.X = A->val + r0 * A->ld;
+      a.ld = A->ld;
+      a.rows = nr;
+      a.k = d.k;
+      a.lo = d.lo + r0;
+      a.s = d.s;
+      a.seed = seed;
+      a.rows_per_split = w.rows_per_split;
+      a.nsplit = w.nsplit;
+      a.out = w.part;
+      a.out_split_stride = d.s * d.k;
+      a.accumulate = i > 0;   // chunks are stream-ordered: fixed summation order
+      LSRN_CUDA(launch_sketch_dense(a, st));
+      c->launches++;
+    }
+    LSRN_CUDA(launch_sketch_finish(w.part, w.nsplit, d.s * d.k, d.s, d.k, 1.0, 0.0, d.L, seed, At, st, c->nsm));
+    c->launches++;
+    return;
+  }
   if (d.cnt > 0) {
     SketchDenseArgs a{};
     a.X = A->val;
@@ -774,6 +829,9 @@ lsrn_status lsrn_ctx_create(lsrn_ctx** out, void* stream, int nranks, int rank, 
     LSRN_SOLVER(cusolverDnSetStream(c->solver, c->stream));
     LSRN_SOLVER(cusolverDnCreateParams(&c->params));
     for (auto& e : c->ev) LSRN_CUDA(cudaEventCreate(&e));
+    LSRN_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : c->chunk_ev) LSRN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    LSRN_CUDA(cudaEventCreateWithFlags(&c->io_ev, cudaEventDisableTiming));
     if (nranks > 1) {
 #ifdef LSRN_WITH_NCCL
       LSRN_REQUIRE(nccl_id != nullptr, LSRN_EINVAL, "nccl_id required for nranks > 1");
@@ -801,6 +859,10 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->pass_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->chunk_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->io_ev) cudaEventDestroy(c->io_ev);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->params) cusolverDnDestroyParams(c->params);
   if (c->solver) cusolverDnDestroy(c->solver);
 #ifdef LSRN_WITH_NCCL
@@ -875,7 +937,8 @@ size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar
   if (P.csr)
     P.cw = plan_csr(c, d, A, ar);
   else
-    P.sw = plan_sketch(c, d, ar, c->nranks > 1);
+    P.sw = plan_sketch(c, d, ar, c->nranks > 1,
+                       ((o->flags & LSRN_HOST_IO) && solve && d.cnt > 0) ? stream_chunks(d, A->ld) : 0);
   if (solve) {
     P.vw = plan_svd(c, d, ar);
     // max passes: LSQR cap (2x the count for r = k) or CS passes with r = k; bounded by a generous margin
@@ -906,6 +969,8 @@ void sketch_stage(lsrn_ctx* c, const lsrn_matrix* A_user, const lsrn_matrix* A, 
     else
       run_sketch(c, A, d, seed, P.sw, P.S0);
   }
+  // streamed host IO: everything after the sketch reads all of A
+  if (P.sw.nchunk > 1) LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[P.sw.nchunk - 1], 0));
   LSRN_CUDA(cudaEventRecord(c->ev[2], st));
   if (!reuse) {
     allreduce(c, P.S0, d.s * d.k);
@@ -931,6 +996,19 @@ lsrn_matrix stage_inputs(lsrn_ctx* c, const lsrn_matrix* A_in, const lsrn_opts* 
     }
     A.rowptr = P.rpstage;
     A.colind = P.cistage;
+    A.val = P.Astage;
+  } else if (P.sw.nchunk > 1) {
+    // chunks on the copy stream (after everything already queued on the main stream,
+    // which may still read the staging buffer); the sketch waits per chunk
+    LSRN_CUDA(cudaEventRecord(c->io_ev, st));
+    LSRN_CUDA(cudaStreamWaitEvent(c->copy_stream, c->io_ev, 0));
+    for (int i = 0; i < P.sw.nchunk; ++i) {
+      const int64_t r0 = (int64_t)i * P.sw.rows_per_chunk;
+      const int64_t nr = std::min(P.sw.rows_per_chunk, d.cnt - r0);
+      LSRN_CUDA(cudaMemcpyAsync(P.Astage + r0 * A_in->ld, A_in->val + r0 * A_in->ld, sizeof(double) * nr * A_in->ld,
+                                cudaMemcpyHostToDevice, c->copy_stream));
+      LSRN_CUDA(cudaEventRecord(c->chunk_ev[i], c->copy_stream));
+    }
     A.val = P.Astage;
   } else {
     if (d.cnt > 0)
@@ -966,7 +1044,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     validate_opts(o);
     LSRN_REQUIRE(A_in != nullptr && b_in != nullptr && x_out != nullptr, LSRN_EINVAL, "A, b or x is NULL");
     Arena ar(ws);
-    Plan PL;
+    Plan PL{};
     const size_t need = plan_all(c, A_in, o, ar, PL, false);
     Dims& d = PL.d;
     SketchWs& sw = PL.sw;
@@ -984,12 +1062,19 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     const double* b = b_in;
     double* x = x_out;
     LSRN_CUDA(cudaEventRecord(c->ev[0], st));
-    lsrn_matrix A = stage_inputs(c, A_in, o, PL);
     if (o->flags & LSRN_HOST_IO) {
-      LSRN_CUDA(cudaMemcpyAsync(PL.bstage, b_in, sizeof(double) * (d.tall ? d.cnt : d.m), cudaMemcpyHostToDevice, st));
+      // streamed A: b goes first on the copy stream (st waits for the last chunk of A
+      // before the iterations); st itself then issues no H2D copy the sketch could queue behind
+      cudaStream_t bs = PL.sw.nchunk > 1 ? c->copy_stream : st;
+      if (bs != st) {
+        LSRN_CUDA(cudaEventRecord(c->io_ev, st));
+        LSRN_CUDA(cudaStreamWaitEvent(bs, c->io_ev, 0));
+      }
+      LSRN_CUDA(cudaMemcpyAsync(PL.bstage, b_in, sizeof(double) * (d.tall ? d.cnt : d.m), cudaMemcpyHostToDevice, bs));
       b = PL.bstage;
       x = xstage;
     }
+    lsrn_matrix A = stage_inputs(c, A_in, o, PL);
     // ---- sketch (Alg. 1/2 step 3; §5 blocks)
     sketch_stage(c, A_in, &A, PL, o->seed, o->flags, ws, At);
     // ---- SVD + N (steps 4-5), outside the hot path
@@ -1206,6 +1291,9 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
       rep->t_iter = elapsed_s(c->ev[6], c->ev[7]);
       rep->t_total = elapsed_s(c->ev[0], c->ev[7]);
     }
+    if (std::getenv("LSRN_DEBUG_EVENTS")) {   // stage boundaries ev[0..7] (diagnostics)
+      for (int i = 0; i < 7; ++i) std::fprintf(stderr, "ev%d-ev%d %.3f ms\n", i, i + 1, elapsed_s(c->ev[i], c->ev[i + 1]) * 1e3);
+    }
     // ---- stats
     c->stats[0] = elapsed_s(c->ev[1], c->ev[2]) * 1e3;
     double lp = 0.0;
@@ -1251,7 +1339,7 @@ lsrn_status lsrn_workspace_size(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_op
     LSRN_REQUIRE(c != nullptr && bytes != nullptr, LSRN_EINVAL, "NULL argument");
     validate_opts(o);
     Arena ar(nullptr);
-    Plan PL;
+    Plan PL{};
     *bytes = plan_all(c, A, o, ar, PL, true, (o->flags & LSRN_SKETCH_ONLY) == 0) + 256;
     return LSRN_OK;
   } catch (const Fail& f) {
@@ -1269,7 +1357,7 @@ lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double 
     o.tol = 0.5;
     o.seed = seed;
     Arena ar(ws);
-    Plan PL;
+    Plan PL{};
     plan_all(c, A, &o, ar, PL, /*allow_partial=*/true, /*solve=*/false);
     const Dims& d = PL.d;
     LSRN_REQUIRE(ar.off == 0 || (ws != nullptr && ws_bytes >= ar.off), LSRN_ENOMEM,

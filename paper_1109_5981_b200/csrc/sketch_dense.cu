@@ -36,7 +36,7 @@ template <int VEC>
 __global__ void __launch_bounds__(sk::THREADS, 1)
 sketch_dense_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k,
                     int64_t lo, int64_t s, uint64_t seed, int64_t rows_per_split,
-                    double* __restrict__ out, int64_t out_split_stride) {
+                    double* __restrict__ out, int64_t out_split_stride, int accumulate) {
   using namespace sk;
   extern __shared__ __align__(16) double smem[];
   __shared__ double bmT[bm::TAB_SIZE];       // Box-Muller tables (philox_bm.cuh)
@@ -153,10 +153,16 @@ sketch_dense_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int6
       const int64_t gc = n0 + wn * 64 + j * 8 + 2 * (lane & 3);
       double* p = o + gi * k + gc;
       if (gc + 1 < k && (k % 2 == 0)) {
-        *reinterpret_cast<double2*>(p) = make_double2(acc[i][j][0], acc[i][j][1]);
+        double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (accumulate) {
+          const double2 w = *reinterpret_cast<const double2*>(p);
+          v.x = w.x + v.x;
+          v.y = w.y + v.y;
+        }
+        *reinterpret_cast<double2*>(p) = v;
       } else {
-        if (gc < k) p[0] = acc[i][j][0];
-        if (gc + 1 < k) p[1] = acc[i][j][1];
+        if (gc < k) p[0] = accumulate ? p[0] + acc[i][j][0] : acc[i][j][0];
+        if (gc + 1 < k) p[1] = accumulate ? p[1] + acc[i][j][1] : acc[i][j][1];
       }
     }
   }
@@ -248,12 +254,12 @@ cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st) {
     e = cudaFuncSetAttribute(sketch_dense_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     sketch_dense_kernel<2><<<grid, THREADS, SMEM_BYTES, st>>>(a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
-                                                             a.rows_per_split, a.out, a.out_split_stride);
+                                                             a.rows_per_split, a.out, a.out_split_stride, a.accumulate);
   } else {
     e = cudaFuncSetAttribute(sketch_dense_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
     sketch_dense_kernel<1><<<grid, THREADS, SMEM_BYTES, st>>>(a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
-                                                             a.rows_per_split, a.out, a.out_split_stride);
+                                                             a.rows_per_split, a.out, a.out_split_stride, a.accumulate);
   }
   return cudaGetLastError();
 }

@@ -96,7 +96,7 @@ template <int CL>
 __global__ void __launch_bounds__(ws::THREADS, 1)
 sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
                  uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride,
-                 int diag) {
+                 int diag, int accumulate) {
   using namespace ws;
   extern __shared__ __align__(128) double smem[];
   double* Xs = smem;                                   // [NSX][BK][A_LD]
@@ -249,9 +249,15 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
     for (int j = 0; j < 8; ++j) {
       const int64_t gc = n0 + wn * 64 + j * 8 + 2 * (lane & 3);
       if (gc + 1 < k) {
-        *reinterpret_cast<double2*>(o + gi * k + gc) = make_double2(acc[i][j][0], acc[i][j][1]);
+        double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (accumulate) {
+          const double2 w = *reinterpret_cast<const double2*>(o + gi * k + gc);
+          v.x = w.x + v.x;
+          v.y = w.y + v.y;
+        }
+        *reinterpret_cast<double2*>(o + gi * k + gc) = v;
       } else if (gc < k) {
-        o[gi * k + gc] = acc[i][j][0];
+        o[gi * k + gc] = accumulate ? o[gi * k + gc] + acc[i][j][0] : acc[i][j][0];
       }
     }
   }
@@ -284,7 +290,7 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, dim3 grid, cudaStream_t
   int diag = 0;
   if (const char* e = std::getenv("LSRN_SKETCH_DIAG")) diag = std::atoi(e);
   return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
-                            a.rows_per_split, a.out, a.out_split_stride, diag);
+                            a.rows_per_split, a.out, a.out_split_stride, diag, a.accumulate);
 }
 
 // Cluster size along N: the largest of {max_cl, ..., 2} dividing the N-tile count.

@@ -10,6 +10,8 @@ Tolerances (north star):
 """
 import math
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -188,6 +190,36 @@ def test_host_io_matches_device(ctx):
     xh, reph = ctx.solve(p.X.pin_memory(), p.b.pin_memory(), p.m, p.n, solver="cs", host_io=True)
     assert torch.equal(xd.cpu(), xh)
     assert repd["iters"] == reph["iters"]
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_host_io_streamed(ctx, solver):
+    """LSRN_HOST_IO with A streamed in chunks (each sketched as soon as its copy lands; the
+    chunk size is read once per process, so a subprocess sets it): same solution as the
+    device-resident call up to the split-K summation order of the sketch."""
+    import subprocess
+    import sys
+    code = (
+        "import torch, numpy as np\n"
+        "from paper_1109_5981_b200 import lsrn\n"
+        "g = torch.Generator().manual_seed(5)\n"
+        "m, n = 40000, 60\n"
+        "X = torch.randn(m, n, generator=g, dtype=torch.float64)\n"
+        "b = torch.randn(m, generator=g, dtype=torch.float64)\n"
+        "c = lsrn.Context()\n"
+        f"xd, rd = c.solve(X.cuda(), b.cuda(), m, n, solver='{solver}')\n"
+        f"xh, rh = c.solve(X.pin_memory(), b.pin_memory(), m, n, solver='{solver}', host_io=True)\n"
+        "xs = np.linalg.lstsq(X.numpy(), b.numpy(), rcond=None)[0]\n"
+        "assert rd['iters'] == rh['iters'], (rd, rh)\n"
+        "e1 = float(np.linalg.norm(xd.cpu().numpy() - xh.numpy()) / np.linalg.norm(xs))\n"
+        "e2 = float(np.linalg.norm(xh.numpy() - xs) / np.linalg.norm(xs))\n"
+        "assert e1 <= 1e-12 and e2 <= 1e-10, (e1, e2)\n"
+        "print('ok', e1, e2)\n"
+    )
+    env = dict(os.environ, LSRN_HOSTIO_CHUNK_MB="2")      # 19.2 MB of A -> 10 chunks
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_repeat_solves_bitwise(ctx):
