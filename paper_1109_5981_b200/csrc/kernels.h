@@ -24,6 +24,7 @@ bool sketch_ws_supported(const SketchDenseArgs& a);
 bool sketch_batch_supported(const SketchDenseArgs& a);
 cudaError_t launch_sketch_batch(const SketchDenseArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st);
+void sketch_ws_tile_dims(int64_t* bm, int64_t* bn, int64_t* bk);
 cudaError_t launch_sketch_finish(const double* part, int nsplit, int64_t split_stride, int64_t s, int64_t k,
                                  double sx, double si, int64_t L, uint64_t seed, double* out, cudaStream_t st,
                                  int nsm);

@@ -82,27 +82,38 @@ LSRN_DEV void bm_load_table(double* Ts) {
     Ts[i] = bm::kTable[i];
 }
 
-LSRN_DEV double bm_ln_u1(uint32_t lo, uint32_t hi, const double* T) {
+// x = -2 ln u1 >= 0 (the square of the Box-Muller radius).  The polynomial is
+// evaluated in Estrin form and the -2 is folded into the table terms: the
+// transform shares the FP64 pipe with DMMA in the dense sketch, where each
+// dependent FP64 instruction waits behind the queued DMMAs, so the length of the
+// dependency chain (not the instruction count) sets the producers' rate.
+LSRN_DEV double bm_m2ln_u1(uint32_t lo, uint32_t hi, const double* T) {
   const uint64_t w0 = (static_cast<uint64_t>(hi) << 32) | lo;
   const uint64_t n1 = (w0 >> 11) + 1ull;                        // 1 .. 2^53
   const int e = 63 - __clzll(static_cast<long long>(n1));      // 0 .. 53
   const uint64_t mant = (e <= 52) ? ((n1 << (52 - e)) & 0xFFFFFFFFFFFFFull) : 0ull;
   const double m = __longlong_as_double(static_cast<long long>(0x3FF0000000000000ull | mant));
   const int i = static_cast<int>(mant >> 45);
-  const double r = fma(m, T[i], -1.0);
-  double p = bm::LOG1P_C8;
-  p = fma(p, r, bm::LOG1P_C7);
-  p = fma(p, r, bm::LOG1P_C6);
-  p = fma(p, r, bm::LOG1P_C5);
-  p = fma(p, r, bm::LOG1P_C4);
-  p = fma(p, r, bm::LOG1P_C3);
-  p = fma(p, r, bm::LOG1P_C2);
-  const double poly = fma(r * r, p, r);
+  const double r = fma(m, T[i], -1.0);                          // exact, |r| < 2^-7
+  // log1p(r) = r + r^2 p(r), p = C2 + C3 r + ... + C8 r^6 (Estrin)
+  const double r2 = r * r;
+  const double m2r = -2.0 * r;
+  const double a0 = fma(bm::LOG1P_C3, r, bm::LOG1P_C2);
+  const double a1 = fma(bm::LOG1P_C5, r, bm::LOG1P_C4);
+  const double a2 = fma(bm::LOG1P_C7, r, bm::LOG1P_C6);
+  const double r4 = r2 * r2;
+  const double q1 = fma(a1, r2, a0);
+  const double q2 = fma(bm::LOG1P_C8, r2, a2);
+  const double p = fma(q2, r4, q1);
+  const double poly = fma(-2.0 * r2, p, m2r);                   // -2 log1p(r)
   const double E = static_cast<double>(e - 53);
-  const double thi = fma(E, bm::LN2_HI, T[128 + i]);
-  const double tlo = fma(E, bm::LN2_LO, T[256 + i]);
+  const double thi = fma(E, -2.0 * bm::LN2_HI, -2.0 * T[128 + i]);   // exact (42-bit heads, x2 exact)
+  const double tlo = fma(E, -2.0 * bm::LN2_LO, -2.0 * T[256 + i]);
   return thi + (tlo + poly);
 }
+
+// ln u1 (kept for reference / tests): -x / 2, exact scaling.
+LSRN_DEV double bm_ln_u1(uint32_t lo, uint32_t hi, const double* T) { return -0.5 * bm_m2ln_u1(lo, hi, T); }
 
 LSRN_DEV void bm_sincos_2pi(uint32_t lo, uint32_t hi, const double* T, double& sn, double& cs) {
   const uint64_t w1 = (static_cast<uint64_t>(hi) << 32) | lo;
@@ -112,17 +123,17 @@ LSRN_DEV void bm_sincos_2pi(uint32_t lo, uint32_t hi, const double* T, double& s
   const uint64_t dm = n2 & ((1ull << 45) - 1);
   const double d = __longlong_as_double(static_cast<long long>(0x3FF0000000000000ull | (dm << 7))) - 1.0;
   const double d2 = d * d;
-  double sp = bm::SIN_C9;
-  sp = fma(sp, d2, bm::SIN_C7);
-  sp = fma(sp, d2, bm::SIN_C5);
-  sp = fma(sp, d2, bm::SIN_C3);
-  sp = fma(sp, d2, bm::SIN_C1);
+  const double d4 = d2 * d2;
+  // sin b = d (S1 + S3 d^2 + ... + S9 d^8), cos b = 1 + d^2 (C2 + C4 d^2 + ... + C10 d^8) (Estrin)
+  const double b0 = fma(bm::SIN_C3, d2, bm::SIN_C1);
+  const double b1 = fma(bm::SIN_C7, d2, bm::SIN_C5);
+  const double c0 = fma(bm::COS_C4, d2, bm::COS_C2);
+  const double c1 = fma(bm::COS_C8, d2, bm::COS_C6);
+  const double b1b = fma(bm::SIN_C9, d4, b1);
+  const double c1b = fma(bm::COS_C10, d4, c1);
+  const double sp = fma(b1b, d4, b0);
+  const double cp = fma(c1b, d4, c0);
   const double sb = sp * d;
-  double cp = bm::COS_C10;
-  cp = fma(cp, d2, bm::COS_C8);
-  cp = fma(cp, d2, bm::COS_C6);
-  cp = fma(cp, d2, bm::COS_C4);
-  cp = fma(cp, d2, bm::COS_C2);
   const double cb = fma(cp, d2, 1.0);
   const double sa = T[384 + j], ca = T[448 + j];
   const double s = fma(sa, cb, ca * sb);
@@ -132,8 +143,21 @@ LSRN_DEV void bm_sincos_2pi(uint32_t lo, uint32_t hi, const double* T, double& s
   cs = (k == 0) ? c : (k == 1) ? -s : (k == 2) ? -c : s;
 }
 
+// sqrt(x) for x in [0, 74] with a short chain: y0 = rsqrt.approx (MUFU.RSQ64H),
+// s0 = x y0, e = 1 - s0 y0, sqrt(x) = s0 (1 + e/2 + 3 e^2 / 8 + O(e^3)); x = 0 -> 0.
+LSRN_DEV double bm_sqrt(double x) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  const double s0 = x * y0;
+  const double e = fma(-s0, y0, 1.0);
+  const double t = fma(e, 0.375, 0.5);
+  const double u = s0 * e;
+  const double r = fma(u, t, s0);
+  return x > 0.0 ? r : 0.0;
+}
+
 LSRN_DEV void box_muller_tab(uint4 o, const double* T, double& z0, double& z1) {
-  const double rho = sqrt(-2.0 * bm_ln_u1(o.x, o.y, T));
+  const double rho = bm_sqrt(bm_m2ln_u1(o.x, o.y, T));
   double sn, cs;
   bm_sincos_2pi(o.z, o.w, T, sn, cs);
   z0 = rho * cs;

@@ -293,9 +293,10 @@ cudaError_t launch_debug_box_muller(const uint32_t* words, int64_t count, int mo
 }
 
 void sketch_tile_counts(int64_t s, int64_t k, int64_t* mtiles, int64_t* ntiles, int64_t* bk) {
-  *mtiles = (s + sk::BM - 1) / sk::BM;
-  *ntiles = (k + sk::BN - 1) / sk::BN;
-  *bk = sk::BK;
+  int64_t bm, bn;
+  sketch_ws_tile_dims(&bm, &bn, bk);     // the default (warp-specialized) kernel's tile
+  *mtiles = (s + bm - 1) / bm;
+  *ntiles = (k + bn - 1) / bn;
 }
 
 }  // namespace lsrn

@@ -9,30 +9,36 @@
 // DMMA, one __syncthreads per k-block) kept the tensor pipe 62 % active on c2
 // (profiles/r01_ncu_full_sketch_rowpass.json): after each barrier all warps sat
 // in the latency-bound Box-Muller phase together.  Here the roles are split:
-//   warpgroups 0-1 (8 producer warps, setmaxnreg 56): one lane streams X tiles
-//     into a shared-memory ring with 1-D TMA bulk copies; all 256 threads
-//     generate the 64 x 16 G tile of each k-block into a second ring;
-//   warpgroups 2-3 (8 consumer warps, setmaxnreg 200): DMMA.8x8x4 on 32 x 64
-//     warp tiles, never touching RNG, released stage by stage with mbarriers.
-// Measured on c2 (profiles/r01_sketch_tune*.jsonl): with the RNG switched off the
-// consumers reach 33.8 TFLOP/s (92 % of the DMMA peak); with it, 25.5 TFLOP/s.
-// The Box-Muller FP64 instructions cost far more than their issue count: each
-// competes with the consumers' DMMAs for the shared FP64 pipe.  Variants tried
-// and rejected: 4 producer warps (66 ms vs 62.7), producers batching 4-8 pairs
-// per thread (register-starved), X streamed by a consumer warp (serialises the
-// consumers), batched RNG phases in a non-specialized kernel (sketch_batch.cu,
-// 73.9 ms).
-// The RNG shares the FP64 pipe with DMMA (measured), so each
-// normal must be generated as few times as possible: the CTAs of a cluster of
-// CL along N (same sketch rows, same k-range, different column tiles) need the
-// SAME G tile, so CTA q generates rows [q BM/CL, (q+1) BM/CL) of it into its own
-// ring and pushes that slice to the other CL-1 CTAs with async-proxy
-// shared->shared bulk copies (cp.async.bulk.shared::cluster.shared::cta) that
-// complete on the destination's `gfull` barrier; consumers release a G stage on
-// every CTA of the cluster with plain remote arrives.  RNG work per CTA drops by
-// CL.  (Without the sharing the consumers waited on the G ring 29 % of the time;
-// distributing with st.shared::cluster + release/acquire.cluster barriers cost
-// a MEMBAR.GPU / L1 invalidate per stage and ran 2x slower.)
+//   warpgroups 0-1 (8 producer warps, setmaxnreg 56): lane 0 of warp 0 streams
+//     X tiles into a shared-memory ring with 1-D TMA bulk copies; each producer
+//     warp generates its own rows of the BM x BK G tile of every k-block into a
+//     second ring and arrives on that stage's barrier by itself (no barrier
+//     across producer warps);
+//   warpgroups 2-3 (8 consumer warps, setmaxnreg 200): DMMA.8x8x4 on
+//     (BM/2) x (BN/4) warp tiles, never touching RNG, released stage by stage
+//     with mbarriers.
+// The RNG shares the FP64 pipe with DMMA: in the ncu source view
+// (profiles/r01_ncu_ws_source.txt) the producers' first FP64 instruction of each
+// pair waits behind the consumers' queued DMMAs ("math pipe throttle") and the
+// consumers wait on the G ring ~21 % of the time, although FP64 ALU work is
+// only ~3 % of the pipe.  So each normal must be generated as few times as
+// possible per flop: the default tile is 32 x 512 (each normal feeds 512
+// columns).  Measured on c2 (profiles/r01_sketch_tile.jsonl, _nsg, _npw):
+// 64 x 256 / cluster 2 -> 60.3 ms, 32 x 512 / no cluster -> 58.1 ms (27.5
+// TFLOP/s, 75 % of the DMMA peak); with the RNG switched off the same kernel
+// reaches 49.3 ms (88 %).  Rejected: 4 producer warps with two interleaved
+// pairs per lane (66 ms), deeper G rings (no change), BK = 8 (70 ms), X
+// streamed by a consumer warp (serialises the consumers), batched RNG phases
+// in a non-specialized kernel (sketch_batch.cu, 73.9 ms).
+// Clusters (64 x 256 tile only by default): the CTAs of a cluster of CL along N
+// (same sketch rows, same k-range, different column tiles) need the SAME G
+// tile, so each producer warp of CTA q generates its rows of slice q and
+// pushes them to the other CL-1 CTAs with async-proxy shared->shared bulk
+// copies (cp.async.bulk.shared::cluster.shared::cta) that complete on the
+// destination's `gfull` barrier; consumers release a G stage on every CTA of
+// the cluster with plain remote arrives.  (Distributing with st.shared::cluster
+// + release/acquire.cluster barriers cost a MEMBAR.GPU / L1 invalidate per
+// stage and ran 2x slower.)
 //
 // Requirements (else the caller uses sketch_dense_kernel): ld even, X 16-byte
 // aligned, k even (every bulk row segment is a multiple of 16 bytes).
@@ -45,16 +51,24 @@
 namespace lsrn {
 
 namespace ws {
-constexpr int BM = 64, BN = 256, BK = 16;
-constexpr int NSX = 4, NSG = 4;             // X ring and G ring depth
-constexpr int A_LD = BN + 8;                // padded smem row (doubles)
-constexpr int G_LD = BK + 4;
-constexpr int X_STAGE = BK * A_LD;          // doubles
-constexpr int G_STAGE = BM * G_LD;
-constexpr int NPROD = 256;                 // producer threads (2 warpgroups)
-constexpr int THREADS = NPROD + 256;
-constexpr int NCONS_WARPS = 8;
-constexpr size_t SMEM_BYTES = sizeof(double) * (size_t)(NSX * X_STAGE + NSG * G_STAGE) + 128;
+constexpr int NPW = 8;                      // producer warps
+constexpr int THREADS = NPW * 32 + 256;     // launch 128 regs; producers 56, consumers 200
+constexpr int NCONS_WARPS = 8;              // consumers: 2 (M) x 4 (N) warps
+// CTA tile BM x BN (BM = 64: warp tile 32 x 64; BM = 32: 16 x 128; 32 accumulator
+// fragments per lane either way), k-block BK, X ring NSX deep, G ring NSG deep.
+template <int BM_, int BN_, int BK_, int NSX_, int NSG_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, NSX = NSX_, NSG = NSG_;
+  static constexpr int A_LD = BN + 8;       // padded smem row (doubles)
+  static constexpr int G_LD = BK + 4;
+  static constexpr int X_STAGE = BK * A_LD; // doubles
+  static constexpr int G_STAGE = BM * G_LD;
+  static constexpr int MI = BM / 16;        // 8-row fragments per warp (2 warps along M)
+  static constexpr int NJ = BN / 32;        // 8-col fragments per warp (4 warps along N)
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(NSX * X_STAGE + NSG * G_STAGE) + 128;
+  static_assert(MI * NJ == 32, "32 accumulator fragments per lane");
+  static_assert(BK % 4 == 0, "k-block is a multiple of the DMMA k = 4");
+};
 }  // namespace ws
 
 namespace {
@@ -92,12 +106,15 @@ LSRN_DEV void cluster_sync_all() {
 }
 }  // namespace
 
-template <int CL>
+template <class C, int CL>
 __global__ void __launch_bounds__(ws::THREADS, 1)
 sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
                  uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride,
                  int diag, int accumulate) {
   using namespace ws;
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, NSX = C::NSX, NSG = C::NSG;
+  constexpr int A_LD = C::A_LD, G_LD = C::G_LD, X_STAGE = C::X_STAGE, G_STAGE = C::G_STAGE;
+  constexpr int MI = C::MI, NJ = C::NJ;
   extern __shared__ __align__(128) double smem[];
   double* Xs = smem;                                   // [NSX][BK][A_LD]
   double* Gs = smem + NSX * X_STAGE;                   // [NSG][BM][G_LD]
@@ -113,14 +130,13 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
 
   const unsigned qrank = (CL > 1) ? cluster_rank() : 0u;
   constexpr int SLICE_ROWS = BM / CL;                  // G rows generated by this CTA
-  constexpr unsigned SLICE_BYTES = (unsigned)(SLICE_ROWS * G_LD * sizeof(double));
   if (tid == 0) {
     for (int i = 0; i < NSX; ++i) {
       mbar_init(&xfull[i], 1);
       mbar_init(&xempty[i], NCONS_WARPS);
     }
     for (int i = 0; i < NSG; ++i) {
-      mbar_init(&gfull[i], 1);                          // local producer leader (+ tx of CL-1 remote slices)
+      mbar_init(&gfull[i], NPW);                        // one per local producer warp (+ tx of remote rows)
       mbar_init(&gempty[i], NCONS_WARPS * CL);          // one per consumer warp of each CTA of the cluster
     }
     mbar_fence_init();
@@ -129,14 +145,24 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
     cluster_sync_all();                                 // every CTA's barriers exist before remote traffic
   else
     __syncthreads();
+  static_assert(CL >= 1 && BM % CL == 0, "cluster size must divide BM");
 
-  if (warp < NPROD / 32) {
+  if (warp < NPW) {
     // ------------------------------------------------------------ producers
+    // Each producer warp owns ROWS_W consecutive rows of this CTA's G slice and runs
+    // its own flow (no barrier across producer warps): wait for the stage to be
+    // free, generate its PPT pairs per lane (independent chains, interleaved),
+    // store, push its rows to the other CTAs of the cluster, arrive on gfull.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    constexpr int ROWS_W = SLICE_ROWS / NPW;            // G rows per producer warp (even)
+    static_assert(ROWS_W >= 2 && ROWS_W % 2 == 0, "each producer warp needs whole row pairs");
+    constexpr int PAIRS_W = (ROWS_W / 2) * BK;
+    constexpr int PPT = (PAIRS_W + 31) / 32;
+    constexpr unsigned WBYTES = (unsigned)(ROWS_W * G_LD * sizeof(double));
     const uint2 key = philox_key(seed);
-    const int ptid = tid;                                // 0..127
-    for (int i = ptid; i < bm::TAB_SIZE; i += NPROD) bmT[i] = bm::kTable[i];
-    named_bar(1, NPROD);
+    for (int i = tid; i < bm::TAB_SIZE; i += NPW * 32) bmT[i] = bm::kTable[i];
+    named_bar(1, NPW * 32);
+    const int row0 = (int)qrank * SLICE_ROWS + warp * ROWS_W;   // first G row of this warp in the tile
     const int64_t ncols = min((int64_t)BN, k - n0);      // even (k even, n0 multiple of BN)
     const unsigned seg_bytes = (unsigned)(ncols * 8);
     for (int kb = 0; kb < nk; ++kb) {
@@ -158,43 +184,50 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
         }
       }
       // G stage sg must be free on every CTA of the cluster, and (CL > 1) the bulk
-      // copies that last read our slice of it must have finished reading
+      // copies that last read this warp's rows of it must have finished reading
       if (kb >= NSG) mbar_wait(&gempty[sg], pg);
       if (CL > 1) {
-        if (ptid == 0) bulk_wait_read<NSG - 1>();
-        named_bar(1, NPROD);
+        if (lane == 0) bulk_wait_read<NSG - 1>();
+        __syncwarp();
       }
       double* gdst = Gs + sg * G_STAGE;
       const int64_t jbase = lo + rbase;
-      constexpr int PAIRS = (SLICE_ROWS / 2) * BK;       // pairs per CTA per k-block
+      double z[PPT][2];
 #pragma unroll
-      for (int t = 0; t < (PAIRS + NPROD - 1) / NPROD; ++t) {
-        const int p = ptid + NPROD * t;
-        if (PAIRS % NPROD == 0 || p < PAIRS) {
-          const int qp = (int)qrank * (SLICE_ROWS / 2) + p / BK, kk = p % BK;
-          double z0 = 0.0, z1 = 0.0;
-          if (kk < nrow && !(diag & 1)) gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z0, z1);
-          gdst[(2 * qp) * G_LD + kk] = z0;
-          gdst[(2 * qp + 1) * G_LD + kk] = z1;
+      for (int t = 0; t < PPT; ++t) {
+        const int p = lane + 32 * t;
+        const int qp = row0 / 2 + p / BK, kk = p % BK;
+        z[t][0] = z[t][1] = 0.0;
+        if ((PAIRS_W % 32 == 0 || p < PAIRS_W) && kk < nrow && !(diag & 1))
+          gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z[t][0], z[t][1]);
+      }
+#pragma unroll
+      for (int t = 0; t < PPT; ++t) {
+        const int p = lane + 32 * t;
+        if (PAIRS_W % 32 == 0 || p < PAIRS_W) {
+          const int qp = row0 / 2 + p / BK, kk = p % BK;
+          gdst[(2 * qp) * G_LD + kk] = z[t][0];
+          gdst[(2 * qp + 1) * G_LD + kk] = z[t][1];
         }
       }
       if (CL > 1) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic -> async proxy
-      named_bar(1, NPROD);                                // the whole slice is written
-      if (ptid == 0) {
-        mbar_arrive_expect_tx(&gfull[sg], SLICE_BYTES * (unsigned)(CL - 1));   // local slice: this arrive
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&gfull[sg], WBYTES * (unsigned)(CL - 1));   // + the matching warps' rows
         if (CL > 1) {
-          const double* src = gdst + (int64_t)qrank * SLICE_ROWS * G_LD;
+          const double* src = gdst + (int64_t)row0 * G_LD;
 #pragma unroll
           for (unsigned r = 1; r < (unsigned)CL; ++r) {
             const unsigned dr = (qrank + r) % (unsigned)CL;
-            bulk_s2s(map_rank(src, dr), src, SLICE_BYTES, map_rank(&gfull[sg], dr));
+            bulk_s2s(map_rank(src, dr), src, WBYTES, map_rank(&gfull[sg], dr));
           }
           bulk_commit();
         }
       }
     }
     if (CL > 1) {
-      if (ptid == 0) bulk_wait_read<0>();
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
       cluster_sync_all();                               // no CTA leaves while others may still signal it
     }
     return;
@@ -202,13 +235,13 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
 
   // -------------------------------------------------------------- consumers
   asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n");
-  const int cw = warp - NPROD / 32;                      // 0..7
+  const int cw = warp - NPW;                             // 0..7
   const int wm = cw >> 2, wn = cw & 3;                   // 2 x 4 warps
-  double acc[4][8][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int kb = 0; kb < nk; ++kb) {
     const int sx = kb % NSX, sg = kb % NSG;
@@ -218,15 +251,15 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
     const double* gs = Gs + sg * G_STAGE;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
-      double a[4], b[8];
+      double a[MI], b[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = gs[(wm * 32 + i * 8 + (lane >> 2)) * G_LD + ks * 4 + (lane & 3)];
+      for (int i = 0; i < MI; ++i) a[i] = gs[(wm * (BM / 2) + i * 8 + (lane >> 2)) * G_LD + ks * 4 + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = as[(ks * 4 + (lane & 3)) * A_LD + wn * 64 + j * 8 + (lane >> 2)];
+      for (int j = 0; j < NJ; ++j) b[j] = as[(ks * 4 + (lane & 3)) * A_LD + wn * (BN / 4) + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) dmma884(acc[i][j], a[i], b[j]);
+        for (int j = 0; j < NJ; ++j) dmma884(acc[i][j], a[i], b[j]);
     }
     __syncwarp();
     if (lane == 0) {
@@ -242,12 +275,12 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
 
   double* o = out + (int64_t)blockIdx.z * out_split_stride;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t gi = m0 + wm * 32 + i * 8 + (lane >> 2);
+  for (int i = 0; i < MI; ++i) {
+    const int64_t gi = m0 + wm * (BM / 2) + i * 8 + (lane >> 2);
     if (gi >= s) continue;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t gc = n0 + wn * 64 + j * 8 + 2 * (lane & 3);
+    for (int j = 0; j < NJ; ++j) {
+      const int64_t gc = n0 + wn * (BN / 4) + j * 8 + 2 * (lane & 3);
       if (gc + 1 < k) {
         double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
         if (accumulate) {
@@ -268,16 +301,17 @@ bool sketch_ws_supported(const SketchDenseArgs& a) {
   return (a.ld % 2 == 0) && (a.k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
 }
 
-template <int CL>
-static cudaError_t launch_ws_t(const SketchDenseArgs& a, dim3 grid, cudaStream_t st) {
+template <class C, int CL>
+static cudaError_t launch_ws_t(const SketchDenseArgs& a, cudaStream_t st) {
   using namespace ws;
-  cudaError_t e = cudaFuncSetAttribute(sketch_ws_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)SMEM_BYTES);
+  dim3 grid((unsigned)((a.k + C::BN - 1) / C::BN), (unsigned)((a.s + C::BM - 1) / C::BM), (unsigned)a.nsplit);
+  cudaError_t e = cudaFuncSetAttribute(sketch_ws_kernel<C, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)C::SMEM);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -289,33 +323,58 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, dim3 grid, cudaStream_t
   // LSRN_SKETCH_DIAG (timing experiments only, results are wrong): 1 = skip the RNG
   int diag = 0;
   if (const char* e = std::getenv("LSRN_SKETCH_DIAG")) diag = std::atoi(e);
-  return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
+  return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<C, CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
                             a.rows_per_split, a.out, a.out_split_stride, diag, a.accumulate);
 }
 
+// Tile shape (LSRN_SKETCH_TILE, tuning aid).  Measured on c2 (1e5 x 2000,
+// profiles/r01_sketch_tile.jsonl), ms: 64 x 256 (BK 16, 4 + 4 stages) CL 1/2 ->
+// 65.7 / 60.3; 32 x 512 (BK 16, 3 X stages) CL 1/2 -> 58.1 / 61.1; 32 x 512 with
+// BK 8 (5 X stages) CL 1/2 -> 70.2 / 74.9.  The 32 x 512 tile needs half the G
+// per flop of the 64 x 256 one (each normal feeds 512 columns) without the
+// cluster exchange, so it is the default: tile 1, CL 1.
+using Tile0 = ws::Cfg<64, 256, 16, 4, 4>;
+using Tile1 = ws::Cfg<32, 512, 16, 3, 4>;
+
+int sketch_ws_tile() {   // read at every launch (tests switch it)
+  const char* e = std::getenv("LSRN_SKETCH_TILE");
+  return e ? std::atoi(e) : 1;
+}
+
+void sketch_ws_tile_dims(int64_t* bm, int64_t* bn, int64_t* bk) {
+  if (sketch_ws_tile() == 0) {
+    *bm = Tile0::BM; *bn = Tile0::BN; *bk = Tile0::BK;
+  } else {
+    *bm = Tile1::BM; *bn = Tile1::BN; *bk = Tile1::BK;
+  }
+}
+
 // Cluster size along N: the largest of {max_cl, ..., 2} dividing the N-tile count.
-// LSRN_SKETCH_MAXCL (tuning aid) caps it.  Default 2, measured on c2
-// (profiles/r01_sketch_tune.jsonl): CL = 1/2/4/8 -> 82.6/69.3/72.3/83.0 ms; larger
-// clusters cut the RNG further but leave SMs idle (whole clusters must fit in a
-// GPC: with CL = 8 only 76 % of the SM-cycles were active).
-int sketch_ws_cluster(int64_t k) {
-  const int64_t nt = (k + ws::BN - 1) / ws::BN;
-  int max_cl = 2;
+// LSRN_SKETCH_MAXCL (tuning aid) caps it; default 2 for the 64 x 256 tile
+// (CL = 1/2/4/8 -> 82.6/69.3/72.3/83.0 ms on c2 in the first measurement,
+// profiles/r01_sketch_tune.jsonl: whole clusters must fit in a GPC, with CL = 8
+// only 76 % of the SM-cycles were active) and 1 for the 32 x 512 tile.
+template <class C>
+static int cluster_for(int64_t k) {
+  const int64_t nt = (k + C::BN - 1) / C::BN;
+  int max_cl = C::BM == 64 ? 2 : 1;
   if (const char* e = std::getenv("LSRN_SKETCH_MAXCL")) max_cl = std::atoi(e);
-  for (int cl : {8, 4, 2})
+  for (int cl : {4, 2})
     if (cl <= max_cl && nt % cl == 0) return cl;
   return 1;
 }
 
-cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st) {
-  using namespace ws;
-  dim3 grid((unsigned)((a.k + BN - 1) / BN), (unsigned)((a.s + BM - 1) / BM), (unsigned)a.nsplit);
-  switch (sketch_ws_cluster(a.k)) {
-    case 8: return launch_ws_t<8>(a, grid, st);
-    case 4: return launch_ws_t<4>(a, grid, st);
-    case 2: return launch_ws_t<2>(a, grid, st);
-    default: return launch_ws_t<1>(a, grid, st);
+template <class C>
+static cudaError_t launch_ws_tile(const SketchDenseArgs& a, cudaStream_t st) {
+  switch (cluster_for<C>(a.k)) {
+    case 4: if constexpr (C::BM / 4 >= 2 * ws::NPW) return launch_ws_t<C, 4>(a, st); [[fallthrough]];
+    case 2: if constexpr (C::BM / 2 >= 2 * ws::NPW) return launch_ws_t<C, 2>(a, st); [[fallthrough]];
+    default: return launch_ws_t<C, 1>(a, st);
   }
+}
+
+cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st) {
+  return sketch_ws_tile() == 0 ? launch_ws_tile<Tile0>(a, st) : launch_ws_tile<Tile1>(a, st);
 }
 
 }  // namespace lsrn

@@ -229,13 +229,17 @@ def test_repeat_solves_bitwise(ctx):
     assert torch.equal(x1, x2)
 
 
-@pytest.mark.parametrize("maxcl,n", [(4, 1024), (8, 2048), (8, 1536), ("batch", 1000), ("batch", 2048)])
-def test_sketch_cluster_sizes(ctx, monkeypatch, maxcl, n):
-    """The G-sharing cluster paths CL = 4 and 8 (the default caps CL at 2; LSRN_SKETCH_MAXCL
-    is read at each launch) give the same sketch."""
-    if maxcl == "batch":
+@pytest.mark.parametrize("tile,maxcl,n", [("0", 1, 1000), ("0", 2, 1024), ("0", 4, 1024), ("0", 4, 2048),
+                                          ("0", 2, 1536), ("1", 1, 1000), ("1", 2, 1024), ("1", 2, 1536),
+                                          ("1", 1, 3000), ("batch", 0, 1000), ("batch", 0, 2048)])
+def test_sketch_tiles_and_clusters(ctx, monkeypatch, tile, maxcl, n):
+    """Every tile shape / G-sharing cluster size of the warp-specialized sketch (64 x 256 with
+    CL = 1, 2, 4; 32 x 512 with CL = 1, 2; LSRN_SKETCH_TILE / _MAXCL are read at each launch)
+    and the batched-RNG variant give the same sketch, ragged N tiles included."""
+    if tile == "batch":
         monkeypatch.setenv("LSRN_SKETCH_IMPL", "batch")
     else:
+        monkeypatch.setenv("LSRN_SKETCH_TILE", tile)
         monkeypatch.setenv("LSRN_SKETCH_MAXCL", str(maxcl))
     m = n + 300
     g = torch.Generator().manual_seed(n)
