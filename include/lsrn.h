@@ -177,6 +177,26 @@ lsrn_status lsrn_solve_cs(lsrn_ctx* ctx, const lsrn_matrix* A, const double* b,
                           const lsrn_opts* opts, void* ws, size_t ws_bytes, double* x,
                           lsrn_report* report);
 
+enum { LSRN_SOLVER_LSQR = 0, LSRN_SOLVER_CS = 1 };
+
+/* Oversampling choice (NEXT-4), §6.3: "initialize LSRN by measuring
+ * randn/sec and flops/sec ... and then determine the best value of gamma by
+ * minimizing the total running time".  Host-only (no device work).  The rates
+ * come from a probe solve's report (any gamma): for s = ceil(gamma k),
+ * k = min(m, n),
+ *   T(gamma) = t_sketch s / s0                                (randn + mult, linear in s)
+ *            + t_svd (2 s k^2 + 11 k^3) / (2 s0 k^2 + 11 k^3)  (SVD cost)
+ *            + t_iter / it0 * it(s)                           (it = Thm 4.5 LSQR count or
+ *                                                              Alg. 3 K + 1 passes, P:643, P:694,
+ *                                                              at the probe's rank r, alpha = 1/sqrt(s))
+ * minimised over gamma on a 0.01 grid of [gamma_lo, gamma_hi] (s > r required).
+ * probe: a report filled by lsrn_solve_lsqr / _cs for the same (m, n) and
+ * solver (iters > 0); solver: LSRN_SOLVER_LSQR or _CS.  Returns LSRN_EINVAL on
+ * an unusable probe or range; *gamma_out and (optional) *t_out = the model's
+ * time at the choice. */
+lsrn_status lsrn_choose_gamma(const lsrn_report* probe, int64_t m, int64_t n, double tol, int solver,
+                              double gamma_lo, double gamma_hi, double* gamma_out, double* t_out);
+
 /* Testing aid (K1 parity): out[t] = G[rows[t], cols[t]] for t < count
  * (rows/cols/out device arrays), the in-kernel Philox + Box-Muller. */
 lsrn_status lsrn_debug_gaussian(lsrn_ctx* ctx, uint64_t seed, const int64_t* rows,

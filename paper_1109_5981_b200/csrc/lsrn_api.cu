@@ -159,6 +159,29 @@ Dims make_dims(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, b
   return d;
 }
 
+// Iteration counts from the Thm 4.4 bounds: LSQR, Thm 4.5 at alpha = 0
+// (§8(c) C5: (log eps - log 2) / log sqrt(r/s)); CS, Alg. 3's K + 1 passes with
+// rho = (sU - sL) / (sU + sL) (§8(c) C2).
+struct Counts {
+  double sigL, sigU;
+  int lsqr, cs_passes;
+};
+Counts iteration_counts(double s, double r, double alpha, double tol) {
+  Counts c{};
+  c.sigU = 1.0 / ((1.0 - alpha) * std::sqrt(s) - std::sqrt(r));
+  c.sigL = 1.0 / ((1.0 + alpha) * std::sqrt(s) + std::sqrt(r));
+  const double rate0 = std::sqrt(r / s);
+  c.lsqr = (int)std::ceil((std::log(tol) - std::log(2.0)) / std::log(rate0));
+  if (c.lsqr < 0) c.lsqr = 0;
+  c.cs_passes = 1;
+  const double rho = (c.sigU - c.sigL) / (c.sigU + c.sigL);
+  if (rho > 0.0) {
+    const int K = (int)std::ceil((std::log(tol) - std::log(2.0)) / std::log(rho));
+    c.cs_passes = (K > 0 ? K : 0) + 1;
+  }
+  return c;
+}
+
 int choose_nsplit(int64_t s, int64_t k, int64_t rows, int nsm) {
   int64_t mt, nt, bk;
   sketch_tile_counts(s, k, &mt, &nt, &bk);
@@ -884,6 +907,41 @@ lsrn_status lsrn_last_stats(lsrn_ctx* c, double* out, int cap) {
   return LSRN_OK;
 }
 
+lsrn_status lsrn_choose_gamma(const lsrn_report* pr, int64_t m, int64_t n, double tol, int solver,
+                              double gamma_lo, double gamma_hi, double* gamma_out, double* t_out) {
+  if (!pr || !gamma_out) return set_error(LSRN_EINVAL, "NULL argument");
+  if (m <= 0 || n <= 0) return set_error(LSRN_EDIM, "m and n must be positive");
+  if (!(tol > 0.0 && tol < 1.0)) return set_error(LSRN_EINVAL, "tol must lie in (0, 1)");
+  if (solver != LSRN_SOLVER_LSQR && solver != LSRN_SOLVER_CS) return set_error(LSRN_EINVAL, "unknown solver");
+  if (!(gamma_lo > 1.0 && gamma_hi >= gamma_lo)) return set_error(LSRN_EINVAL, "need 1 < gamma_lo <= gamma_hi");
+  if (pr->s <= 0 || pr->r <= 0 || pr->r >= pr->s || pr->iters <= 0 || !(pr->t_sketch >= 0.0) ||
+      !(pr->t_svd >= 0.0) || !(pr->t_iter > 0.0))
+    return set_error(LSRN_EINVAL, "probe report unusable (needs s > r > 0, iters > 0, stage times)");
+  const double k = (double)std::min(m, n);
+  const double s0 = (double)pr->s, r = (double)pr->r;
+  const double svd0 = 2.0 * s0 * k * k + 11.0 * k * k * k;
+  const double per_it = pr->t_iter / (double)pr->iters;
+  double best_t = INFINITY, best_g = 0.0;
+  for (int step = 0;; ++step) {
+    const double g = gamma_lo + 0.01 * step;
+    if (g > gamma_hi + 1e-12) break;
+    const double s = std::ceil(g * k);
+    const double alpha = 1.0 / std::sqrt(s);
+    if (!(alpha < 1.0 - std::sqrt(r / s))) continue;          // Thm 4.4 needs s large enough
+    const Counts cn = iteration_counts(s, r, alpha, tol);
+    const int it = solver == LSRN_SOLVER_LSQR ? cn.lsqr : cn.cs_passes;
+    const double t = pr->t_sketch * s / s0 + pr->t_svd * (2.0 * s * k * k + 11.0 * k * k * k) / svd0 + per_it * it;
+    if (t < best_t) {
+      best_t = t;
+      best_g = g;
+    }
+  }
+  if (!(best_g > 1.0)) return set_error(LSRN_EINVAL, "no gamma in the range gives s with alpha < 1 - sqrt(r/s)");
+  *gamma_out = best_g;
+  if (t_out) *t_out = best_t;
+  return LSRN_OK;
+}
+
 }  // extern "C"
 
 // -------------------------------------------------------------- shared driver
@@ -1086,19 +1144,10 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     double alpha = o->alpha < 0.0 ? 1.0 / std::sqrt(s) : o->alpha;
     LSRN_REQUIRE(alpha > 0.0 && alpha < 1.0 - std::sqrt((double)r / s), LSRN_EINVAL,
                  "alpha must lie in (0, 1 - sqrt(r/s)) (Thm 4.4)");
-    const double sigU = 1.0 / ((1.0 - alpha) * std::sqrt(s) - std::sqrt((double)r));
-    const double sigL = 1.0 / ((1.0 + alpha) * std::sqrt(s) + std::sqrt((double)r));
-    const double rate0 = std::sqrt((double)r / s);
-    int kl = (int)std::ceil((std::log(o->tol) - std::log(2.0)) / std::log(rate0));
-    if (kl < 0) kl = 0;
-    int passes = 1;
-    {
-      const double rho = (sigU - sigL) / (sigU + sigL);
-      if (rho > 0.0) {
-        int K = (int)std::ceil((std::log(o->tol) - std::log(2.0)) / std::log(rho));
-        passes = (K > 0 ? K : 0) + 1;
-      }
-    }
+    const Counts cnts = iteration_counts(s, (double)r, alpha, o->tol);
+    const double sigU = cnts.sigU, sigL = cnts.sigL;
+    const int kl = cnts.lsqr;
+    const int passes = cnts.cs_passes;
     int iters_graph = 0;
     if (solver == SOLVER_LSQR)
       iters_graph = (o->mode == LSRN_MODE_PREDICTABLE) ? kl : (o->max_iter > 0 ? o->max_iter : 2 * kl);

@@ -385,6 +385,7 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
 namespace {
 constexpr int64_t kMaxSlice = 4096;        // doubles per CTA slice (32 KB per staged row)
 constexpr size_t kStageBudget = 192 * 1024;
+constexpr size_t kWideBudget = 224 * 1024;   // + ~2.5 KB static shared memory <= 227 KB
 }  // namespace
 
 // Tuning aids (env): LSRN_ROWPASS_OCC=1 (one CTA per SM, the whole stage budget),
@@ -410,7 +411,11 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   if (vpt > 16) return false;                                     // no kernel instance: fallback
   int occ = wide ? 1 : 2;
   if (const char* e = std::getenv("LSRN_ROWPASS_OCC")) occ = std::atoi(e) == 1 ? 1 : 2;
-  const size_t budget = kStageBudget / occ;
+  // wide rows (one CTA per SM): the refill of a stage waits until its phase 2 is
+  // done, so two stages are always busy; use (almost) all of shared memory so that
+  // >= 3 stages stay in flight (LSRN_ROWPASS_BUDGET_KB: tuning aid)
+  size_t budget = wide && occ == 1 ? kWideBudget : kStageBudget / occ;
+  if (const char* e = std::getenv("LSRN_ROWPASS_BUDGET_KB")) budget = (size_t)std::atoi(e) * 1024;
   int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(budget / 3) / (cq * 8)));
   int t2 = 1;
   while (t2 * 2 <= tr) t2 *= 2;

@@ -25,7 +25,8 @@ STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE
 # every symbol include/lsrn.h declares
 EXPORTS = ["lsrn_last_error", "lsrn_version", "lsrn_nccl_unique_id", "lsrn_ctx_create", "lsrn_ctx_destroy",
            "lsrn_ctx_set_profiling", "lsrn_workspace_size", "lsrn_sketch",
-           "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_debug_box_muller", "lsrn_last_stats"]
+           "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_debug_box_muller", "lsrn_last_stats",
+           "lsrn_choose_gamma"]
 
 
 class LsrnError(RuntimeError):
@@ -86,6 +87,8 @@ def lib():
             "lsrn_debug_gaussian": [vp, u64, vp, vp, i64, vp],
             "lsrn_debug_box_muller": [vp, vp, i64, i32, vp],
             "lsrn_last_stats": [vp, ctypes.POINTER(ctypes.c_double), i32],
+            "lsrn_choose_gamma": [ctypes.POINTER(Report), i64, i64, dbl, i32, dbl, dbl,
+                                  ctypes.POINTER(dbl), ctypes.POINTER(dbl)],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -93,6 +96,16 @@ def lib():
             f.restype = ctypes.c_int
         _lib = L
     return _lib
+
+
+def choose_gamma(probe, m, n, tol=1e-14, solver="lsqr", lo=1.2, hi=3.0):
+    """lsrn_choose_gamma (NEXT-4, §6.3): the gamma minimising the stage-time
+    model calibrated by a probe solve's report (a dict from Context.solve).  Host-only."""
+    rep = Report(**{f: probe[f] for f, _ in Report._fields_})
+    g, t = ctypes.c_double(), ctypes.c_double()
+    _check(lib().lsrn_choose_gamma(ctypes.byref(rep), m, n, tol, 0 if solver == "lsqr" else 1, lo, hi,
+                                   ctypes.byref(g), ctypes.byref(t)))
+    return {"gamma": round(g.value, 2), "t_model": t.value}
 
 
 def _check(code):
