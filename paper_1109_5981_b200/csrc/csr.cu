@@ -142,14 +142,65 @@ __global__ void csr_colptr_kernel(const int64_t* __restrict__ total, const int* 
   if (threadIdx.x == 0) colptr[k] = carry;
 }
 
-// In-order fill of the CSC copy of the light columns (rowidx = local row, cval)
-// and of the heavy block D (rows x ld_d, zero-filled beforehand).  One CTA per chunk, one warp walking
-// the chunk's rows in order (distinct columns within a row -> no conflicts).
+// Light entries per row chunk (for the light CSR's chunk offsets).
+__global__ void csr_chunk_light_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                                       int64_t rows, int64_t CH, const int* __restrict__ colmap,
+                                       int64_t* __restrict__ lchunk_cnt) {
+  __shared__ int64_t sh[THR / 32];
+  const int64_t chunk = blockIdx.x;
+  const int64_t base = rowptr[0];
+  const int64_t r0 = chunk * CH, r1 = min(rows, r0 + CH);
+  const int64_t e0 = rowptr[r0] - base, e1 = rowptr[r1] - base;
+  int64_t n = 0;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) n += colmap[colind[e]] < 0 ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < THR / 32; ++w) t += sh[w];
+    lchunk_cnt[chunk] = t;
+  }
+}
+
+// out[i] = sum_{i' < i} in[i'] for i <= n (out[n] = total).  Single CTA, tiles of THR.
+__global__ void excl_scan_kernel(const int64_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  __shared__ int64_t sh[THR];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < n; t0 += THR) {
+    const int64_t i = t0 + threadIdx.x;
+    const int64_t v = i < n ? in[i] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int off = 1; off < THR; off <<= 1) {      // Hillis-Steele inclusive scan
+      const int64_t add = (threadIdx.x >= off) ? sh[threadIdx.x - off] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (i < n) out[i] = carry + sh[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == THR - 1) carry += sh[THR - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+// In-order fill of the CSC copy of the light columns (rowidx = local row, cval),
+// of the heavy block D (rows x ld_d, zero-filled beforehand) and of the light CSR
+// (lrowptr / lcol / lval: each row's light entries in their CSR order).  One CTA
+// per chunk, one warp walking the chunk's rows in order (distinct columns within
+// a row -> no conflicts; light positions within a row by ballot).
 __global__ void csr_fill_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
                                 const double* __restrict__ val, int64_t rows, int64_t k, int64_t CH,
                                 const int64_t* __restrict__ offs, const int64_t* __restrict__ colptr,
                                 const int* __restrict__ colmap, int32_t* __restrict__ rowidx,
-                                double* __restrict__ cval, double* __restrict__ D, int64_t ld_d) {
+                                double* __restrict__ cval, double* __restrict__ D, int64_t ld_d,
+                                const int64_t* __restrict__ lchunk_off, int64_t* __restrict__ lrowptr,
+                                int32_t* __restrict__ lcol, double* __restrict__ lval) {
   extern __shared__ int64_t cur[];
   const int64_t chunk = blockIdx.x;
   for (int64_t c = threadIdx.x; c < k; c += blockDim.x) cur[c] = colptr[c] + offs[chunk * k + c];
@@ -158,22 +209,34 @@ __global__ void csr_fill_kernel(const int64_t* __restrict__ rowptr, const int32_
   const int lane = threadIdx.x;
   const int64_t base = rowptr[0];
   const int64_t r1 = min(rows, (chunk + 1) * CH);
+  int64_t lrun = lchunk_off[chunk];
   for (int64_t r = chunk * CH; r < r1; ++r) {
     const int64_t e0 = rowptr[r] - base, e1 = rowptr[r + 1] - base;
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const int c = colind[e];
-      const double a = val[e];
-      const int h = colmap[c];
-      if (h >= 0) {
-        D[r * ld_d + h] = a;
-      } else {
-        const int64_t pos = cur[c]++;
-        rowidx[pos] = (int32_t)r;
-        cval[pos] = a;
+    if (lane == 0) lrowptr[r] = lrun;
+    for (int64_t eb = e0; eb < e1; eb += 32) {
+      const int64_t e = eb + lane;
+      const bool ok = e < e1;
+      const int c = ok ? colind[e] : 0;
+      const double a = ok ? val[e] : 0.0;
+      const int h = ok ? colmap[c] : 0;
+      const unsigned lm = __ballot_sync(0xffffffffu, ok && h < 0);
+      if (ok) {
+        if (h >= 0) {
+          D[r * ld_d + h] = a;
+        } else {
+          const int64_t pos = cur[c]++;
+          rowidx[pos] = (int32_t)r;
+          cval[pos] = a;
+          const int64_t lp = lrun + __popc(lm & ((1u << lane) - 1u));
+          lcol[lp] = c;
+          lval[lp] = a;
+        }
       }
+      lrun += __popc(lm);
     }
     __syncwarp();
   }
+  if (lane == 0 && r1 == rows) lrowptr[rows] = lrun;
 }
 
 // ------------------------------------------------------------ K4 sketch kernels
@@ -348,6 +411,93 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
       for (int w = 0; w < THR / 32; ++w) v += wd[w][h];
       wpart[(int64_t)blockIdx.x * ND + h] = sx * v;
     }
+  }
+}
+
+// Long pass in the heavy-dense + light-CSR form (k > csr_rowdot_all_max_k()):
+//   u_j <- c1 u_j + c2 (D_j . t_heavy + sum_light a t_c),  w_heavy += D_j u_j,
+// npart[block] = partial ||u||^2, wpart[block][h] = sx sum_j D_jh u_j (fixed-order
+// block reduction).  Lane l owns heavy columns l and l + 32 (t and the w
+// accumulators in registers, no column map, no shared-memory atomics), the D row
+// is one coalesced load, the ~20 light entries of a row one gather; two rows per
+// step keep independent loads in flight.  The light w comes from the CSC gather.
+template <int HPL>
+__global__ void __launch_bounds__(THR)
+csr_rowdot_hl_kernel(const double* __restrict__ D, int ND, int nd, const int* __restrict__ heavy_cols,
+                     const int64_t* __restrict__ lrowptr, const int32_t* __restrict__ lcol,
+                     const double* __restrict__ lval, int64_t rows, const double* __restrict__ t,
+                     const double* __restrict__ coef, double sx, double* __restrict__ u, double* __restrict__ acc,
+                     double* __restrict__ npart, double* __restrict__ wpart, const int* __restrict__ done) {
+  __shared__ double sh[THR / 32];
+  __shared__ double wsh[THR / 32][HPL * 32];
+  if (done != nullptr && *done != 0) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * THR + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * THR) >> 5;
+  const double c1 = coef[0], c2 = coef[1] * sx;
+  const double ca = (acc != nullptr) ? coef[2] : 0.0;
+  double th[HPL], wh[HPL];
+#pragma unroll
+  for (int q = 0; q < HPL; ++q) {
+    const int h = lane + 32 * q;
+    th[q] = h < nd ? __ldg(t + heavy_cols[h]) : 0.0;
+    wh[q] = 0.0;
+  }
+  double nrm = 0.0;
+  const int64_t per = (rows + nwarps - 1) / nwarps;
+  const int64_t r0 = warp * per, r1 = min(rows, r0 + per);
+  const int64_t lbase = lrowptr[0];
+  for (int64_t r = r0; r < r1; r += 2) {
+    const bool has2 = r + 1 < r1;
+    double da[HPL], db[HPL];
+#pragma unroll
+    for (int q = 0; q < HPL; ++q) {
+      const int h = lane + 32 * q;
+      da[q] = h < nd ? ldg_stream1(D + r * ND + h) : 0.0;
+      db[q] = (h < nd && has2) ? ldg_stream1(D + (r + 1) * ND + h) : 0.0;
+    }
+    const int64_t ea0 = lrowptr[r] - lbase, ea1 = lrowptr[r + 1] - lbase;
+    const int64_t eb1 = has2 ? lrowptr[r + 2] - lbase : ea1;
+    double sa = 0.0, sb = 0.0;
+    for (int64_t e = ea0 + lane; e < ea1; e += 32) sa = fma(ldg_stream1(lval + e), __ldg(t + lcol[e]), sa);
+    for (int64_t e = ea1 + lane; e < eb1; e += 32) sb = fma(ldg_stream1(lval + e), __ldg(t + lcol[e]), sb);
+#pragma unroll
+    for (int q = 0; q < HPL; ++q) {
+      sa = fma(da[q], th[q], sa);
+      sb = fma(db[q], th[q], sb);
+    }
+    const double uoa = lane == 0 ? u[r] : 0.0;
+    const double uob = (lane == 0 && has2) ? u[r + 1] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    const double una = fma(c1, __shfl_sync(0xffffffffu, uoa, 0), c2 * sa);
+    const double unb = has2 ? fma(c1, __shfl_sync(0xffffffffu, uob, 0), c2 * sb) : 0.0;
+    if (lane == 0) {
+      u[r] = una;
+      if (acc != nullptr) acc[r] = fma(ca, una, acc[r]);
+      nrm = fma(una, una, nrm);
+      if (has2) {
+        u[r + 1] = unb;
+        if (acc != nullptr) acc[r + 1] = fma(ca, unb, acc[r + 1]);
+        nrm = fma(unb, unb, nrm);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < HPL; ++q) wh[q] = fma(db[q], unb, fma(da[q], una, wh[q]));
+  }
+#pragma unroll
+  for (int q = 0; q < HPL; ++q) wsh[wib][lane + 32 * q] = wh[q];
+  if (lane != 0) nrm = 0.0;
+  const double b = block_sum(nrm, sh);     // contains __syncthreads: wsh complete
+  if (threadIdx.x == 0) npart[blockIdx.x] = b;
+  for (int h = threadIdx.x; h < nd; h += THR) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < THR / 32; ++w) v += wsh[w][h];
+    wpart[(int64_t)blockIdx.x * ND + h] = sx * v;
   }
 }
 
@@ -533,6 +683,14 @@ cudaError_t launch_csr_build(const CsrBuildArgs& a, cudaStream_t st) {
 cudaError_t launch_csr_fill(const CsrBuildArgs& a, cudaStream_t st) {
   const int64_t nch = csr_nchunks(a.rows);
   csr_colptr_kernel<<<1, THR, 0, st>>>(a.total, a.colmap, a.k, a.colptr);
+  if (nch > 0)
+    csr_chunk_light_kernel<<<(unsigned)nch, THR, 0, st>>>(a.rowptr, a.colind, a.rows, csr_chunk_rows(), a.colmap,
+                                                           a.lchunk_cnt);
+  excl_scan_kernel<<<1, THR, 0, st>>>(a.lchunk_cnt, nch, a.lchunk_off);
+  if (a.rows == 0) {
+    cudaError_t e = cudaMemsetAsync(a.lrowptr, 0, sizeof(int64_t), st);
+    if (e != cudaSuccess) return e;
+  }
   if (a.D != nullptr && a.rows > 0) {
     cudaError_t e = cudaMemsetAsync(a.D, 0, sizeof(double) * (size_t)a.rows * a.ld_d, st);
     if (e != cudaSuccess) return e;
@@ -542,7 +700,8 @@ cudaError_t launch_csr_fill(const CsrBuildArgs& a, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(csr_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh);
     if (e != cudaSuccess) return e;
     csr_fill_kernel<<<(unsigned)nch, 256, sh, st>>>(a.rowptr, a.colind, a.val, a.rows, a.k, csr_chunk_rows(), a.offs,
-                                                    a.colptr, a.colmap, a.rowidx, a.cval, a.D, a.ld_d);
+                                                    a.colptr, a.colmap, a.rowidx, a.cval, a.D, a.ld_d, a.lchunk_off,
+                                                    a.lrowptr, a.lcol, a.lval);
   }
   return cudaGetLastError();
 }
@@ -591,6 +750,18 @@ cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st) {
     default: LSRN_ROWDOT(64); break;
   }
 #undef LSRN_ROWDOT
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_rowdot_hl(const CsrRowdotArgs& a, cudaStream_t st) {
+  const unsigned nb = (unsigned)a.nblocks;
+  const int ND = a.ND > 0 ? a.ND : 32;
+  if (ND > 32)
+    csr_rowdot_hl_kernel<2><<<nb, THR, 0, st>>>(a.D, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows, a.t,
+                                                a.coef, a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
+  else
+    csr_rowdot_hl_kernel<1><<<nb, THR, 0, st>>>(a.D, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows, a.t,
+                                                a.coef, a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
   return cudaGetLastError();
 }
 

@@ -57,6 +57,7 @@ struct RowPassPlan {
   int keep = 0;                     // bulk: row tile kept in registers between the two phases
   int occ = 1;                      // bulk: CTAs per SM
   int async_x = 0;                  // bulk, cl > 1: pipelined st.async partial-dot exchange
+  int nt = 256;                     // bulk: threads per CTA (wide rows: 256, or 512 as a tuning aid)
 };
 // allow_bulk = false forces the register-load kernel (tests compare both)
 RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, bool allow_bulk = true);
@@ -117,6 +118,12 @@ struct CsrBuildArgs {
   double* D;               // [rows][ld_d] heavy block (nullable when no heavy column)
   int64_t ld_d;
   int* bad;                // validation flags (zeroed by launch_csr_build): 1 column range, 2 order, 4 rowptr
+  // light-column CSR (row order, heavy entries removed) for the iteration pass
+  int64_t* lrowptr;        // [rows + 1]
+  int32_t* lcol;           // [nnz_light]
+  double* lval;            // [nnz_light]
+  int64_t* lchunk_cnt;     // [nchunks]: light entries per row chunk
+  int64_t* lchunk_off;     // [nchunks + 1]: exclusive scan
 };
 int64_t csr_chunk_rows();
 int64_t csr_nchunks(int64_t rows);
@@ -159,8 +166,16 @@ struct CsrRowdotArgs {
   double* wpart;           // [nblocks][ND]
   const int* done;
   int ND, nblocks;
+  // heavy-dense + light-CSR form (csr_rowdot_hl_kernel)
+  const double* D;         // [rows][ND] heavy block
+  const int* heavy_cols;   // [nd]
+  int nd;
+  const int64_t* lrowptr;
+  const int32_t* lcol;
+  const double* lval;
 };
 cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st);
+cudaError_t launch_csr_rowdot_hl(const CsrRowdotArgs& a, cudaStream_t st);
 // single-pass variant for k <= csr_rowdot_all_max_k(): wpart[nblocks][k], then colreduce
 int64_t csr_rowdot_all_max_k();
 int csr_rowdot_all_blocks(int nsm, int64_t k);

@@ -256,6 +256,9 @@ struct CsrWs {
   int *colmap, *heavy_cols;
   int32_t* rowidx;
   double *cval, *D, *part, *npart, *wpart;
+  int64_t *lrowptr, *lchunk_cnt, *lchunk_off;   // light-column CSR (iteration pass, k > 2048)
+  int32_t* lcol;
+  double* lval;
   int nsplit;
   int64_t rows_per_split;
   // filled by csr_prepare
@@ -278,6 +281,11 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
   w.rowidx = ar.take<int32_t>((size_t)nnz);
   w.cval = ar.take<double>((size_t)nnz);
   w.D = ar.take<double>((size_t)std::max<int64_t>(d.cnt, 1) * kMaxHeavy);
+  w.lrowptr = ar.take<int64_t>((size_t)d.cnt + 1);
+  w.lcol = ar.take<int32_t>((size_t)nnz);
+  w.lval = ar.take<double>((size_t)nnz);
+  w.lchunk_cnt = ar.take<int64_t>((size_t)std::max<int64_t>(nch, 1));
+  w.lchunk_off = ar.take<int64_t>((size_t)nch + 1);
   // heavy-part split-K: enough (row block, split) CTAs for two waves
   const int64_t row_blocks = (d.s + 255) / 256;
   int nsplit = (int)std::max<int64_t>(1, (2 * (int64_t)c->nsm + row_blocks - 1) / row_blocks);
@@ -343,6 +351,11 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
     LSRN_CUDA(cudaMemcpyAsync(w.heavy_cols, cand.data(), sizeof(int) * w.nd, cudaMemcpyHostToDevice, st));
   b.D = w.nd > 0 ? w.D : nullptr;
   b.ld_d = w.ND;
+  b.lrowptr = w.lrowptr;
+  b.lcol = w.lcol;
+  b.lval = w.lval;
+  b.lchunk_cnt = w.lchunk_cnt;
+  b.lchunk_off = w.lchunk_off;
   LSRN_CUDA(launch_csr_fill(b, st));
   c->launches += 2;
   LSRN_CUDA(cudaStreamSynchronize(st));   // host vectors above are pageable: keep them alive until copied
@@ -694,7 +707,16 @@ struct Pass {
       return;
     }
     a.nblocks = csr_rowdot_blocks(c->nsm);
-    LSRN_CUDA(launch_csr_rowdot(a, st));
+    a.D = cw->D;
+    a.heavy_cols = cw->heavy_cols;
+    a.nd = cw->nd;
+    a.lrowptr = cw->lrowptr;
+    a.lcol = cw->lcol;
+    a.lval = cw->lval;
+    if (std::getenv("LSRN_CSR_ROWDOT_V1"))   // tuning aid: the warp-per-row pass over the full CSR
+      LSRN_CUDA(launch_csr_rowdot(a, st));
+    else
+      LSRN_CUDA(launch_csr_rowdot_hl(a, st));
     CsrGatherArgs g{};
     g.colptr = cw->colptr;
     g.rowidx = cw->rowidx;
@@ -1358,8 +1380,13 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     // algorithmic bytes of one long pass: dense rows (8k + 16 per row);
     // CSR: the CSR stream (12 B per nonzero + 8 B rowptr + 16 B u per row) + the light CSC (12 B per entry)
     // (k <= 2048: single pass over the CSR, no CSC read in the iterations)
+    // k > 2048: the heavy block D (8 B per heavy entry, nd per row) + the light CSR (12 B per entry,
+    // 8 B row pointer) + u (16 B per row) + the light CSC (12 B per entry)
+    const bool hl = d.k > csr_rowdot_all_max_k() && !std::getenv("LSRN_CSR_ROWDOT_V1");
     const double csc_bytes = d.k <= csr_rowdot_all_max_k() ? 0.0 : 12.0 * (double)PL.cw.nnz_light;
-    c->stats[5] = PL.csr ? (12.0 * (double)A_in->nnz + 24.0 * (double)d.cnt + csc_bytes)
+    const double nnz_b = hl ? 8.0 * (double)PL.cw.nd * (double)d.cnt + 12.0 * (double)PL.cw.nnz_light
+                            : 12.0 * (double)A_in->nnz;
+    c->stats[5] = PL.csr ? (nnz_b + 24.0 * (double)d.cnt + csc_bytes)
                          : (double)d.cnt * ((double)d.k * 8.0 + 16.0);
     c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
     c->stats[7] = (double)graph_launches;

@@ -229,13 +229,14 @@ LSRN_DEV void cluster_sync_all2() {
 }
 }  // namespace
 
-template <int P, int TR, int OCC>
-__global__ void __launch_bounds__(THREADS, OCC)
+template <int P, int TR, int OCC, int NT>
+__global__ void __launch_bounds__(NT, OCC)
 rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq, int nst) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages];
   __shared__ uint64_t xbar[4];
-  __shared__ double red[2][NWARP][TR];
+  constexpr int NWARP_ = NT / 32;
+  __shared__ double red[2][NWARP_][TR];
   __shared__ double xs[4][16][TR];
   __shared__ double zs[4][TR];                       // old z of the tile, read before the exchange
   if (a.done != nullptr && *a.done != 0) return;     // uniform over the grid
@@ -280,7 +281,7 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
   double2 tv[P], wv[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    const int64_t cl = 2 * (tid + THREADS * p);
+    const int64_t cl = 2 * (tid + NT * p);
     tv[p].x = (cl < ncol) ? a.t[c0 + cl] : 0.0;
     tv[p].y = (cl + 1 < ncol) ? a.t[c0 + cl + 1] : 0.0;
     wv[p] = make_double2(0.0, 0.0);
@@ -302,7 +303,7 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
       double s = 0.0;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const int64_t cl = 2 * (tid + THREADS * p);
+        const int64_t cl = 2 * (tid + NT * p);
         if (rok && cl < ncol) {
           const double2 y = *reinterpret_cast<const double2*>(row + cl);
           s = fma(y.x, tv[p].x, fma(y.y, tv[p].y, s));
@@ -324,7 +325,7 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
       zs[xb][tid] = zpre;
       double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < NWARP; ++w) s += red[rb2][w][tid];
+      for (int w = 0; w < NWARP_; ++w) s += red[rb2][w][tid];
       for (int rr = 0; rr < CL; ++rr)
         st_async_f64(cl_map(&xs[xb][q][tid], (unsigned)rr), s, cl_map(&xbar[xb], (unsigned)rr));
     }
@@ -350,7 +351,7 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
       const double* rowp = stage + ((int64_t)st * TR + tr) * stage_ld;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const int64_t cl = 2 * (tid + THREADS * p);
+        const int64_t cl = 2 * (tid + NT * p);
         if (cl < ncol) {
           const double2 y = *reinterpret_cast<const double2*>(rowp + cl);
           wv[p].x = fma(y.x, zn, wv[p].x);
@@ -373,7 +374,7 @@ rowpass_cluster_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t 
   double* wp = a.wpart + g * C;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    const int64_t cl = 2 * (tid + THREADS * p);
+    const int64_t cl = 2 * (tid + NT * p);
     if (cl < ncol) wp[c0 + cl] = a.sx * wv[p].x;
     if (cl + 1 < ncol) wp[c0 + cl + 1] = a.sx * wv[p].y;
   }
@@ -409,12 +410,17 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   int vpt = 1;
   while (512 * vpt < cq) vpt = (vpt < 8) ? vpt * 2 : vpt + 4;   // 1, 2, 4, 8, 12, 16
   if (vpt > 16) return false;                                     // no kernel instance: fallback
-  int occ = wide ? 1 : 2;
+  // Wide rows: two CTAs (clusters) per SM with two 1-row stages each when two
+  // slices fit in half of shared memory.  Each CTA's per-tile chain (block
+  // reduction, exchange, stage release) is latency-bound, and the second CTA
+  // hides it: c5 4.05 -> 4.43 TB/s (profiles/r01_rowpass_tune_c5c.jsonl) against
+  // one CTA per SM with 4-5 stages.  Otherwise one CTA with (almost) all of shared
+  // memory so that >= 3 stages stay in flight.  Tuning aids: LSRN_ROWPASS_OCC,
+  // LSRN_ROWPASS_BUDGET_KB.
+  int occ = 2;
+  if (wide && 2 * (size_t)cq * 8 > kWideBudget / 2) occ = 1;
   if (const char* e = std::getenv("LSRN_ROWPASS_OCC")) occ = std::atoi(e) == 1 ? 1 : 2;
-  // wide rows (one CTA per SM): the refill of a stage waits until its phase 2 is
-  // done, so two stages are always busy; use (almost) all of shared memory so that
-  // >= 3 stages stay in flight (LSRN_ROWPASS_BUDGET_KB: tuning aid)
-  size_t budget = wide && occ == 1 ? kWideBudget : kStageBudget / occ;
+  size_t budget = wide ? (occ == 1 ? kWideBudget : kWideBudget / 2) : kStageBudget / occ;
   if (const char* e = std::getenv("LSRN_ROWPASS_BUDGET_KB")) budget = (size_t)std::atoi(e) * 1024;
   int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(budget / 3) / (cq * 8)));
   int t2 = 1;
@@ -422,11 +428,14 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   tr = t2;
   const size_t stage_bytes = (size_t)tr * cq * 8;
   int nst = (int)std::min<size_t>(kMaxStages, budget / stage_bytes);
-  if (nst < 3) return false;    // one stage being reduced, one waiting for its refill, >= 1 in flight
+  // one stage being reduced, one waiting for its refill, >= 1 in flight; with two
+  // CTAs per SM on wide rows (tuning aid) two stages each still keep two in flight per SM
+  if (nst < 3 && !(wide && occ == 2 && nst == 2)) return false;
   bool keep = vpt * tr <= (occ == 2 ? 4 : 16);
   if (const char* e = std::getenv("LSRN_ROWPASS_KEEP")) keep = std::atoi(e) != 0 && vpt * tr <= 16;
   p->keep = keep ? 1 : 0;
   p->occ = occ;
+  p->nt = 256;
   // wide rows: pipelined asynchronous partial-dot exchange (LSRN_ROWPASS_ASYNCX=0: cluster barrier per tile)
   p->async_x = 1;
   if (const char* e = std::getenv("LSRN_ROWPASS_ASYNCX")) p->async_x = std::atoi(e) != 0;
@@ -443,6 +452,24 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   p->bulk = 1;
   p->cq = cq;
   p->nst = nst;
+  // Wide rows, tuning aid LSRN_ROWPASS_NT=512: 16 warps per CTA.  The c5 pass is
+  // latency-bound (ncu: 12.5 % warps active; stalls on fixed-latency dependencies,
+  // shared loads and the per-tile barrier, profiles/r01_ncu_c5_cluster.txt), but
+  // neither 512 threads (3.76 TB/s) nor an mbarrier-only tile flow without the two
+  // per-tile __syncthreads (3.50 TB/s) beat this kernel (4.05 TB/s,
+  // profiles/r01_rowpass_tune_c5c.jsonl).
+  if (cl > 1 && p->async_x) {
+    int nt = 256;
+    if (const char* e = std::getenv("LSRN_ROWPASS_NT")) nt = std::atoi(e) == 512 ? 512 : 256;
+    if (nt == 512) {
+      int v = 4;
+      while (v < 8 && 1024 * v < cq) v += 2;                     // 4, 6, 8 pairs per thread
+      if (1024 * v >= cq && p->tr <= 2) {
+        p->nt = 512;
+        p->vpt = v;
+      }
+    }
+  }
   return true;
 }
 
@@ -471,10 +498,10 @@ static cudaError_t launch_bulk_k(const RowPassArgs& a, const RowPassPlan& p, cud
   return cudaLaunchKernelEx(&cfg, kern, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
 }
 
-template <int P, int TR, int OCC>
+template <int P, int TR, int OCC, int NT = THREADS>
 static cudaError_t launch_cluster_k(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
   const size_t smem = (size_t)p.nst * TR * p.cq * 8;
-  auto kern = rowpass_cluster_kernel<P, TR, OCC>;
+  auto kern = rowpass_cluster_kernel<P, TR, OCC, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (p.cl > 8) {
@@ -483,7 +510,7 @@ static cudaError_t launch_cluster_k(const RowPassArgs& a, const RowPassPlan& p, 
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.nclusters * p.cl));
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -528,7 +555,19 @@ static cudaError_t launch_bulk_p(const RowPassArgs& a, const RowPassPlan& p, cud
   }
 }
 
+template <int P>
+static cudaError_t launch_cluster512(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  return p.tr == 1 ? launch_cluster_k<P, 1, 1, 512>(a, p, st) : launch_cluster_k<P, 2, 1, 512>(a, p, st);
+}
+
 cudaError_t launch_rowpass_bulk(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  if (p.nt == 512) {
+    switch (p.vpt) {
+      case 4: return launch_cluster512<4>(a, p, st);
+      case 6: return launch_cluster512<6>(a, p, st);
+      default: return launch_cluster512<8>(a, p, st);
+    }
+  }
   switch (p.vpt) {
     case 1: return launch_bulk_p<1>(a, p, st);
     case 2: return launch_bulk_p<2>(a, p, st);

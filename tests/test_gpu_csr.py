@@ -205,13 +205,20 @@ def test_csr_small_t4_vs_oracle(ctx, solver):
 
 
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
-def test_csr_solve_wide_k_uses_csc_gather(ctx, solver):
-    """k > 2048: the CSR long pass gathers w = A^T u from the CSC copy (light columns) and the
-    heavy block (for k <= 2048 it accumulates w in shared memory in one pass)."""
-    A = _random_csr(4400, 2100, 4, 3, 20.0, 0, seed=41)
-    b = np.random.default_rng(3).standard_normal(4400)
-    x, rep = ctx.solve(_gpu_csr(A), torch.from_numpy(b).cuda(), 4400, 2100, solver=solver, gamma=1.5)
-    orc = orc_solve(A, b, solver=solver, gamma=1.5, precise_g=False)
+@pytest.mark.parametrize("m,nnz_row,dense,empty,lam", [
+    (4400, 4, 3, 0, 0.0),       # heavy ND = 16 (one heavy column per lane)
+    (4600, 40, 40, 25, 0.0),    # ND = 64 (two per lane, 40 used), 40 light entries per row, empty rows
+    (4400, 6, 0, 0, 0.3),       # no heavy block, tall Tikhonov block
+])
+def test_csr_solve_wide_k_uses_csc_gather(ctx, solver, m, nnz_row, dense, empty, lam):
+    """k > 2048: the CSR long pass runs in the heavy-dense + light-CSR form (csr_rowdot_hl) and
+    gathers the light part of w = A^T u from the CSC copy (for k <= 2048 it accumulates w in
+    shared memory in one pass)."""
+    n = 2100
+    A = _random_csr(m, n, nnz_row, dense, 20.0, empty, seed=41 + m)
+    b = np.random.default_rng(3).standard_normal(m)
+    x, rep = ctx.solve(_gpu_csr(A), torch.from_numpy(b).cuda(), m, n, solver=solver, gamma=1.5, lam=lam)
+    orc = orc_solve(A, b, solver=solver, gamma=1.5, lam=lam, precise_g=False)
     assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
     rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
     assert rel <= 1e-9, rel
