@@ -28,6 +28,8 @@
 // (csr_colgather); out = [w ; ||u||^2] like colreduce_kernel.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "philox_bm.cuh"
@@ -243,8 +245,8 @@ __global__ void csr_fill_kernel(const int64_t* __restrict__ rowptr, const int32_
 // Heavy part: part[split][i][h] = sum_{j in split} G[i, lo + j] D[j][h].
 template <int ND>
 __global__ void __launch_bounds__(THR)
-csr_sketch_heavy_kernel(const double* __restrict__ D, int64_t rows, int64_t lo, int64_t s, uint64_t seed,
-                        int64_t rows_per_split, double* __restrict__ part) {
+csr_sketch_heavy_kernel(const double* __restrict__ D, int ldd, int nd, int64_t rows, int64_t lo, int64_t s,
+                        uint64_t seed, int64_t rows_per_split, double* __restrict__ part) {
   constexpr int JT = 32;                       // D rows staged per step
   __shared__ __align__(16) double Ds[JT][ND];
   __shared__ double bmT[bm::TAB_SIZE];
@@ -263,7 +265,7 @@ csr_sketch_heavy_kernel(const double* __restrict__ D, int64_t rows, int64_t lo, 
     __syncthreads();
     for (int e = threadIdx.x; e < JT * ND; e += THR) {
       const int r = e / ND, h = e % ND;
-      Ds[r][h] = (r < nj) ? D[(jb + r) * ND + h] : 0.0;
+      Ds[r][h] = (r < nj && h < nd) ? D[(jb + r) * ldd + h] : 0.0;
     }
     __syncthreads();
     for (int r = 0; r < nj; r += 2) {            // rows r, r+1 (Ds row nj is zero when nj is odd)
@@ -423,7 +425,7 @@ csr_rowdot_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict_
 // step keep independent loads in flight.  The light w comes from the CSC gather.
 template <int HPL>
 __global__ void __launch_bounds__(THR)
-csr_rowdot_hl_kernel(const double* __restrict__ D, int ND, int nd, const int* __restrict__ heavy_cols,
+csr_rowdot_hl_kernel(const double* __restrict__ D, int ldd, int ND, int nd, const int* __restrict__ heavy_cols,
                      const int64_t* __restrict__ lrowptr, const int32_t* __restrict__ lcol,
                      const double* __restrict__ lval, int64_t rows, const double* __restrict__ t,
                      const double* __restrict__ coef, double sx, double* __restrict__ u, double* __restrict__ acc,
@@ -453,8 +455,8 @@ csr_rowdot_hl_kernel(const double* __restrict__ D, int ND, int nd, const int* __
 #pragma unroll
     for (int q = 0; q < HPL; ++q) {
       const int h = lane + 32 * q;
-      da[q] = h < nd ? ldg_stream1(D + r * ND + h) : 0.0;
-      db[q] = (h < nd && has2) ? ldg_stream1(D + (r + 1) * ND + h) : 0.0;
+      da[q] = h < nd ? ldg_stream1(D + r * ldd + h) : 0.0;
+      db[q] = (h < nd && has2) ? ldg_stream1(D + (r + 1) * ldd + h) : 0.0;
     }
     const int64_t ea0 = lrowptr[r] - lbase, ea1 = lrowptr[r + 1] - lbase;
     const int64_t eb1 = has2 ? lrowptr[r + 2] - lbase : ea1;
@@ -498,6 +500,127 @@ csr_rowdot_hl_kernel(const double* __restrict__ D, int ND, int nd, const int* __
 #pragma unroll
     for (int w = 0; w < THR / 32; ++w) v += wsh[w][h];
     wpart[(int64_t)blockIdx.x * ND + h] = sx * v;
+  }
+}
+
+// The same pass with eight rows per warp step and every load of the step issued
+// up front: one coalesced load of the eight row pointers and u values, the D rows
+// (lane l: heavy columns l, l + 32), and the batch's light entries as one
+// contiguous stream (each lane adds its products to the row they fall in).  The
+// eight row dots come out of one butterfly transpose-reduction (lane l ends with
+// row (l >> 2) & 7).  Deterministic: fixed lane order and reduction tree.
+template <int HPL>
+__global__ void __launch_bounds__(THR)
+csr_rowdot_hl8_kernel(const double* __restrict__ D, int ldd, int ND, int nd, const int* __restrict__ heavy_cols,
+                      const int64_t* __restrict__ lrowptr, const int32_t* __restrict__ lcol,
+                      const double* __restrict__ lval, int64_t rows, const double* __restrict__ t,
+                      const double* __restrict__ coef, double sx, double* __restrict__ u, double* __restrict__ acc,
+                      double* __restrict__ npart, double* __restrict__ wpart, const int* __restrict__ done) {
+  constexpr int RB = 8;
+  __shared__ double sh[THR / 32];
+  __shared__ double wsh[THR / 32][HPL * 32];
+  if (done != nullptr && *done != 0) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * THR + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * THR) >> 5;
+  const double c1 = coef[0], c2 = coef[1] * sx;
+  const double ca = (acc != nullptr) ? coef[2] : 0.0;
+  double th[HPL], wh[HPL];
+#pragma unroll
+  for (int q = 0; q < HPL; ++q) {
+    const int h = lane + 32 * q;
+    th[q] = h < nd ? __ldg(t + heavy_cols[h]) : 0.0;
+    wh[q] = 0.0;
+  }
+  double nrm = 0.0;
+  int64_t per = (rows + nwarps - 1) / nwarps;
+  per = (per + RB - 1) / RB * RB;
+  const int64_t r0 = min(rows, warp * per), r1 = min(rows, r0 + per);
+  const int64_t lbase = lrowptr[0];
+  const int myrow = (lane >> 2) & 7;
+  for (int64_t rb = r0; rb < r1; rb += RB) {
+    const int nb = (int)min((int64_t)RB, r1 - rb);
+    const int64_t lpl = lane <= nb ? lrowptr[rb + lane] - lbase : 0;
+    const double uo = lane < nb ? u[rb + lane] : 0.0;
+    double dv[RB][HPL];
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+#pragma unroll
+      for (int q = 0; q < HPL; ++q) {
+        const int h = lane + 32 * q;
+        dv[i][q] = (i < nb && h < nd) ? ldg_stream1(D + (rb + i) * ldd + h) : 0.0;
+      }
+    const int64_t e0 = __shfl_sync(0xffffffffu, lpl, 0);
+    const int64_t e1 = __shfl_sync(0xffffffffu, lpl, nb);
+    int off[RB];                                 // row starts relative to e0 (rows 1..7)
+#pragma unroll
+    for (int i = 1; i < RB; ++i) off[i] = (int)(__shfl_sync(0xffffffffu, lpl, i < nb ? i : nb) - e0);
+    double ac[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) ac[i] = 0.0;
+#pragma unroll 2
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const double prod = ldg_stream1(lval + e) * __ldg(t + lcol[e]);
+      const int rel = (int)(e - e0);
+      int ri = 0;
+#pragma unroll
+      for (int i = 1; i < RB; ++i) ri += rel >= off[i] ? 1 : 0;
+#pragma unroll
+      for (int i = 0; i < RB; ++i) ac[i] += ri == i ? prod : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+#pragma unroll
+      for (int q = 0; q < HPL; ++q) ac[i] = fma(dv[i][q], th[q], ac[i]);
+    // butterfly transpose-reduction of ac[0..7] over the 32 lanes
+    const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0, b2 = (lane & 4) != 0;
+    double a4[4], a2[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double keep = b4 ? ac[i + 4] : ac[i], send = b4 ? ac[i] : ac[i + 4];
+      a4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double keep = b3 ? a4[i + 2] : a4[i], send = b3 ? a4[i] : a4[i + 2];
+      a2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    double v;
+    {
+      const double keep = b2 ? a2[1] : a2[0], send = b2 ? a2[0] : a2[1];
+      v = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    const double uor = __shfl_sync(0xffffffffu, uo, myrow);
+    const double un = fma(c1, uor, c2 * v);               // row myrow (valid if myrow < nb)
+    if ((lane & 3) == 0 && myrow < nb) {
+      u[rb + myrow] = un;
+      if (acc != nullptr) acc[rb + myrow] = fma(ca, un, acc[rb + myrow]);
+      nrm = fma(un, un, nrm);
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const double uni = __shfl_sync(0xffffffffu, un, 4 * i);
+      if (i < nb)
+#pragma unroll
+        for (int q = 0; q < HPL; ++q) wh[q] = fma(dv[i][q], uni, wh[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < HPL; ++q) wsh[wib][lane + 32 * q] = wh[q];
+  // ||u||^2: fixed-order sum of the eight row-holder lanes of each warp
+  double nw = 0.0;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) nw += __shfl_sync(0xffffffffu, nrm, 4 * i);
+  if (lane != 0) nw = 0.0;
+  const double b = block_sum(nw, sh);      // contains __syncthreads: wsh complete
+  if (threadIdx.x == 0) npart[blockIdx.x] = b;
+  for (int h = threadIdx.x; h < nd; h += THR) {
+    double w = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < THR / 32; ++ww) w += wsh[ww][h];
+    wpart[(int64_t)blockIdx.x * ND + h] = sx * w;
   }
 }
 
@@ -609,6 +732,7 @@ csr_colgather_kernel(const int64_t* __restrict__ colptr, const int32_t* __restri
     if (h >= 0) {          // heavy: fixed-order sum of the row-pass block partials
       for (int g = lane; g < nparts; g += 32) w += wpart[(int64_t)g * ND + h];
     } else {
+      // (four entries per lane in flight ran slower: 278 vs 200 us on the c4-shaped pass)
       for (int64_t e = colptr[c] + lane; e < colptr[c + 1]; e += 32) w = fma(cval[e], u[rowidx[e]], w);
       w *= sx;
     }
@@ -642,6 +766,14 @@ csr_colgather_kernel(const int64_t* __restrict__ colptr, const int32_t* __restri
 int64_t csr_chunk_rows() { return 8192; }
 int64_t csr_nchunks(int64_t rows) { return rows > 0 ? (rows + csr_chunk_rows() - 1) / csr_chunk_rows() : 0; }
 int csr_rowdot_blocks(int nsm) { return nsm * 8; }
+// heavy-dense + light-CSR pass: one wave of resident CTAs (<= csr_rowdot_blocks)
+int csr_rowdot_hl_blocks(int nsm, int ND) {
+  int per_sm = 0;
+  cudaError_t e = ND > 32 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_rowdot_hl8_kernel<2>, THR, 0)
+                          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_rowdot_hl8_kernel<1>, THR, 0);
+  if (e != cudaSuccess || per_sm < 1) per_sm = 2;
+  return nsm * std::min(per_sm, 8);
+}
 int64_t csr_rowdot_all_max_k() { return 2048; }      // 8 warps x k doubles of shared memory (128 KB)
 // CTAs of 8 warps, as many per SM as the per-warp w copies (8 k doubles) allow
 int csr_rowdot_all_blocks(int nsm, int64_t k) {
@@ -708,7 +840,8 @@ cudaError_t launch_csr_fill(const CsrBuildArgs& a, cudaStream_t st) {
 
 template <int ND>
 static void heavy_t(const CsrSketchArgs& a, dim3 grid, cudaStream_t st) {
-  csr_sketch_heavy_kernel<ND><<<grid, THR, 0, st>>>(a.D, a.rows, a.lo, a.s, a.seed, a.rows_per_split, a.part);
+  csr_sketch_heavy_kernel<ND><<<grid, THR, 0, st>>>(a.D, a.ldd, a.nd, a.rows, a.lo, a.s, a.seed, a.rows_per_split,
+                                                    a.part);
 }
 
 cudaError_t launch_csr_sketch(const CsrSketchArgs& a, cudaStream_t st, int nsm) {
@@ -756,11 +889,21 @@ cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st) {
 cudaError_t launch_csr_rowdot_hl(const CsrRowdotArgs& a, cudaStream_t st) {
   const unsigned nb = (unsigned)a.nblocks;
   const int ND = a.ND > 0 ? a.ND : 32;
+  static const bool v8 = !std::getenv("LSRN_CSR_ROWDOT_HL2");   // tuning aid: two rows per step
+  if (v8) {
+    if (ND > 32)
+      csr_rowdot_hl8_kernel<2><<<nb, THR, 0, st>>>(a.D, a.ldd, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows,
+                                                   a.t, a.coef, a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
+    else
+      csr_rowdot_hl8_kernel<1><<<nb, THR, 0, st>>>(a.D, a.ldd, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows,
+                                                   a.t, a.coef, a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
+    return cudaGetLastError();
+  }
   if (ND > 32)
-    csr_rowdot_hl_kernel<2><<<nb, THR, 0, st>>>(a.D, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows, a.t,
+    csr_rowdot_hl_kernel<2><<<nb, THR, 0, st>>>(a.D, a.ldd, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows, a.t,
                                                 a.coef, a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
   else
-    csr_rowdot_hl_kernel<1><<<nb, THR, 0, st>>>(a.D, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows, a.t,
+    csr_rowdot_hl_kernel<1><<<nb, THR, 0, st>>>(a.D, a.ldd, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows, a.t,
                                                 a.coef, a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
   return cudaGetLastError();
 }

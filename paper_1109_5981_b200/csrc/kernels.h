@@ -128,16 +128,18 @@ struct CsrBuildArgs {
 int64_t csr_chunk_rows();
 int64_t csr_nchunks(int64_t rows);
 int csr_rowdot_blocks(int nsm);
+int csr_rowdot_hl_blocks(int nsm, int ND);
 int csr_colgather_blocks(int64_t k);
 size_t csr_max_k();
 cudaError_t launch_csr_build(const CsrBuildArgs& a, cudaStream_t st);   // validate + counts + per-column totals
 cudaError_t launch_csr_fill(const CsrBuildArgs& a, cudaStream_t st);    // colptr + CSC + D (needs colmap)
 
 struct CsrSketchArgs {
-  const double* D;         // heavy block [rows][ND]
+  const double* D;         // heavy block [rows][ldd] (nd columns used)
   int64_t rows, lo, s, k;
   uint64_t seed;
   int nd, ND, nsplit;
+  int ldd;                 // row stride of D (nd rounded up to even)
   int64_t rows_per_split;
   double* part;            // [nsplit][s][ND]
   const int* heavy_cols;   // [nd]
@@ -167,9 +169,9 @@ struct CsrRowdotArgs {
   const int* done;
   int ND, nblocks;
   // heavy-dense + light-CSR form (csr_rowdot_hl_kernel)
-  const double* D;         // [rows][ND] heavy block
+  const double* D;         // [rows][ldd] heavy block
   const int* heavy_cols;   // [nd]
-  int nd;
+  int nd, ldd;
   const int64_t* lrowptr;
   const int32_t* lcol;
   const double* lval;

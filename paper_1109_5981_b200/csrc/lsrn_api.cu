@@ -262,7 +262,7 @@ struct CsrWs {
   int nsplit;
   int64_t rows_per_split;
   // filled by csr_prepare
-  int nd = 0, ND = 0;
+  int nd = 0, ND = 0, ldd = 0;   // ldd: row stride of D (nd rounded up to even: 16-byte rows)
   int64_t nnz_light = 0;
 };
 
@@ -341,6 +341,7 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
   std::sort(cand.begin(), cand.end());
   w.nd = (int)cand.size();
   w.ND = w.nd == 0 ? 0 : (w.nd <= 16 ? 16 : (w.nd <= 32 ? 32 : 64));
+  w.ldd = (w.nd + 1) & ~1;
   std::vector<int> colmap((size_t)d.k, -1);
   for (int h = 0; h < w.nd; ++h) colmap[cand[h]] = h;
   w.nnz_light = 0;
@@ -350,7 +351,7 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
   if (w.nd > 0)
     LSRN_CUDA(cudaMemcpyAsync(w.heavy_cols, cand.data(), sizeof(int) * w.nd, cudaMemcpyHostToDevice, st));
   b.D = w.nd > 0 ? w.D : nullptr;
-  b.ld_d = w.ND;
+  b.ld_d = w.ldd;
   b.lrowptr = w.lrowptr;
   b.lcol = w.lcol;
   b.lval = w.lval;
@@ -372,6 +373,7 @@ void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double*
   a.seed = seed;
   a.nd = w.nd;
   a.ND = w.ND;
+  a.ldd = w.ldd;
   a.nsplit = w.nsplit;
   a.rows_per_split = w.rows_per_split;
   a.part = w.part;
@@ -706,14 +708,16 @@ struct Pass {
       allreduce(c, out, d.k + 1);
       return;
     }
-    a.nblocks = csr_rowdot_blocks(c->nsm);
+    const bool v1 = std::getenv("LSRN_CSR_ROWDOT_V1") != nullptr;   // tuning aid: warp per row, full CSR
+    a.nblocks = v1 ? csr_rowdot_blocks(c->nsm) : csr_rowdot_hl_blocks(c->nsm, cw->ND);
     a.D = cw->D;
     a.heavy_cols = cw->heavy_cols;
     a.nd = cw->nd;
+    a.ldd = cw->ldd;
     a.lrowptr = cw->lrowptr;
     a.lcol = cw->lcol;
     a.lval = cw->lval;
-    if (std::getenv("LSRN_CSR_ROWDOT_V1"))   // tuning aid: the warp-per-row pass over the full CSR
+    if (v1)
       LSRN_CUDA(launch_csr_rowdot(a, st));
     else
       LSRN_CUDA(launch_csr_rowdot_hl(a, st));
