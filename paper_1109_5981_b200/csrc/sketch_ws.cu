@@ -330,7 +330,8 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, cudaStream_t st) {
 // Tile shape (LSRN_SKETCH_TILE, tuning aid).  Measured on c2 (1e5 x 2000,
 // profiles/r01_sketch_tile.jsonl), ms: 64 x 256 (BK 16, 4 + 4 stages) CL 1/2 ->
 // 65.7 / 60.3; 32 x 512 (BK 16, 3 X stages) CL 1/2 -> 58.1 / 61.1; 32 x 512 with
-// BK 8 (5 X stages) CL 1/2 -> 70.2 / 74.9.  The 32 x 512 tile needs half the G
+// BK 8 (5 X stages) CL 1/2 -> 70.2 / 74.9; 16 x 1024 (BK 8, 3 X stages) -> 69.6
+// (51.6 without RNG: the BK = 8 k-block overheads outweigh the halved RNG).  The 32 x 512 tile needs half the G
 // per flop of the 64 x 256 one (each normal feeds 512 columns) without the
 // cluster exchange, so it is the default: tile 1, CL 1.
 using Tile0 = ws::Cfg<64, 256, 16, 4, 4>;
