@@ -133,3 +133,37 @@ def test_c5_full(ctx):
     g = p.X.T @ r
     an = float(torch.linalg.norm(p.X))
     assert float(torch.linalg.norm(g)) <= 10 * 2e-14 * an * float(torch.linalg.norm(p.b))
+
+
+@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+def test_t4_full(ctx, solver):
+    """NEXT-2 at its full size (1024 x 4e6, the CSR of A^T, 21 nonzeros per column of A):
+    sampled sketch entries one by one against the oracle, the Table 3 CS pass count
+    (106), and the min-length characterisation of an under-determined solve:
+    A x = b (consistent, full row rank) and x in range(A^T)."""
+    from paper_1109_5981_b200.lsrn import Csr
+    p = make_problem("t4", device="cuda")
+    m, n = p.m, p.n
+    X = Csr(p.rowptr, p.colind, p.val)                    # rows of X = columns of A
+    At = ctx.sketch(X, m, n, 2.0, 0.0, seed=SKETCH_SEED)
+    assert At.shape == (2048, 1024)
+    Xs = p.to_scipy().T.tocsc()                           # X = A^T as CSC: column c = row c of A
+
+    def col(c):
+        return np.asarray(Xs[:, c].toarray()).ravel()
+    _sampled_sketch_check(At, col, 2048, n, nsamp=8)
+    del At
+    x, rep = ctx.solve(X, p.b, m, n, solver=solver)
+    if solver == "cs":
+        assert rep["iters"] == 106
+    A = p.to_scipy()                                      # m x n
+    xh = x.cpu().numpy()
+    b = p.b.cpu().numpy()
+    res = np.linalg.norm(A @ xh - b) / np.linalg.norm(b)
+    assert res <= 1e-10, res
+    # x = A^T y for the y solving (A A^T) y = A x: the component outside range(A^T) vanishes
+    AAt = (A @ A.T).toarray()
+    y = np.linalg.solve(AAt, A @ xh)
+    leak = np.linalg.norm(xh - A.T @ y) / np.linalg.norm(xh)
+    assert leak <= 1e-10, leak
