@@ -209,6 +209,19 @@ lsrn_status lsrn_debug_gaussian(lsrn_ctx* ctx, uint64_t seed, const int64_t* row
  * kernels use; mode 1: CUDA libm (log, sqrt, sincospi).  Device arrays. */
 lsrn_status lsrn_debug_box_muller(lsrn_ctx* ctx, const uint32_t* words, int64_t count, int mode, double* out);
 
+/* Testing / tuning aid (K5/K6 parity): one fused row pass of the iterations
+ * on a device matrix Y (R x C, row-major, leading
+ * dimension ld), with the kernel plan the solver uses for that shape:
+ *   z_j <- c1 z_j + c2 sx (Y_j . t);  acc_j += ca z_j (acc nullable);
+ *   out[0:C] = sx Y^T z;  out[C] = ||z||^2,
+ * coef = {c1, c2, ca} (device, 3 doubles); t (C), z (R), out (C + 1) device.
+ * reps > 1 repeats the pass (z, acc updated each time) and, with ms_out, returns
+ * the kernel time of the last repetition (CUDA events).  Allocates its scratch
+ * with cudaMallocAsync on the context stream. */
+lsrn_status lsrn_debug_rowpass(lsrn_ctx* ctx, const double* Y, int64_t R, int64_t C, int64_t ld, const double* t,
+                               const double* coef, double sx, double* z, double* acc, double* out, int reps,
+                               double* ms_out);
+
 /* Kernel statistics of the last lsrn_sketch / lsrn_solve_* call on ctx:
  * CUDA-event durations (ms) of the dominant kernels, averaged per launch, and
  * the number of kernel launches.  Fills up to `cap` doubles:

@@ -1472,6 +1472,68 @@ lsrn_status lsrn_debug_box_muller(lsrn_ctx* c, const uint32_t* words, int64_t co
   return LSRN_OK;
 }
 
+lsrn_status lsrn_debug_rowpass(lsrn_ctx* c, const double* Y, int64_t R, int64_t C, int64_t ld, const double* t,
+                               const double* coef, double sx, double* z, double* acc, double* out, int reps,
+                               double* ms_out) {
+  if (!c || !Y || !t || !coef || !z || !out) return set_error(LSRN_EINVAL, "NULL argument");
+  if (R <= 0 || C <= 0 || ld < C || reps < 1) return set_error(LSRN_EDIM, "need R, C > 0, ld >= C, reps >= 1");
+  cudaStream_t st = c->stream;
+  const RowPassPlan pl = plan_rowpass(R, C, ld, Y, c->nsm);
+  double *wpart = nullptr, *npart = nullptr, *blockpart = nullptr;
+  unsigned* counter = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t e = cudaMallocAsync(&wpart, sizeof(double) * (size_t)pl.nclusters * C, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&npart, sizeof(double) * (size_t)pl.nclusters, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&blockpart, sizeof(double) * ((size_t)colreduce_blocks(C) + 1), st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&counter, sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  RowPassArgs a{};
+  a.Y = Y;
+  a.ld = ld;
+  a.sx = sx;
+  a.R = R;
+  a.C = C;
+  a.z = z;
+  a.t = t;
+  a.coef = coef;
+  a.acc = acc;
+  a.wpart = wpart;
+  a.npart = npart;
+  ColReduceArgs r{};
+  r.wpart = wpart;
+  r.npart = npart;
+  r.nparts = pl.nclusters;
+  r.C = C;
+  r.t = t;
+  r.coef = coef;
+  r.out = out;
+  r.blockpart = blockpart;
+  r.counter = counter;
+  // reps > 1 (timing): the pass is repeated on the same z (z, acc change every repetition)
+  for (int i = 0; i < reps && e == cudaSuccess; ++i) {
+    if (i == reps - 1 && ms_out) e = cudaEventRecord(e0, st);
+    if (e == cudaSuccess) e = launch_rowpass(a, pl, st);
+    if (i == reps - 1 && ms_out && e == cudaSuccess) e = cudaEventRecord(e1, st);
+    if (e == cudaSuccess) e = launch_colreduce(r, st);
+  }
+  if (e == cudaSuccess && ms_out) {
+    e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    *ms_out = ms;
+  }
+  if (wpart) cudaFreeAsync(wpart, st);
+  if (npart) cudaFreeAsync(npart, st);
+  if (blockpart) cudaFreeAsync(blockpart, st);
+  if (counter) cudaFreeAsync(counter, st);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (e != cudaSuccess) return set_error(LSRN_ECUDA, cudaGetErrorString(e));
+  return LSRN_OK;
+}
+
 lsrn_status lsrn_debug_gaussian(lsrn_ctx* c, uint64_t seed, const int64_t* rows, const int64_t* cols, int64_t count,
                                 double* out) {
   if (!c || !rows || !cols || !out) return set_error(LSRN_EINVAL, "NULL argument");

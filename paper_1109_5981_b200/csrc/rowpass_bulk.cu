@@ -43,12 +43,13 @@ constexpr int kMaxStages = 8;
 // TR rows per stage; P column pairs per thread (slice width <= 512 P).
 // KEEP: hold the staged row tile in registers between the two phases (2 P TR
 // doubles per thread) instead of re-reading shared memory; OCC: CTAs per SM.
-template <int P, int TR, bool KEEP, int OCC>
-__global__ void __launch_bounds__(THREADS, OCC)
+template <int P, int TR, bool KEEP, int OCC, int NT = THREADS>
+__global__ void __launch_bounds__(NT, OCC)
 rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq, int nst) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages];
-  __shared__ double red[2][NWARP][TR];
+  constexpr int NWARP_ = NT / 32;
+  __shared__ double red[2][NWARP_][TR];
   __shared__ double xs[2][16][TR];
   if (a.done != nullptr && *a.done != 0) return;     // uniform over the grid
 
@@ -94,7 +95,7 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
   double2 tv[P], wv[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    const int64_t cl = 2 * (tid + THREADS * p);
+    const int64_t cl = 2 * (tid + NT * p);
     const int64_t c = c0 + cl;
     tv[p].x = (cl < ncol) ? a.t[c] : 0.0;
     tv[p].y = (cl + 1 < ncol) ? a.t[c + 1] : 0.0;
@@ -122,7 +123,7 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
       const bool rok = rb + tr < r1;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const int64_t cl = 2 * (tid + THREADS * p);
+        const int64_t cl = 2 * (tid + NT * p);
         const double2 y = (rok && cl < ncol) ? *reinterpret_cast<const double2*>(row + cl) : make_double2(0.0, 0.0);
         if constexpr (KEEP) yk[tr][p] = y;
         s = fma(y.x, tv[p].x, fma(y.y, tv[p].y, s));
@@ -143,7 +144,7 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
       if (tid < TR) {
         double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < NWARP; ++w) s += red[buf][w][tid];
+        for (int w = 0; w < NWARP_; ++w) s += red[buf][w][tid];
         for (int rr = 0; rr < CL; ++rr) *cluster.map_shared_rank(&xs[buf][q][tid], rr) = s;
       }
       cluster.sync();
@@ -158,7 +159,7 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
       for (int tr = 0; tr < TR; ++tr) {
         double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < NWARP; ++w) s += red[buf][w][tr];
+        for (int w = 0; w < NWARP_; ++w) s += red[buf][w][tr];
         dot[tr] = s;
       }
     }
@@ -176,7 +177,7 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
         const double* rowp = stage + ((int64_t)st * TR + tr) * stage_ld;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-          const int64_t cl = 2 * (tid + THREADS * p);
+          const int64_t cl = 2 * (tid + NT * p);
           if (cl < ncol) {
             double2 y;
             if constexpr (KEEP)
@@ -194,7 +195,7 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
   double* wp = a.wpart + g * C;
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    const int64_t cl = 2 * (tid + THREADS * p);
+    const int64_t cl = 2 * (tid + NT * p);
     if (cl < ncol) wp[c0 + cl] = a.sx * wv[p].x;
     if (cl + 1 < ncol) wp[c0 + cl + 1] = a.sx * wv[p].y;
   }
@@ -403,12 +404,47 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   int64_t max_slice = wide ? 2 * kMaxSlice : kMaxSlice;
   if (const char* e = std::getenv("LSRN_ROWPASS_WIDE_SLICE"))   // tuning aid
     if (wide) max_slice = std::max<int64_t>(512, std::atoll(e));
+  auto vpt_for = [](int64_t q) {
+    int v = 1;
+    while (512 * v < q) v = (v < 8) ? v * 2 : v + 4;              // 1, 2, 4, 8, 12, 16
+    return v;
+  };
+  auto slice = [&](int n) { return (((C + n - 1) / n) + 1) & ~int64_t(1); };
   int cl = (int)((C + max_slice - 1) / max_slice);
+  // Rows wider than two 5120-double slices (c4's N-pass, k = 2e4): the smallest
+  // cluster whose slice fills >= 90 % of the threads' column pairs (masked pairs
+  // cost issue slots, and the 16-pair instance spills).  Measured with
+  // lsrn_debug_rowpass on 2e4 x 2e4 (profiles/r01_rowpass_shape.log): 3-CTA
+  // clusters (6668-double slices, 16 pairs) 2.04 TB/s, 5-CTA (4000, 8 pairs)
+  // 3.09 TB/s.  Up to 10240 (c5) the 2-CTA cluster stays best (4.44 TB/s against
+  // <= 2.7 for 3-10 CTAs).
+  // Rows of 16384-20480 doubles (c4's N-pass, k = 2e4): 2-CTA clusters of 512
+  // threads x 10 column pairs (slices up to 10240 doubles), one CTA per SM, two
+  // 1-row stages: 2e4 x 2e4 3.09 -> 3.99 TB/s (profiles/r01_rowpass_shape.log);
+  // below 16384 the 256-thread 2-CTA plan is faster (16000: 5.77 vs 4.91 TB/s).
+  // LSRN_ROWPASS_WIDE2=0 (tuning aid) disables it.
+  // Rows of 8192-10240 doubles (c5, k = 1e4): ONE CTA of 512 threads x 10 column
+  // pairs per row, no cluster and no partial-dot exchange, two 1-row stages (80 KB
+  // each): 125000 x 1e4 4.44 -> 5.80 TB/s against the 2-CTA cluster pass
+  // (profiles/r01_rowpass_shape.log).  LSRN_ROWPASS_WIDE1=0 (tuning aid) disables it.
+  const char* w1env = std::getenv("LSRN_ROWPASS_WIDE1");
+  const bool wide1 = wide && C > 8192 && C <= 10240 && !(w1env && std::atoi(w1env) == 0);
+  if (wide1) cl = 1;
+  const char* w2env = std::getenv("LSRN_ROWPASS_WIDE2");
+  const bool wide2 = wide && C > 16384 && C <= 20480 && !(w2env && std::atoi(w2env) == 0);
+  if (wide2) cl = 2;
+  if (wide && C > 10240 && !wide2 && !std::getenv("LSRN_ROWPASS_WIDE_SLICE")) {
+    for (int n = cl; n <= 16; ++n) {
+      const int64_t q = slice(n);
+      if ((double)q >= 0.9 * 512.0 * vpt_for(q)) {
+        cl = n;
+        break;
+      }
+    }
+  }
   if (cl > 16) return false;
-  int64_t cq = (C + cl - 1) / cl;
-  cq = (cq + 1) & ~int64_t(1);
-  int vpt = 1;
-  while (512 * vpt < cq) vpt = (vpt < 8) ? vpt * 2 : vpt + 4;   // 1, 2, 4, 8, 12, 16
+  const int64_t cq = slice(cl);
+  const int vpt = (wide2 || wide1) ? 16 : vpt_for(cq);            // replaced by the 512-thread plans below
   if (vpt > 16) return false;                                     // no kernel instance: fallback
   // Wide rows: two CTAs (clusters) per SM with two 1-row stages each when two
   // slices fit in half of shared memory.  Each CTA's per-tile chain (block
@@ -419,6 +455,7 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   // LSRN_ROWPASS_BUDGET_KB.
   int occ = 2;
   if (wide && 2 * (size_t)cq * 8 > kWideBudget / 2) occ = 1;
+  if (wide2 || wide1) occ = 1;
   if (const char* e = std::getenv("LSRN_ROWPASS_OCC")) occ = std::atoi(e) == 1 ? 1 : 2;
   size_t budget = wide ? (occ == 1 ? kWideBudget : kWideBudget / 2) : kStageBudget / occ;
   if (const char* e = std::getenv("LSRN_ROWPASS_BUDGET_KB")) budget = (size_t)std::atoi(e) * 1024;
@@ -426,11 +463,13 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   int t2 = 1;
   while (t2 * 2 <= tr) t2 *= 2;
   tr = t2;
+  if (const char* e = std::getenv("LSRN_ROWPASS_TR"))            // tuning aid (wide rows: 1 or 2)
+    if (wide) tr = std::atoi(e) == 2 ? 2 : 1;
   const size_t stage_bytes = (size_t)tr * cq * 8;
   int nst = (int)std::min<size_t>(kMaxStages, budget / stage_bytes);
   // one stage being reduced, one waiting for its refill, >= 1 in flight; with two
   // CTAs per SM on wide rows (tuning aid) two stages each still keep two in flight per SM
-  if (nst < 3 && !(wide && occ == 2 && nst == 2)) return false;
+  if (nst < 3 && !(wide && (occ == 2 || wide2 || wide1 || tr == 2) && nst == 2)) return false;
   bool keep = vpt * tr <= (occ == 2 ? 4 : 16);
   if (const char* e = std::getenv("LSRN_ROWPASS_KEEP")) keep = std::atoi(e) != 0 && vpt * tr <= 16;
   p->keep = keep ? 1 : 0;
@@ -458,6 +497,16 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   // neither 512 threads (3.76 TB/s) nor an mbarrier-only tile flow without the two
   // per-tile __syncthreads (3.50 TB/s) beat this kernel (4.05 TB/s,
   // profiles/r01_rowpass_tune_c5c.jsonl).
+  if (wide1 && p->tr == 1) {
+    p->nt = 512;
+    p->vpt = 10;
+    return true;
+  }
+  if (wide2 && p->async_x && p->tr == 1) {
+    p->nt = 512;
+    p->vpt = 10;
+    return true;
+  }
   if (cl > 1 && p->async_x) {
     int nt = 256;
     if (const char* e = std::getenv("LSRN_ROWPASS_NT")) nt = std::atoi(e) == 512 ? 512 : 256;
@@ -473,10 +522,10 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   return true;
 }
 
-template <int P, int TR, bool KEEP, int OCC>
+template <int P, int TR, bool KEEP, int OCC, int NT = THREADS>
 static cudaError_t launch_bulk_k(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
   const size_t smem = (size_t)p.nst * TR * p.cq * 8;
-  auto kern = rowpass_bulk_kernel<P, TR, KEEP, OCC>;
+  auto kern = rowpass_bulk_kernel<P, TR, KEEP, OCC, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (p.cl > 8) {
@@ -485,7 +534,7 @@ static cudaError_t launch_bulk_k(const RowPassArgs& a, const RowPassPlan& p, cud
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.nclusters * p.cl));
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -561,10 +610,12 @@ static cudaError_t launch_cluster512(const RowPassArgs& a, const RowPassPlan& p,
 }
 
 cudaError_t launch_rowpass_bulk(const RowPassArgs& a, const RowPassPlan& p, cudaStream_t st) {
+  if (p.nt == 512 && p.cl == 1) return launch_bulk_k<10, 1, false, 1, 512>(a, p, st);
   if (p.nt == 512) {
     switch (p.vpt) {
       case 4: return launch_cluster512<4>(a, p, st);
       case 6: return launch_cluster512<6>(a, p, st);
+      case 10: return launch_cluster512<10>(a, p, st);
       default: return launch_cluster512<8>(a, p, st);
     }
   }

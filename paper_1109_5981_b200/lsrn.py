@@ -25,7 +25,7 @@ STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE
 # every symbol include/lsrn.h declares
 EXPORTS = ["lsrn_last_error", "lsrn_version", "lsrn_nccl_unique_id", "lsrn_ctx_create", "lsrn_ctx_destroy",
            "lsrn_ctx_set_profiling", "lsrn_workspace_size", "lsrn_sketch",
-           "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_debug_box_muller", "lsrn_last_stats",
+           "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_debug_box_muller", "lsrn_debug_rowpass", "lsrn_last_stats",
            "lsrn_choose_gamma"]
 
 
@@ -87,6 +87,7 @@ def lib():
             "lsrn_debug_gaussian": [vp, u64, vp, vp, i64, vp],
             "lsrn_debug_box_muller": [vp, vp, i64, i32, vp],
             "lsrn_last_stats": [vp, ctypes.POINTER(ctypes.c_double), i32],
+            "lsrn_debug_rowpass": [vp, vp, i64, i64, i64, vp, vp, dbl, vp, vp, vp, i32, ctypes.POINTER(dbl)],
             "lsrn_choose_gamma": [ctypes.POINTER(Report), i64, i64, dbl, i32, dbl, dbl,
                                   ctypes.POINTER(dbl), ctypes.POINTER(dbl)],
         }
@@ -280,6 +281,20 @@ class Context:
             x, rep = self.solve(X, b, m, n, lam=lam, reuse_sketch=(i > 0), **kw)
             out.append((x.clone(), rep))
         return out
+
+    def debug_rowpass(self, Y, t, z, coef, sx=1.0, acc=None, reps=1):
+        """One fused row pass (lsrn_debug_rowpass) on device tensors; returns (out, ms)
+        with out = [sx Y^T z_new ; ||z_new||^2] (z, acc updated in place)."""
+        R, C = Y.shape
+        out = torch.empty(C + 1, dtype=torch.float64, device=self.device)
+        cf = torch.as_tensor(coef, dtype=torch.float64).to(self.device)
+        ms = ctypes.c_double(0.0)
+        cur = self._enter()
+        _check(lib().lsrn_debug_rowpass(self.h, _ptr(Y), R, C, Y.stride(0), _ptr(t), _ptr(cf), sx, _ptr(z),
+                                        _ptr(acc) if acc is not None else None, _ptr(out), reps, ctypes.byref(ms)))
+        self._leave(cur)
+        torch.cuda.synchronize(self.device)
+        return out, ms.value
 
     def debug_box_muller(self, words, mode=0):
         """(count, 2) normals of the Box-Muller transform of (count, 4) uint32 Philox words."""

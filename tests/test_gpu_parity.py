@@ -265,22 +265,25 @@ def test_tuning_variants_match(ctx, monkeypatch, env):
     _check_solution(A, x.cpu().numpy(), orc["x"], p.meta["kappa"])
 
 
-@pytest.mark.parametrize("asyncx", ["1", "0"])
+@pytest.mark.parametrize("n,env", [(4100, {}), (9000, {}), (9000, {"LSRN_ROWPASS_WIDE1": "0"}),
+                                   (9000, {"LSRN_ROWPASS_WIDE1": "0", "LSRN_ROWPASS_ASYNCX": "0"})])
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
-def test_wide_rows_cluster_pass_vs_pseudoinverse(ctx, monkeypatch, asyncx, solver):
-    """k > 4096: each row of A is split over a 2-CTA cluster in the long pass (partial dots
-    exchanged with st.async, or with a cluster barrier when LSRN_ROWPASS_ASYNCX=0).  The
-    generator's factors give x* = V diag(1/sigma) U^T b exactly."""
-    monkeypatch.setenv("LSRN_ROWPASS_ASYNCX", asyncx)
-    p = make_problem("c1", m=6000, n=4100, keep_factors=True)
+def test_wide_rows_vs_pseudoinverse(ctx, monkeypatch, n, env, solver):
+    """k > 4096: one CTA per row up to 8192 doubles (256 threads) and up to 10240 (512
+    threads); with LSRN_ROWPASS_WIDE1=0 each row is split over a 2-CTA cluster (partial
+    dots exchanged with st.async, or with a cluster barrier when LSRN_ROWPASS_ASYNCX=0).
+    The generator's factors give x* = V diag(1/sigma) U^T b exactly."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    p = make_problem("c1", m=n + 1900, n=n, keep_factors=True)
     U, V, sig = p.meta["U"].numpy(), p.meta["V"].numpy(), p.meta["sigma"].numpy()
     b = p.b.numpy()
     xstar = V @ ((U.T @ b) / sig)
     x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver=solver, gamma=1.5)
-    assert rep["r"] == 4100
+    assert rep["r"] == n
     dx = x.cpu().numpy() - xstar
     # Thm 4.5's A-norm form (P:656-662) is kappa-free; the 2-norm carries the fp64
-    # floor ~ kappa u sqrt(n) of any two implementations (DESIGN.md C18), here n = 4100
+    # floor ~ kappa u sqrt(n) of any two implementations (DESIGN.md C18), here n >= 4100
     an = np.linalg.norm(sig * (V.T @ dx)) / np.linalg.norm(sig * (V.T @ xstar))
     assert an <= 1e-10, an
     rel = np.linalg.norm(dx) / np.linalg.norm(xstar)
