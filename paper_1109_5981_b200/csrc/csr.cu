@@ -660,7 +660,8 @@ csr_rowdot_all_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restr
   const int64_t r0 = warp * per, r1 = min(rows, r0 + per);
   // two rows per step (independent loads and reductions in flight); rows of <= 32
   // entries (the common sparse case) keep (c, a) in registers for the w update.
-  // (Four rows of eight lanes each ran slower: 0.81 vs 1.27 TB/s on t4.)
+  // (Four rows of eight lanes each ran slower: 0.81 vs 1.27 TB/s on t4; so did eight
+  // rows per step with all loads up front and chunk-wise smem updates: 1.05 TB/s.)
   for (int64_t r = r0; r < r1; r += 2) {
     const bool has2 = r + 1 < r1;
     const int64_t ea0 = rowptr[r] - base, ea1 = rowptr[r + 1] - base;
