@@ -29,7 +29,7 @@
 // reaches 49.3 ms (88 %).  Rejected: 4 producer warps with two interleaved
 // pairs per lane (66 ms), 8 producer warps each computing the pairs of two
 // k-blocks interleaved (64 / 192 registers: 58.2 vs 57.9 ms), deeper G rings
-// (no change), BK = 8 (70 ms), X
+// (no change), consumers in warpgroups 0-1 instead of 2-3 (no change), BK = 8 (70 ms), X
 // streamed by a consumer warp (serialises the consumers), batched RNG phases
 // in a non-specialized kernel (sketch_batch.cu, 73.9 ms).
 // Clusters (64 x 256 tile only by default): the CTAs of a cluster of CL along N
