@@ -1131,7 +1131,6 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     Plan PL{};
     const size_t need = plan_all(c, A_in, o, ar, PL, false);
     Dims& d = PL.d;
-    SketchWs& sw = PL.sw;
     SvdWs& vw = PL.vw;
     IterWs& iw = PL.iw;
     double* At = PL.At;
@@ -1186,7 +1185,6 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     else
       P.plong = plan_rowpass(d.cnt, d.k, A.ld, A.val, c->nsm);
     P.pshort = plan_rowpass(r, d.k, d.k, vw.Nt, c->nsm);
-    const int64_t nV = d.tall ? r : d.Lz;  // length of the v-side vectors (LSQR)
 
     // coefficient table (device): consts + CS schedule
     std::vector<double> coefh((size_t)iw.ncoef, 0.0);

@@ -35,7 +35,6 @@ namespace lsrn {
 namespace {
 
 constexpr int THREADS = 256;
-constexpr int NWARP = THREADS / 32;
 constexpr int kMaxStages = 8;
 
 }  // namespace
