@@ -8,8 +8,9 @@ The oracle cannot redo a full-size solve in seconds, so these tests check
     against A^+ b directly; iteration counts against Thm 4.5 / Alg. 3 (P:643,
     P:694) and the rank against the generator's rank;
   * invariants at any size: x in range(A^T) and the normal equations.
-c2 runs by default (about a minute); c3 (3.2 GB), c4 (CSR, 1.4e8 nonzeros)
-and c5 (80 GB) run when LSRN_FULLSIZE=1 (their SVD / sketch stages take long).
+c2 runs by default (about a minute); c3 (3.2 GB), c4 (CSR, 1.4e8 nonzeros:
+sampled sketch and a full CS solve), c5 (80 GB) and t4 (NEXT-2) run when
+LSRN_FULLSIZE=1 (their SVD / sketch stages take long).
 """
 import os
 
@@ -112,6 +113,25 @@ def test_c4_full_sketch(ctx):
     def col(c):
         return np.asarray(A[:, c].toarray()).ravel()
     _sampled_sketch_check(At, col, At.shape[0], p.m, nsamp=8)
+
+
+@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
+def test_c4_full_solve(ctx):
+    """c4 end to end with CS (the config's solver): Alg. 3's pass count from the Thm 4.4
+    bounds at r = k = 2e4, s = 4e4, and the normal equations
+    A^T (b - A x) = 0 to the iteration tolerance (Thm 4.5's A-norm bound, as for c5)."""
+    from paper_1109_5981_b200.lsrn import Csr
+    p = make_problem("c4", device="cuda")
+    X = Csr(p.rowptr, p.colind, p.val)
+    x, rep = ctx.solve(X, p.b, p.m, p.n, solver="cs")
+    s = 40000
+    sl, su = bounds.sigma_bounds(s, 20000, bounds.default_alpha(s))
+    assert rep["r"] == 20000 and rep["iters"] == bounds.cs_passes(sl, su, 1e-14)
+    A = p.to_scipy()
+    xh, b = x.cpu().numpy(), p.b.cpu().numpy()
+    g = A.T @ (b - A @ xh)
+    an = np.sqrt((A.data ** 2).sum())                     # ||A||_F >= ||A||_2
+    assert np.linalg.norm(g) <= 10 * 2e-14 * an * np.linalg.norm(b)
 
 
 @pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
