@@ -541,7 +541,7 @@ SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   double vl = 0.0, vu = 0.0;
   LSRN_SOLVER(cusolverDnXgeqrf_bufferSize(c->solver, c->params, d.s, d.k, CUDA_R_64F, nullptr, d.s, CUDA_R_64F,
                                           nullptr, CUDA_R_64F, &d1, &h1));
-  w.jw = 2 * d.k <= kMaxJW;
+  w.jw = 2 * d.k <= kMaxJW && !std::getenv("LSRN_SVD_GESVD");   // tuning / test aid: force the fallback
   if (w.jw) {
     LSRN_SOLVER(cusolverDnXsyevdx_bufferSize(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
                                              CUBLAS_FILL_MODE_LOWER, 2 * d.k, CUDA_R_64F, nullptr, 2 * d.k, &vl, &vu,

@@ -137,6 +137,24 @@ def test_solve_small_configs(ctx, solver, name):
                     x.cpu().numpy(), orc["x"], kappa)
 
 
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_svd_gesvd_fallback_small(ctx, monkeypatch, name):
+    """The SVD fallback used when the Jordan-Wielandt matrix exceeds cuSOLVER's limit
+    (k > 16384, c4) -- geqrf + gesvd of R -- forced at small size: same rank, counts and
+    solution as the oracle (rank-deficient c2 and Tikhonov c3)."""
+    monkeypatch.setenv("LSRN_SVD_GESVD", "1")
+    p = small(name)
+    A = p.dense_A().numpy()
+    b = p.b.numpy()
+    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs", lam=p.lam)
+    orc = orc_solve(A, b, solver="cs", lam=p.lam)
+    assert rep["r"] == orc["r"] and rep["iters"] == orc["iters"]
+    sv = np.linalg.svd(A, compute_uv=False)
+    kappa = sv[0] / sv[sv > sv[0] * 1e-12][-1]
+    _check_solution(A if p.lam == 0 else np.vstack([A, p.lam * np.eye(p.n)]) if p.tall else A,
+                    x.cpu().numpy(), orc["x"], kappa)
+
+
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
 @pytest.mark.parametrize("shape,r,lam", [((400, 20), 20, 0.0), ((400, 20), 13, 0.0), ((20, 400), 9, 0.0),
                                          ((300, 15), 15, 1e-2), ((15, 300), 15, 1e-2)])
@@ -250,7 +268,7 @@ def test_sketch_tiles_and_clusters(ctx, monkeypatch, tile, maxcl, n):
     assert _relfro(At, ref) <= 1e-12
 
 
-@pytest.mark.parametrize("env", [{"LSRN_ROWPASS_KEEP": "0"}, {"LSRN_ROWPASS_OCC": "1"},
+@pytest.mark.parametrize("env", [{"LSRN_SVD_GESVD": "1"}, {"LSRN_ROWPASS_KEEP": "0"}, {"LSRN_ROWPASS_OCC": "1"},
                                  {"LSRN_ROWPASS_OCC": "1", "LSRN_ROWPASS_KEEP": "1"}, {"LSRN_SKETCH_V1": "1"},
                                  {"LSRN_SKETCH_IMPL": "batch"}, {"LSRN_SKETCH_IMPL": "ws"}])
 def test_tuning_variants_match(ctx, monkeypatch, env):
