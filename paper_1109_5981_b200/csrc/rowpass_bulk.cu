@@ -15,11 +15,14 @@
 // current stage out of shared memory.
 //
 // Layout: cluster g owns a contiguous chunk of rows; CTA q of the cluster owns
-// the column slice [q Cq, (q+1) Cq) (Cq <= 4096 doubles = 32 KB); thread tid owns
-// columns 2 (tid + 256 p) + {0, 1} of the slice, p < P, and keeps t and w for
-// them in registers.  Partial row dots of the cluster's CTAs are exchanged
-// through distributed shared memory (one cluster barrier per stage).
-// Deterministic: fixed row chunks and reduction trees, no atomics.
+// the column slice [q Cq, (q+1) Cq); thread tid owns columns 2 (tid + NT p) +
+// {0, 1} of the slice, p < P, and keeps t and w for them in registers.  Plans
+// (plan_rowpass_bulk): rows <= 8192 doubles in one 256-thread CTA (two CTAs per
+// SM); 8192-10240 in one 512-thread CTA with two 1-row stages (c5); wider rows in
+// clusters whose partial row dots are exchanged through distributed shared
+// memory (rowpass_cluster_kernel, asynchronous st.async exchange; 2-CTA clusters
+// of 512 threads up to 20480, c4's N-pass).  Deterministic: fixed row chunks and
+// reduction trees, no atomics.
 #include <algorithm>
 #include <cstdlib>
 
