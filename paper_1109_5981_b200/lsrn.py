@@ -122,7 +122,7 @@ def dense(X, m, n, lo=0, cnt=None):
     """Matrix descriptor for a long-index-major dense shard X (cnt x k, row-major)."""
     if X.dtype != torch.float64:
         raise TypeError("A must be float64")
-    if X.dim() != 2 or X.stride(1) != 1:
+    if X.dim() != 2 or (X.stride(1) != 1 and X.shape[1] > 1):   # a 1-column stride is immaterial
         raise ValueError("X must be a 2-D tensor with unit column stride (long-index-major)")
     cnt = X.shape[0] if cnt is None else cnt
     return Matrix(kind=LSRN_DENSE, m=m, n=n, lo=lo, cnt=cnt, val=X.data_ptr(), ld=X.stride(0) if cnt > 1 else
@@ -247,7 +247,7 @@ class Context:
               mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False, reuse_sketch=False):
         """LSRN solve; X a long-index-major dense shard or a Csr row shard (device, or pinned host with host_io)."""
         if host_io and not isinstance(X, Csr):
-            if X.dim() != 2 or X.stride(1) != 1:
+            if X.dim() != 2 or (X.stride(1) != 1 and X.shape[1] > 1):   # a 1-column stride is immaterial
                 raise ValueError("X must be row-major 2-D")
             cnt_ = X.shape[0] if cnt is None else cnt
             mat = Matrix(kind=LSRN_DENSE, m=m, n=n, lo=lo, cnt=cnt_, val=X.data_ptr(), ld=X.stride(0))
