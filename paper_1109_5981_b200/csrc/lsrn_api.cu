@@ -186,18 +186,27 @@ int choose_nsplit(int64_t s, int64_t k, int64_t rows, int nsm) {
   int64_t mt, nt, bk;
   sketch_tile_counts(s, k, &mt, &nt, &bk);
   const int64_t tiles = mt * nt;
+  if (const char* e = std::getenv("LSRN_SKETCH_NSPLIT")) {       // tuning aid
+    const int f = std::atoi(e);
+    if (f >= 1) return f;
+  }
+  // Split-K over rows for whole waves of CTAs: the smallest split whose last wave
+  // is >= 99 % full, else the fullest (partials capped at 4 GB).  c2 (500 tiles of
+  // 32 x 512): 2 splits (96.5 %) 58.1 ms, 13 splits (99.8 %) 56.5 ms
+  // (profiles/r01_sketch_nsplit.jsonl).
   int best = 1;
   double best_eff = 0.0;
   for (int sp = 1; sp <= 16; ++sp) {
     if (sp > 1 && rows / sp < 1024) break;
+    if (sp > 1 && (double)sp * (double)s * (double)k * 8.0 > 4.0e9) break;
     const int64_t units = tiles * sp;
     const int64_t waves = (units + nsm - 1) / nsm;
     const double eff = (double)units / (double)(waves * nsm);
-    if (eff > best_eff + 0.02) {
+    if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = sp;
     }
-    if (eff > 0.95) break;
+    if (eff >= 0.99) break;
   }
   return best;
 }
