@@ -211,6 +211,8 @@ int choose_nsplit(int64_t s, int64_t k, int64_t rows, int nsm) {
   return best;
 }
 
+constexpr int kMaxChunks = 16;   // = size of lsrn_ctx::chunk_ev
+
 struct SketchWs {
   int nsplit = 1;
   int64_t rows_per_split = 0;
@@ -218,32 +220,50 @@ struct SketchWs {
   // LSRN_HOST_IO streaming: A arrives in nchunk H2D chunks; chunk i is sketched (split-K
   // nsplit inside the chunk) as soon as it lands and accumulated into the nsplit partials
   int nchunk = 0;
-  int64_t rows_per_chunk = 0;
+  int64_t chunk_r0[kMaxChunks + 1] = {};   // chunk i = rows [chunk_r0[i], chunk_r0[i+1])
 };
 
 // Host-IO streaming: A is copied in chunks of >= 128 MB on a second stream and
 // each chunk is sketched as soon as it has landed, so the H2D copy of A
 // overlaps the sketch (one split-K slot per chunk, summed in fixed order).
-int stream_chunks(const Dims& d, int64_t ld) {
-  const double bytes = 8.0 * (double)d.cnt * (double)ld;
-  static const double chunk_mb = [] {
-    const char* e = std::getenv("LSRN_HOSTIO_CHUNK_MB");   // test / tuning knob
-    return (e && std::atof(e) > 0.0) ? std::atof(e) : 128.0;
+// Chunk boundaries (rows) of the streamed host copy of A: geometric sizes (first
+// 32 MB, x1.5 each, <= 16 chunks) so that the first sketch launch starts after a
+// short copy and later chunks (copied at ~55 GB/s, sketched at ~29 GB/s of A)
+// stay ahead of the sketch.  Returns the chunk count (1: no streaming).
+int stream_chunks(const Dims& d, int64_t ld, int64_t* r0) {
+  const double row_bytes = 8.0 * (double)ld;
+  static const double first_mb = [] {
+    const char* e = std::getenv("LSRN_HOSTIO_CHUNK_MB");   // test / tuning knob: first chunk size
+    return (e && std::atof(e) > 0.0) ? std::atof(e) : 32.0;
   }();
-  const int n = (int)std::ceil(bytes / (chunk_mb * 1024 * 1024));
-  return std::max(1, std::min(16, std::min(n, (int)std::max<int64_t>(1, d.cnt / 256))));
+  if (8.0 * (double)d.cnt * (double)ld < 2.0 * first_mb * 1024 * 1024 || d.cnt < 512) return 1;
+  int n = 0;
+  int64_t row = 0;
+  double size = first_mb * 1024 * 1024;
+  while (row < d.cnt && n < kMaxChunks) {
+    r0[n++] = row;
+    int64_t nr = std::max<int64_t>(256, (int64_t)(size / row_bytes) / 16 * 16);
+    if (n == kMaxChunks || row + nr > d.cnt) nr = d.cnt - row;
+    row += nr;
+    size *= 1.5;
+  }
+  r0[n] = d.cnt;
+  return n;
 }
 
-SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_flag, int force_chunks = 0) {
+SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_flag, bool host_stream = false,
+                     int64_t ld = 0) {
   SketchWs w{};
-  if (force_chunks > 1) {
-    const int64_t rpc = (d.cnt + force_chunks - 1) / force_chunks;
-    w.rows_per_chunk = std::max<int64_t>(16, (rpc + 15) / 16 * 16);
-    w.nchunk = (int)((d.cnt + w.rows_per_chunk - 1) / w.rows_per_chunk);
-    w.nsplit = choose_nsplit(d.s, d.k, w.rows_per_chunk, c->nsm);
-    w.rows_per_split = (w.rows_per_chunk + w.nsplit - 1) / w.nsplit;
-    w.part = ar.take<double>((size_t)w.nsplit * d.s * d.k);
-    return w;
+  if (host_stream && d.cnt > 0) {
+    w.nchunk = stream_chunks(d, ld, w.chunk_r0);
+    if (w.nchunk > 1) {
+      w.nsplit = 1;
+      for (int i = 0; i < w.nchunk; ++i)
+        w.nsplit = std::max(w.nsplit, choose_nsplit(d.s, d.k, w.chunk_r0[i + 1] - w.chunk_r0[i], c->nsm));
+      w.part = ar.take<double>((size_t)w.nsplit * d.s * d.k);
+      return w;
+    }
+    w.nchunk = 0;
   }
   w.nsplit = choose_nsplit(d.s, d.k, d.cnt, c->nsm);
   int64_t rps = (d.cnt + w.nsplit - 1) / w.nsplit;
@@ -400,9 +420,11 @@ void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double*
 void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed, const SketchWs& w, double* At) {
   cudaStream_t st = c->stream;
   if (w.nchunk > 1) {          // one launch per H2D chunk, each after its copy event
+    LSRN_CUDA(launch_fill(w.part, 0.0, (int64_t)w.nsplit * d.s * d.k, st));
+    c->launches++;
     for (int i = 0; i < w.nchunk; ++i) {
-      const int64_t r0 = (int64_t)i * w.rows_per_chunk;
-      const int64_t nr = std::min(w.rows_per_chunk, d.cnt - r0);
+      const int64_t r0 = w.chunk_r0[i];
+      const int64_t nr = w.chunk_r0[i + 1] - r0;
       LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[i], 0));
       SketchDenseArgs a{};
       a.X = A->val + r0 * A->ld;
@@ -412,11 +434,11 @@ void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed,
       a.lo = d.lo + r0;
       a.s = d.s;
       a.seed = seed;
-      a.rows_per_split = w.rows_per_split;
-      a.nsplit = w.nsplit;
+      a.nsplit = choose_nsplit(d.s, d.k, nr, c->nsm);      // <= w.nsplit
+      a.rows_per_split = (nr + a.nsplit - 1) / a.nsplit;
       a.out = w.part;
       a.out_split_stride = d.s * d.k;
-      a.accumulate = i > 0;   // chunks are stream-ordered: fixed summation order
+      a.accumulate = 1;       // chunks are stream-ordered: fixed summation order
       LSRN_CUDA(launch_sketch_dense(a, st));
       c->launches++;
     }
@@ -1030,8 +1052,7 @@ size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar
   if (P.csr)
     P.cw = plan_csr(c, d, A, ar);
   else
-    P.sw = plan_sketch(c, d, ar, c->nranks > 1,
-                       ((o->flags & LSRN_HOST_IO) && solve && d.cnt > 0) ? stream_chunks(d, A->ld) : 0);
+    P.sw = plan_sketch(c, d, ar, c->nranks > 1, (o->flags & LSRN_HOST_IO) && solve, A->ld);
   if (solve) {
     P.vw = plan_svd(c, d, ar);
     // max passes: LSQR cap (2x the count for r = k) or CS passes with r = k; bounded by a generous margin
@@ -1096,8 +1117,8 @@ lsrn_matrix stage_inputs(lsrn_ctx* c, const lsrn_matrix* A_in, const lsrn_opts* 
     LSRN_CUDA(cudaEventRecord(c->io_ev, st));
     LSRN_CUDA(cudaStreamWaitEvent(c->copy_stream, c->io_ev, 0));
     for (int i = 0; i < P.sw.nchunk; ++i) {
-      const int64_t r0 = (int64_t)i * P.sw.rows_per_chunk;
-      const int64_t nr = std::min(P.sw.rows_per_chunk, d.cnt - r0);
+      const int64_t r0 = P.sw.chunk_r0[i];
+      const int64_t nr = P.sw.chunk_r0[i + 1] - r0;
       LSRN_CUDA(cudaMemcpyAsync(P.Astage + r0 * A_in->ld, A_in->val + r0 * A_in->ld, sizeof(double) * nr * A_in->ld,
                                 cudaMemcpyHostToDevice, c->copy_stream));
       LSRN_CUDA(cudaEventRecord(c->chunk_ev[i], c->copy_stream));
