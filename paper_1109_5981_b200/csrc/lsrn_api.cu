@@ -104,6 +104,9 @@ struct lsrn_ctx {
 #endif
   // cached iteration graph
   cudaGraphExec_t gexec = nullptr;
+  // the iteration graph is re-captured only when something it bakes in changed
+  std::vector<int64_t> graph_key;
+  int graph_launches = 0, graph_pass_ev = 0;
   std::vector<char> gkey;
   // timing
   cudaEvent_t ev[8] = {};
@@ -1284,7 +1287,52 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
       }
     }
     const int launches_before = c->launches;
+    // Everything the captured graph holds by value: pointers, sizes, plans, counts,
+    // the CSR heavy/light split and the profiling events.  Coefficients, LSQR state
+    // and the stop flag live in device memory and are re-initialised above, so an
+    // identical key means the previous graph is this solve's graph.
+    std::vector<int64_t> gk;
+    auto kp = [&](const void* v) { gk.push_back((int64_t)reinterpret_cast<uintptr_t>(v)); };
+    auto ki = [&](int64_t v) { gk.push_back(v); };
+    auto kd = [&](double v) {
+      int64_t bits;
+      std::memcpy(&bits, &v, sizeof(bits));
+      gk.push_back(bits);
+    };
+    auto kplan = [&](const RowPassPlan& q) {
+      for (int64_t v : {(int64_t)q.vpt, (int64_t)q.cl, (int64_t)q.tr, (int64_t)q.nclusters, (int64_t)q.vec,
+                        q.rows_per_cluster, (int64_t)q.bulk, q.cq, (int64_t)q.nst, (int64_t)q.keep, (int64_t)q.occ,
+                        (int64_t)q.async_x, (int64_t)q.nt})
+        ki(v);
+    };
+    kp(A.val), kp(A.rowptr), kp(A.colind), kp(ws), kp(b), kp(x), kp(c->pass_ev.empty() ? nullptr : c->pass_ev.data());
+    // workspace carve-up (offsets move when the plan changes, e.g. the SVD fallback)
+    for (const void* q : {(const void*)iw.z, (const void*)iw.v, (const void*)iw.y, (const void*)iw.wy,
+                          (const void*)iw.xL, (const void*)iw.wxL, (const void*)iw.comm, (const void*)iw.tbuf,
+                          (const void*)iw.xbuf, (const void*)iw.wpart, (const void*)iw.npart,
+                          (const void*)iw.blockpart, (const void*)iw.ypart, (const void*)iw.coef,
+                          (const void*)iw.consts, (const void*)iw.counters, (const void*)iw.state,
+                          (const void*)vw.Nt})
+      kp(q);
+    if (PL.csr)
+      for (const void* q : {(const void*)PL.cw.colptr, (const void*)PL.cw.rowidx, (const void*)PL.cw.cval,
+                            (const void*)PL.cw.D, (const void*)PL.cw.colmap, (const void*)PL.cw.heavy_cols,
+                            (const void*)PL.cw.wpart, (const void*)PL.cw.npart, (const void*)PL.cw.lrowptr,
+                            (const void*)PL.cw.lcol, (const void*)PL.cw.lval})
+        kp(q);
+    ki(A.ld), ki(A.nnz), ki(r), ki(iters_graph), ki(passes), ki(solver), ki(o->mode), ki(c->profile ? 1 : 0);
+    ki((int64_t)c->pass_ev.size()), ki(PL.csr ? 1 : 0), ki(std::getenv("LSRN_CSR_ROWDOT_V1") ? 1 : 0);
+    if (PL.csr) ki(PL.cw.nd), ki(PL.cw.ND), ki(PL.cw.ldd), ki(PL.cw.nnz_light);
+    ki(d.tall ? 1 : 0), ki(d.m), ki(d.n), ki(d.L), ki(d.k), ki(d.s), ki(d.cnt), ki(d.lo), kd(d.sx), kd(d.si);
+    ki(d.has_I ? 1 : 0), ki(d.Lz);
+    kplan(P.plong), kplan(P.pshort);
+    const bool graph_hit = c->gexec && c->graph_key == gk && !std::getenv("LSRN_GRAPH_RECAPTURE");   // test aid
     cudaGraph_t graph = nullptr;
+    if (graph_hit) {
+      c->launches += c->graph_launches;
+      c->n_pass_ev = c->graph_pass_ev;
+    } else {
+    c->graph_key.clear();
     if (c->gexec) {
       cudaGraphExecDestroy(c->gexec);
       c->gexec = nullptr;
@@ -1353,6 +1401,10 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     LSRN_CUDA(cudaStreamEndCapture(st, &graph));
     LSRN_CUDA(cudaGraphInstantiate(&c->gexec, graph, 0));
     cudaGraphDestroy(graph);
+    c->graph_key = gk;
+    c->graph_launches = c->launches - launches_before;
+    c->graph_pass_ev = c->n_pass_ev;
+    }   // capture
     const int graph_launches = c->launches - launches_before;
     LSRN_CUDA(cudaEventRecord(c->ev[6], st));
     LSRN_CUDA(cudaGraphLaunch(c->gexec, st));

@@ -271,6 +271,28 @@ def test_host_io_streamed(ctx, solver):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
+def test_graph_cache_matches_fresh_context(ctx, monkeypatch):
+    """The iteration graph is reused when nothing it holds by value changed; a sequence that
+    changes solver, Tikhonov lambda, the SVD path (workspace carve-up) and back must give,
+    solve by solve, bit-for-bit the result of a fresh context (which always captures)."""
+    from paper_1109_5981_b200 import lsrn
+    p = small("c2")
+    X, b = p.X.cuda(), p.b.cuda()
+    steps = [dict(solver="lsqr"), dict(solver="lsqr"), dict(solver="cs"), dict(solver="lsqr", lam=0.3),
+             dict(solver="lsqr", lam=0.3), dict(solver="lsqr", env="1"), dict(solver="lsqr"), dict(solver="cs")]
+    for st_ in steps:
+        kw = {k_: v_ for k_, v_ in st_.items() if k_ != "env"}
+        if "env" in st_:
+            monkeypatch.setenv("LSRN_SVD_GESVD", "1")
+        else:
+            monkeypatch.delenv("LSRN_SVD_GESVD", raising=False)
+        x1, r1 = ctx.solve(X, b, p.m, p.n, **kw)
+        fresh = lsrn.Context()
+        x2, r2 = fresh.solve(X, b, p.m, p.n, **kw)
+        fresh.close()
+        assert r1["iters"] == r2["iters"] and torch.equal(x1, x2), st_
+
+
 def test_repeat_solves_bitwise(ctx):
     p = small("c2")
     x1, _ = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="lsqr")
