@@ -65,6 +65,11 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.first = 0
+
+    def mark(self):
+        """Start of the timed region: samples before it (sampler start-up) are dropped."""
+        self.first = len(self.lines)
 
     def start(self):
         try:
@@ -90,7 +95,8 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines[self.first:] or self.lines
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -224,9 +230,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the sampler starts before the timed region (nvidia-smi's start-up would
+    # otherwise stall the first timed solves) and keeps sampling through it
     clocks = ClockSampler(local)
-    barrier()
     clocks.start()
+    time.sleep(1.0)
+    barrier()
+    clocks.mark()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     reps, stats = [], []
@@ -237,11 +247,13 @@ def main():
         for _ in range(args.steps):
             x, rep = ctx.solve(X, b, m, n, **kw)
             reps.append(rep)
-            stats.append(ctx.stats())
         e1.record(stream)
     torch.cuda.profiler.stop()
     torch.cuda.nvtx.range_pop()
     barrier()
+    # per-kernel event times of the last timed step (read after the timed region: the
+    # library keeps the events, so no host work sits between the timed solves)
+    stats.append(ctx.stats())
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)

@@ -113,6 +113,7 @@ struct lsrn_ctx {
   bool profile = false;
   std::vector<cudaEvent_t> pass_ev;   // pairs around long-pass kernels
   int n_pass_ev = 0;
+  bool stats_pending = false;   // stats[1], [2], [4] not yet computed from the pass events
   double stats[8] = {};
   int launches = 0;
 };
@@ -961,8 +962,27 @@ lsrn_status lsrn_ctx_set_profiling(lsrn_ctx* c, int on) {
   return LSRN_OK;
 }
 
+}  // extern "C"
+namespace {
+extern int g_elapsed_err;
+double elapsed_s(cudaEvent_t a, cudaEvent_t b);
+}  // namespace
+extern "C" {
+
 lsrn_status lsrn_last_stats(lsrn_ctx* c, double* out, int cap) {
   if (!c || !out) return set_error(LSRN_EINVAL, "NULL argument");
+  if (c->stats_pending) {
+    c->stats_pending = false;
+    double lp = 0.0;
+    int nlp = 0;
+    for (int i = 0; i + 1 < c->n_pass_ev; i += 2) {
+      lp += elapsed_s(c->pass_ev[i], c->pass_ev[i + 1]) * 1e3;
+      ++nlp;
+    }
+    c->stats[1] = nlp ? lp / nlp : 0.0;
+    c->stats[2] = (double)g_elapsed_err;
+    c->stats[4] = (double)nlp;
+  }
   for (int i = 0; i < cap && i < 8; ++i) out[i] = c->stats[i];
   return LSRN_OK;
 }
@@ -1451,16 +1471,10 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     }
     // ---- stats
     c->stats[0] = elapsed_s(c->ev[1], c->ev[2]) * 1e3;
-    double lp = 0.0;
-    int nlp = 0;
-    for (int i = 0; i + 1 < c->n_pass_ev; i += 2) {
-      lp += elapsed_s(c->pass_ev[i], c->pass_ev[i + 1]) * 1e3;
-      ++nlp;
-    }
-    c->stats[1] = nlp ? lp / nlp : 0.0;
-    c->stats[2] = (double)g_elapsed_err;
+    // per-pass kernel times are read lazily by lsrn_last_stats (the events stay valid
+    // until the next call): no host work between back-to-back solves
+    c->stats_pending = true;
     c->stats[3] = (double)c->launches;
-    c->stats[4] = (double)nlp;
     // algorithmic bytes of one long pass: dense rows (8k + 16 per row);
     // CSR: the CSR stream (12 B per nonzero + 8 B rowptr + 16 B u per row) + the light CSC (12 B per entry)
     // (k <= 2048: single pass over the CSR, no CSC read in the iterations)
@@ -1523,6 +1537,9 @@ lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double 
     LSRN_REQUIRE(ar.off == 0 || (ws != nullptr && ws_bytes >= ar.off), LSRN_ENOMEM,
                  "workspace too small for the sketch: need " + std::to_string(ar.off) + " bytes");
     c->launches = 0;
+    c->n_pass_ev = 0;
+    c->stats_pending = false;
+    c->stats[1] = c->stats[4] = 0.0;
     sketch_stage(c, A, A, PL, seed, 0, ws, At);
     LSRN_CUDA(cudaGetLastError());
     c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
