@@ -133,8 +133,10 @@ lsrn_status lsrn_nccl_unique_id(void* id_out /* 128 bytes */);
 /* Create a context on the current CUDA device.
  *   stream : cudaStream_t (NULL = the legacy default stream) every call runs on;
  *   nranks, rank : process group (1, 0 for single GPU); nccl_id from rank 0's
- *   lsrn_nccl_unique_id, identical on all ranks (ignored when nranks == 1).
- * Creates the cuSOLVER handle and, for nranks > 1, the NCCL communicator. */
+ *   lsrn_nccl_unique_id, identical on all ranks (required for nranks > 1; with
+ *   nranks == 1 it is optional and, if given, builds a one-rank communicator so
+ *   the NCCL allreduce path runs on a single GPU -- a testing aid).
+ * Creates the cuSOLVER handle and the NCCL communicator (nranks > 1 or an id). */
 lsrn_status lsrn_ctx_create(lsrn_ctx** ctx, void* stream, int nranks, int rank,
                             const void* nccl_id);
 lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);

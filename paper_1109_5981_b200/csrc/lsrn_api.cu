@@ -530,7 +530,11 @@ SketchKey make_key(const lsrn_matrix* A_user, const Dims& d, uint64_t seed, cons
 }
 
 void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
+#ifdef LSRN_WITH_NCCL
+  if (c->comm == nullptr) return;       // one rank without a communicator
+#else
   if (c->nranks == 1) return;
+#endif
 #ifdef LSRN_WITH_NCCL
   ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, c->comm, c->stream);
   if (r != ncclSuccess) {
@@ -916,7 +920,9 @@ lsrn_status lsrn_ctx_create(lsrn_ctx** out, void* stream, int nranks, int rank, 
     LSRN_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (auto& e : c->chunk_ev) LSRN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     LSRN_CUDA(cudaEventCreateWithFlags(&c->io_ev, cudaEventDisableTiming));
-    if (nranks > 1) {
+    // nranks = 1 with an id: a one-rank communicator, so that the NCCL path (the
+    // allreduces, also inside the captured iteration graph) runs on a single GPU
+    if (nranks > 1 || nccl_id != nullptr) {
 #ifdef LSRN_WITH_NCCL
       LSRN_REQUIRE(nccl_id != nullptr, LSRN_EINVAL, "nccl_id required for nranks > 1");
       ncclUniqueId id;
