@@ -6,11 +6,13 @@ inputs: Gaussian sketch (K1+K2, DMMA) -> [NCCL allreduce] -> SVD (cuSOLVER,
 outside the hot path, reported separately) -> N -> fused LSQR (or CS)
 iterations (K5/K6/K8, one CUDA graph) -> x.
 
-Default workload (N = 1): BASELINE.json configs[1] = c2, dense 1e5 x 2000 rank
-1800, gamma = 2 (s = 4000), LSQR predictable count.  A (1.6 GB) is larger than
-L2 (126 MB), so no L2 flush is needed between steps.
+Default workload: BASELINE.json's largest single-GPU configuration, c5: dense
+1e6 x 1e4 (80 GB, column scales 1 -> 1e-5), gamma = 2 (s = 2e4), LSQR with the
+predictable Thm 4.5 count (96 iterations), row-sharded over N GPUs.  A is far
+larger than L2 (126 MB), so no L2 flush is needed between steps.  The other
+configs (--config c1..c4, t4) are parity-test cases and optional bench lines.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--solver lsqr|cs]
+  python bench.py [--gpus N --steps K --warmup W] [--config c5] [--solver lsqr|cs]
   python bench.py --impl reference ...     # the CPU oracle arm (rank 0 only)
 """
 import argparse
@@ -112,63 +114,143 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(cfg_name, solver, m_sample):
-    """The oracle (as it stands) on a bounded sample of the workload, extrapolated.
+def host_info():
+    """CPU model, cores and RAM of the host the oracle runs on (BASELINE.md's plan asks for them)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    ram = round(int(ln.split()[1]) / 1024 ** 2, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu": model, "nproc": os.cpu_count(), "ram_gb": ram}
 
-    Sample: the same recipe with m' = m_sample rows (same n, s, r/s); the oracle's
-    sketch and iteration stages scale linearly in m, the s x k SVD does not, so
-    T(full) = (t_sketch + t_iter) * m / m' + t_svd.
-    """
-    import numpy as np  # noqa: F401
-    from oracle.lsrn import solve as orc_solve
-    from synth.generate import CONFIGS, make_problem
-    cfg = CONFIGS[cfg_name]
-    if min(cfg["m"], cfg["n"]) > 4096:
-        return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                "unavailable": f"{cfg_name}: the oracle's SVD of the {2 * min(cfg['m'], cfg['n'])} x "
-                               f"{min(cfg['m'], cfg['n'])} sketch alone exceeds the bench's few-minute budget; "
-                               "shrinking the short dimension would change the problem"}
-    p = make_problem(cfg_name, m=m_sample, n=cfg["n"]) if cfg["m"] >= cfg["n"] else \
-        make_problem(cfg_name, m=cfg["m"], n=m_sample)
-    A = p.to_scipy() if p.kind == "csr" else p.dense_A().numpy()
-    t0 = time.perf_counter()
-    rep = orc_solve(A, p.b.numpy(), gamma=cfg["gamma"], lam=cfg["lam"], solver=solver, precise_g=False)
-    wall = time.perf_counter() - t0
-    L_full = max(cfg["m"], cfg["n"])
-    scale = L_full / m_sample
-    est = (rep["t_sketch"] + rep["t_iter"]) * scale + rep["t_svd"]
+
+def _blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
-        cores = os.cpu_count()
-    return {"value": est, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": (f"oracle solve ({solver}) of the {cfg_name} recipe at {m_sample} long-index rows "
-                       f"(1/{scale:.0f} of L={L_full}); stages sketch {rep['t_sketch']:.2f}s svd "
-                       f"{rep['t_svd']:.2f}s iter {rep['t_iter']:.2f}s; value = (sketch+iter)*{scale:.0f}+svd"),
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg_name, solver, sample_rows=1024, svd_k=2000, full_max=2.5e8):
+    """The oracle (as it stands, oracle/) timed on the box's host cores.
+
+    Small configs (k <= 2048 and L k <= 2.5e8: c1, c2) are solved IN FULL by the oracle
+    and the wall time is the value.  Larger ones are timed stage by stage on bounded
+    pieces of the same workload and scaled by the stage's operation count:
+      sketch  oracle.sketch.sketch on the first `sample_rows` long-index rows of the
+              config's own matrix (same recipe bytes), x L / rows      (2 s k L flops);
+      SVD     oracle.precond.factor on a Gaussian s' x k' sketch with k' = svd_k,
+              s' = ceil(gamma k'), x (k / k')^3                       (2 s k^2 + 11 k^3, s = gamma k);
+      iters   three passes of the oracle's operator pair (A N y, N^T A^T u) with the
+              row sample and a full k x k N, per pass = t_A L / rows + t_N, x passes.
+    """
+    import math
+    import numpy as np
+    from oracle import bounds
+    from oracle.lsrn import LongOperator
+    from oracle.lsrn import solve as orc_solve
+    from oracle.precond import factor
+    from oracle.sketch import plan as orc_plan
+    from oracle.sketch import sketch as orc_sketch
+    from synth.generate import CONFIGS, SKETCH_SEED, make_problem
+    cfg = CONFIGS[cfg_name]
+    m, n = cfg["m"], cfg["n"]
+    L, k = max(m, n), min(m, n)
+    t0 = time.perf_counter()
+    if k <= 2048 and L * k <= full_max:
+        p = make_problem(cfg_name)
+        A = p.to_scipy() if p.kind == "csr" else p.dense_A().numpy()
+        rep = orc_solve(A, p.b.numpy(), gamma=cfg["gamma"], lam=cfg["lam"], solver=solver)
+        wall = time.perf_counter() - t0
+        return {"value": rep["t_sketch"] + rep["t_svd"] + rep["t_iter"], "unit": UNIT, "cores": _blas_threads(),
+                "kind": "oracle", "host": host_info(),
+                "sample": (f"the full {cfg_name} solve ({solver}) by the oracle: sketch {rep['t_sketch']:.1f}s "
+                           f"svd {rep['t_svd']:.1f}s iterations {rep['t_iter']:.1f}s ({rep['iters']} it.)"),
+                "stages_s": {"sketch": rep["t_sketch"], "svd": rep["t_svd"], "iterations": rep["t_iter"]},
+                "sample_wall_s": wall}
+    pl = orc_plan(m, n, cfg["gamma"], cfg["lam"])
+    s = pl["s"]
+    rows = min(sample_rows, L)
+    p = make_problem(cfg_name, shard=(0, rows))
+    if p.kind == "csr":
+        import scipy.sparse as sp
+        X = sp.csr_matrix((p.val.numpy(), p.colind.numpy(), p.rowptr.numpy()), shape=(rows, k))
+    else:
+        X = p.X.numpy()
+    ta = time.perf_counter()
+    orc_sketch(X, s, SKETCH_SEED, pl["sigma_x"], 0.0)
+    t_sk = (time.perf_counter() - ta) * L / rows
+    kp = min(svd_k, k)
+    sp_ = int(math.ceil(cfg["gamma"] * kp))
+    G = np.random.default_rng(0).standard_normal((sp_, kp))
+    ta = time.perf_counter()
+    factor(G)
+    t_svd = (time.perf_counter() - ta) * (k / kp) ** 3
+    del G
+    r = k
+    alpha = bounds.default_alpha(s)
+    sl, su = bounds.sigma_bounds(s, r, alpha)
+    passes = bounds.lsqr_count(1e-14, r, s) + 1 if solver == "lsqr" else bounds.cs_passes(sl, su, 1e-14)
+    op = LongOperator(X, pl["sigma_x"], 0.0)
+    Nm = np.random.default_rng(1).standard_normal((k, k))
+    y, u = np.ones(k), np.ones(rows)
+    ta = time.perf_counter()
+    for _ in range(3):
+        op.PT(op.P(y) + u)
+    t_a = (time.perf_counter() - ta) / 3
+    ta = time.perf_counter()
+    for _ in range(3):
+        Nm.T @ (Nm @ y)
+    t_n = (time.perf_counter() - ta) / 3
+    del Nm
+    t_it = passes * (t_a * L / rows + t_n)
+    wall = time.perf_counter() - t0
+    return {"value": t_sk + t_svd + t_it, "unit": UNIT, "cores": _blas_threads(), "kind": "oracle",
+            "host": host_info(),
+            "sample": (f"oracle stages on pieces of {cfg_name} scaled by operation count: sketch of the first "
+                       f"{rows} of L={L} rows x{L / rows:.0f} ({t_sk:.0f}s); SVD (factor) of a {sp_}x{kp} sketch "
+                       f"x(k/{kp})^3 ({t_svd:.0f}s); {passes} passes of the operator pair, long side x{L / rows:.0f} "
+                       f"plus a {k}x{k} N ({t_it:.0f}s)"),
+            "stages_s": {"sketch": t_sk, "svd": t_svd, "iterations": t_it},
             "sample_wall_s": wall}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle arm (rank 0 only, N > 1 ranks exit 0)."""
+    """--impl reference: the CPU oracle arm (rank 0 only, N > 1 ranks exit 0).  Each step is
+    one bounded oracle measurement of the workload (cpu_baseline); value = the median."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    m_sample = args.ref_rows
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state; keep the contract's W for symmetry
     vals = []
     last = None
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        last = cpu_baseline(args.config, args.solver, m_sample)
+        last = cpu_baseline(args.config, args.solver, sample_rows=args.ref_rows, svd_k=args.ref_svd_k)
         vals.append(last["value"])
+    wall = time.perf_counter() - t0
     v = statistics.median(vals)
     cb = dict(last)
     cb["value"] = v
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "solver": args.solver, "sample_rows": m_sample},
+            "config": {"workload": args.config, "solver": args.solver},
+            "note": ("value = the oracle's time for the whole workload, estimated per step from a bounded "
+                     f"sample (cpu_baseline.sample); the {args.steps} samples took {wall:.0f} s of wall time"),
             "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -176,15 +258,18 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "t4"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5", "t4"])
     ap.add_argument("--solver", default="lsqr", choices=["lsqr", "cs"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-rows", type=int, default=4000)
-    ap.add_argument("--cpu-rows", type=int, default=10000)
+    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--ref-svd-k", type=int, default=1500)
+    ap.add_argument("--cpu-rows", type=int, default=1024)
+    ap.add_argument("--cpu-svd-k", type=int, default=2000)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -315,14 +400,24 @@ def main():
     # ---- end to end through the C ABI with HOST buffers (H2D of A, b and D2H of x inside)
     e2e = None
     if not args.no_e2e:
+        def pinned(t):          # straight into pinned host memory (c5's A is 80 GB: no pageable copy)
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
         if csr:
-            Xh = lsrn.Csr(p.rowptr.cpu().pin_memory(), p.colind.cpu().pin_memory(), p.val.cpu().pin_memory())
+            Xh = lsrn.Csr(pinned(p.rowptr), pinned(p.colind), pinned(p.val))
             h2d_A = int(p.rowptr.numel() * 8 + p.colind.numel() * 4 + p.val.numel() * 8)
         else:
-            Xh = X.cpu().pin_memory()
+            Xh = pinned(X)
             h2d_A = int(Xh.numel() * 8)
-        bh = b.cpu().pin_memory()
-        nsteps = min(3, args.steps)
+        bh = pinned(b)
+        # the device copy of A is not used by the end-to-end solves (they stage A from the
+        # host into the workspace): free it so the staging copy fits next to it
+        X = p.X = p.val = p.colind = p.rowptr = None
+        ctx._ws = None
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        nsteps = min(args.e2e_steps, args.steps)
         barrier()
         h0 = torch.cuda.Event(enable_timing=True)
         h1 = torch.cuda.Event(enable_timing=True)
@@ -347,7 +442,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(args.config, args.solver, args.cpu_rows)
+            cpu = cpu_baseline(args.config, args.solver, sample_rows=args.cpu_rows, svd_k=args.cpu_svd_k)
         except Exception as ex:  # report, do not fail the bench
             cpu = {"error": repr(ex)}
 

@@ -40,11 +40,16 @@
  *     allreduce of k+1 doubles.
  *   - Every call is asynchronous on the context stream except for one
  *     device->host read of the singular values after the SVD (to get r).
- *   - Outputs are written only when the call returns LSRN_OK.  A and b are
- *     never modified.  No C++ exception crosses the ABI; on error a
- *     thread-local message is available from lsrn_last_error().
+ *   - Outputs are written only when the call returns LSRN_OK: every argument,
+ *     shape and format check (and, for solves, the non-finite check) happens
+ *     before the first write to an output.  A fault inside an asynchronous
+ *     kernel surfaces as LSRN_ECUDA from this or a later call (standard CUDA
+ *     semantics); output contents are then undefined.  A and b are never
+ *     modified.  No C++ exception crosses the ABI; on error a thread-local
+ *     message is available from lsrn_last_error().
  *   - The library performs no device allocation: every buffer lives in the
- *     caller's workspace (size from lsrn_workspace_size).
+ *     caller's workspace (size from lsrn_workspace_size; any alignment -- the
+ *     library aligns its carve-up to 256 bytes inside the slack it asks for).
  */
 #ifndef LSRN_H
 #define LSRN_H
@@ -61,7 +66,7 @@ typedef enum {
   LSRN_EINVAL = -1,      /* gamma <= 1, lambda < 0, tol not in (0,1), alpha not in
                             (0, 1 - sqrt(r/s)), unknown kind/solver/mode, NULL pointer */
   LSRN_EDIM = -2,        /* inconsistent dims / shard / leading dimension */
-  LSRN_ENONFINITE = -3,  /* non-finite value met (reserved) */
+  LSRN_ENONFINITE = -3,  /* solves: NaN / Inf in b or in the sketch of A (so in A) */
   LSRN_ERANK0 = -4,      /* "sketch has numerical rank 0" */
   LSRN_ESVD = -5,        /* cuSOLVER failed */
   LSRN_ENOMEM = -6,      /* workspace smaller than lsrn_workspace_size() */
@@ -95,7 +100,9 @@ typedef struct {
   int64_t ld;            /* dense leading dimension (>= k) */
   const int64_t* rowptr; /* CSR: cnt + 1 entries */
   const int32_t* colind; /* CSR: column indices (global, in [0, n)) */
-  int64_t nnz;           /* CSR: rowptr[cnt] - rowptr[0] */
+  int64_t nnz;           /* CSR: must equal rowptr[cnt] - rowptr[0] (checked on the device
+                            copy of rowptr before any buffer is sized from it: LSRN_EDIM);
+                            cnt < 2^31 */
 } lsrn_matrix;
 
 typedef struct {
@@ -118,6 +125,11 @@ typedef struct {
   double sigma_L, sigma_U, alpha;   /* Thm 4.4 bounds used */
   double t_sketch, t_allreduce, t_svd, t_iter, t_total;  /* seconds (CUDA events) */
   double rnorm_est;      /* LSQR phibar estimate of ||Abar y - bbar|| (0 for CS) */
+  int32_t svd_used;      /* SVD method that produced N: LSRN_SVD_JW / _GESVD / _POLAR (a rejected
+                            polar result redone with gesvd reports LSRN_SVD_GESVD) */
+  int32_t collectives;   /* collective calls issued by this rank during the solve (sketch
+                            allreduce, non-finite flag, sigma / N broadcasts, per-pass reductions);
+                            0 with one rank and no communicator */
 } lsrn_report;
 
 /* Human-readable message of the last failing call on this thread ("" if none). */
@@ -131,15 +143,107 @@ const char* lsrn_version(void);
 lsrn_status lsrn_nccl_unique_id(void* id_out /* 128 bytes */);
 
 /* Create a context on the current CUDA device.
- *   stream : cudaStream_t (NULL = the legacy default stream) every call runs on;
+ *   stream : cudaStream_t every call is ordered on.  NULL means the legacy
+ *     default stream: the context then runs on a stream of its own (the
+ *     iteration loop is captured as a CUDA graph, which the legacy stream does
+ *     not allow) that waits for the legacy stream at the start of every call and
+ *     that the legacy stream waits for at its end, so the ordering seen by the
+ *     caller is that of the legacy stream;
  *   nranks, rank : process group (1, 0 for single GPU); nccl_id from rank 0's
- *   lsrn_nccl_unique_id, identical on all ranks (required for nranks > 1; with
- *   nranks == 1 it is optional and, if given, builds a one-rank communicator so
- *   the NCCL allreduce path runs on a single GPU -- a testing aid).
- * Creates the cuSOLVER handle and the NCCL communicator (nranks > 1 or an id). */
+ *   lsrn_nccl_unique_id, identical on all ranks.  For nranks > 1 either an
+ *   nccl_id (NCCL communicator, the normal multi-GPU path) or, afterwards,
+ *   lsrn_ctx_set_host_collectives is required.  With nranks == 1 an id is
+ *   optional and, if given, builds a one-rank communicator so the NCCL path runs
+ *   on a single GPU (a testing aid).
+ * Creates the cuSOLVER handle and the NCCL communicator (when an id is given). */
 lsrn_status lsrn_ctx_create(lsrn_ctx** ctx, void* stream, int nranks, int rank,
                             const void* nccl_id);
 lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
+
+/* Context options (lsrn_ctx_set_option).  Values are validated (LSRN_EINVAL on
+ * an unknown option or value).  The product options:
+ *   LSRN_OPT_PROFILING      0/1, as lsrn_ctx_set_profiling.
+ *   LSRN_OPT_SVD            how the SVD of the s x k sketch is computed (Alg. 1/2
+ *                           step 4; outside the hot path).  Every method
+ *                           is a true SVD (no Gram matrix):
+ *                           LSRN_SVD_AUTO (default): Jordan-Wielandt eigenproblem of R
+ *                             for k <= 16384, else LSRN_SVD_POLAR;
+ *                           LSRN_SVD_JW: geqrf, then syevdx on [[0, R^T], [R, 0]]
+ *                             (k <= 16384, cuSOLVER's symmetric-eigensolver limit);
+ *                           LSRN_SVD_GESVD: geqrf, then gesvd of R;
+ *                           LSRN_SVD_POLAR: geqrf, then gesvdp of R (polar
+ *                             decomposition + symmetric eigensolver, k x k).  Its
+ *                             result is accepted only when every sigma_i >= 1e-6
+ *                             sigma_1 (clearly full rank, where the polar route is
+ *                             accurate); otherwise the SVD is redone with gesvd, so
+ *                             the rank rule (C4) always sees exact
+ *                             singular values.
+ *   LSRN_OPT_GRAPH_REUSE    1 (default): reuse the captured iteration graph when
+ *                           nothing it holds by value changed; 0: capture every solve.
+ *   LSRN_OPT_HOSTIO_CHUNK_MB  first chunk (MB, default 32) of the streamed
+ *                           LSRN_HOST_IO copy of dense A.
+ *   LSRN_OPT_LSQR_SYNC      collectives per LSQR half-step with nranks > 1:
+ *                           0 (default) one -- the vector A^T u and ||u||^2 are
+ *                           reduced together (lazy normalisation);
+ *                           1 two -- ||u||^2 first, then the vector, the
+ *                           synchronisation count of textbook LSQR that the paper
+ *                           compares CS against.
+ *   LSRN_OPT_BCAST_N        nranks > 1: 1 (default) rank 0 computes the SVD and
+ *                           broadcasts sigma and N to every rank (the paper's
+ *                           MPI_Bcast), so all ranks iterate with the same
+ *                           N bit for bit; 0: every rank computes the SVD itself.
+ * Kernel-plan overrides (testing / tuning; -1 = the planner's shape-based
+ * choice).  Each selects among kernels computing the same quantities (results
+ * may differ by summation order only):
+ *   LSRN_OPT_SKETCH_KERNEL  0 warp-specialized DMMA kernel, 1 non-specialized kernel
+ *   LSRN_OPT_SKETCH_TILE    0: 64 x 256 tile, 1: 32 x 512 tile (default)
+ *   LSRN_OPT_SKETCH_MAXCL   cap on the G-sharing cluster size
+ *   LSRN_OPT_SKETCH_NSPLIT  split-K factor of the dense sketch (>= 1)
+ *   LSRN_OPT_ROWPASS_*      row-pass plan fields
+ *   LSRN_OPT_CSR_ROWDOT     CSR long pass: 0 heavy-dense + light-CSR, 8 rows per step;
+ *                           1 warp per row over the full CSR; 2 as 0 with 2 rows per step
+ *   LSRN_OPT_CSR_SKETCH     CSR sketch light part: 0 column-stationary (per nonzero),
+ *                           1 generate-once row-stationary slab */
+enum {
+  LSRN_OPT_PROFILING = 1,
+  LSRN_OPT_SVD = 2,
+  LSRN_OPT_GRAPH_REUSE = 3,
+  LSRN_OPT_HOSTIO_CHUNK_MB = 4,
+  LSRN_OPT_LSQR_SYNC = 5,
+  LSRN_OPT_BCAST_N = 6,
+  LSRN_OPT_SKETCH_KERNEL = 100,
+  LSRN_OPT_SKETCH_TILE = 101,
+  LSRN_OPT_SKETCH_MAXCL = 102,
+  LSRN_OPT_SKETCH_NSPLIT = 103,
+  LSRN_OPT_ROWPASS_KEEP = 110,
+  LSRN_OPT_ROWPASS_OCC = 111,
+  LSRN_OPT_ROWPASS_WIDE1 = 112,
+  LSRN_OPT_ROWPASS_WIDE2 = 113,
+  LSRN_OPT_ROWPASS_ASYNCX = 114,
+  LSRN_OPT_ROWPASS_NT = 115,
+  LSRN_OPT_ROWPASS_TR = 116,
+  LSRN_OPT_ROWPASS_BUDGET_KB = 117,
+  LSRN_OPT_ROWPASS_WIDE_SLICE = 118,
+  LSRN_OPT_CSR_ROWDOT = 120,
+  LSRN_OPT_CSR_SKETCH = 121
+};
+enum { LSRN_SVD_AUTO = 0, LSRN_SVD_JW = 1, LSRN_SVD_GESVD = 2, LSRN_SVD_POLAR = 3 };
+lsrn_status lsrn_ctx_set_option(lsrn_ctx* ctx, int option, int64_t value);
+
+/* Host-staged collectives for nranks > 1 without NCCL (any host transport: MPI,
+ * gloo, ... -- the paper's own cluster runs used MPI).  The library
+ * synchronises its stream, copies the operand to host memory, calls the
+ * callback and copies the result back:
+ *   allreduce(user, buf, count): in-place elementwise sum of buf[0..count) over
+ *     all ranks (every rank calls it in the same order with the same count);
+ *   bcast(user, buf, count, root): buf[0..count) of rank `root` to every rank.
+ * Callbacks return 0 on success (non-zero -> LSRN_ENCCL).  With host
+ * collectives the iteration loop is launched eagerly (a CUDA graph cannot hold
+ * the host round trips).  Only used when the context has no NCCL communicator. */
+typedef int (*lsrn_host_allreduce_fn)(void* user, double* buf, int64_t count);
+typedef int (*lsrn_host_bcast_fn)(void* user, double* buf, int64_t count, int root);
+lsrn_status lsrn_ctx_set_host_collectives(lsrn_ctx* ctx, lsrn_host_allreduce_fn allreduce, lsrn_host_bcast_fn bcast,
+                                          void* user);
 
 /* Record CUDA events around every long-pass (K6) launch of the next solves so
  * lsrn_last_stats reports its average duration (adds event nodes to the graph). */

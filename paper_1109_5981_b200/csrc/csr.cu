@@ -896,7 +896,7 @@ cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st) {
 cudaError_t launch_csr_rowdot_hl(const CsrRowdotArgs& a, cudaStream_t st) {
   const unsigned nb = (unsigned)a.nblocks;
   const int ND = a.ND > 0 ? a.ND : 32;
-  static const bool v8 = !std::getenv("LSRN_CSR_ROWDOT_HL2");   // tuning aid: two rows per step
+  const bool v8 = ovr().csr_rowdot != 2;   // override csr_rowdot = 2: two rows per step
   if (v8) {
     if (ND > 32)
       csr_rowdot_hl8_kernel<2><<<nb, THR, 0, st>>>(a.D, a.ldd, ND, a.nd, a.heavy_cols, a.lrowptr, a.lcol, a.lval, a.rows,

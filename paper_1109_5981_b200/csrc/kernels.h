@@ -6,6 +6,35 @@
 
 namespace lsrn {
 
+// ---- kernel-plan overrides (lsrn_ctx_set_option; testing / tuning aids)
+// Each field < 0 (or 0 where noted) leaves the planner's shape-based choice.
+// Every value selects among kernels that compute the same result; none changes
+// the arithmetic.  The context's overrides are installed for the duration of an
+// API call (OverrideScope) and read by the host-side planners through ovr().
+struct Overrides {
+  int sketch_kernel = -1;     // 0 warp-specialized DMMA (sketch_ws.cu), 1 non-specialized (sketch_dense.cu)
+  int sketch_tile = -1;       // 0: 64 x 256 tile, 1: 32 x 512 tile
+  int sketch_maxcl = -1;      // cap on the G-sharing cluster size along N
+  int sketch_nsplit = -1;     // split-K factor (>= 1)
+  int rowpass_keep = -1;      // 0/1: re-read / register-kept row tile
+  int rowpass_occ = -1;       // 1/2 CTAs per SM
+  int rowpass_wide1 = -1;     // 0 disables the single 512-thread CTA plan for 8192 < k <= 10240
+  int rowpass_wide2 = -1;     // 0 disables the 2 x 512-thread cluster plan for 16384 < k <= 20480
+  int rowpass_asyncx = -1;    // 0: cluster barrier per tile instead of the st.async exchange
+  int rowpass_nt = -1;        // 256 / 512 threads for cluster plans
+  int rowpass_tr = -1;        // wide rows: rows per tile (1 or 2)
+  int rowpass_budget_kb = -1; // shared-memory stage budget
+  int rowpass_wide_slice = -1;// wide rows: max columns per CTA slice
+  int csr_rowdot = -1;        // 0 heavy-dense + light-CSR 8 rows/step, 1 warp per row (full CSR), 2 hl 2 rows/step
+  int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch
+};
+const Overrides& ovr();
+struct OverrideScope {
+  explicit OverrideScope(const Overrides* o);
+  ~OverrideScope();
+  const Overrides* prev;
+};
+
 // ---- K2 dense sketch (sketch_dense.cu)
 struct SketchDenseArgs {
   const double* X;   // shard rows (row-major, leading dim ld)
@@ -21,8 +50,6 @@ size_t sketch_dense_smem();
 void sketch_tile_counts(int64_t s, int64_t k, int64_t* mtiles, int64_t* ntiles, int64_t* bk);
 cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st);   // picks v2 when supported
 bool sketch_ws_supported(const SketchDenseArgs& a);
-bool sketch_batch_supported(const SketchDenseArgs& a);
-cudaError_t launch_sketch_batch(const SketchDenseArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st);
 void sketch_ws_tile_dims(int64_t* bm, int64_t* bn, int64_t* bk);
 cudaError_t launch_sketch_finish(const double* part, int nsplit, int64_t split_stride, int64_t s, int64_t k,
@@ -219,5 +246,10 @@ cudaError_t launch_extract_r(const double* qr, int64_t ld, int64_t k, double* R,
 // Nt[c][j] = VT[c + j * k] / S[c], c < r, j < k  (Nt row-major r x k == N column-major)
 cudaError_t launch_form_nt(const double* VT, const double* S, int64_t k, int64_t r, double* Nt,
                            cudaStream_t st);
+
+// V column-major k x k (gesvdp): Nt[c][j] = V[j + c k] / S[c]
+cudaError_t launch_form_nt_v(const double* V, const double* S, int64_t k, int64_t r, double* Nt, cudaStream_t st);
+// flag[0] <- 1.0 if any of p[0..n) is not finite (never cleared here)
+cudaError_t launch_check_finite(const double* p, int64_t n, double* flag, cudaStream_t st);
 
 }  // namespace lsrn

@@ -63,13 +63,18 @@ lsrn_status set_error(lsrn_status code, const std::string& msg) {
   } while (0)
 
 // ------------------------------------------------------------------ workspace
+// Carve-up of the caller's workspace.  Offsets are aligned to 256 bytes of the
+// ABSOLUTE address (16-byte vector stores, TMA bulk copies): the base is rounded
+// up first, inside the 256 bytes of slack lsrn_workspace_size adds.
 struct Arena {
   char* base;
-  size_t off = 0;
-  explicit Arena(void* b) : base(static_cast<char*>(b)) {}
+  size_t pad = 0, off = 0;
+  explicit Arena(void* b) : base(static_cast<char*>(b)) {
+    if (base) pad = off = (256 - (reinterpret_cast<uintptr_t>(base) & 255)) & 255;
+  }
   template <typename T>
   T* take(size_t count) {
-    off = (off + 255) & ~size_t(255);
+    off = pad + ((off - pad + 255) & ~size_t(255));
     T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
     off += count * sizeof(T);
     return p;
@@ -88,6 +93,20 @@ struct Dims {
 
 struct lsrn_ctx {
   cudaStream_t stream = nullptr;
+  bool own_stream = false;            // created with stream == NULL: own stream joined to the legacy stream
+  cudaEvent_t join_ev[2] = {};
+  // options (lsrn_ctx_set_option)
+  Overrides ovr;
+  int svd_method = LSRN_SVD_AUTO;
+  bool graph_reuse = true;
+  double hostio_chunk_mb = 32.0;
+  int lsqr_sync = 0;
+  bool bcast_n = true;
+  // host-staged collectives (nranks > 1 without NCCL)
+  lsrn_host_allreduce_fn h_allreduce = nullptr;
+  lsrn_host_bcast_fn h_bcast = nullptr;
+  void* h_user = nullptr;
+  std::vector<double> h_buf;
   int nranks = 1, rank = 0, device = 0, nsm = 148;
   cusolverDnHandle_t solver = nullptr;
   cusolverDnParams_t params = nullptr;
@@ -107,6 +126,10 @@ struct lsrn_ctx {
   // the iteration graph is re-captured only when something it bakes in changed
   std::vector<int64_t> graph_key;
   int graph_launches = 0, graph_pass_ev = 0;
+  int svd_polar_fallbacks = 0;        // polar SVD results rejected (redone with gesvd)
+  int svd_used = 0;                   // method that produced N in the last solve
+  int collectives = 0;                // collective calls of the current call (reported)
+  int graph_collectives = 0;          // ... inside the cached iteration graph
   std::vector<char> gkey;
   // timing
   cudaEvent_t ev[8] = {};
@@ -119,6 +142,26 @@ struct lsrn_ctx {
 };
 
 namespace {
+
+// Every ABI call that touches the device runs inside a CallScope: the context's
+// kernel-plan overrides are installed for the planners (ovr()), and a context
+// created on the legacy stream joins its own stream to it at entry and exit.
+struct CallScope {
+  lsrn_ctx* c;
+  OverrideScope os;
+  explicit CallScope(lsrn_ctx* c_) : c(c_), os(c_ ? &c_->ovr : nullptr) {
+    if (c && c->own_stream) {
+      cudaEventRecord(c->join_ev[0], cudaStreamLegacy);
+      cudaStreamWaitEvent(c->stream, c->join_ev[0], 0);
+    }
+  }
+  ~CallScope() {
+    if (c && c->own_stream) {
+      cudaEventRecord(c->join_ev[1], c->stream);
+      cudaStreamWaitEvent(cudaStreamLegacy, c->join_ev[1], 0);
+    }
+  }
+};
 
 Dims make_dims(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, bool allow_partial = false) {
   LSRN_REQUIRE(A != nullptr, LSRN_EINVAL, "A is NULL");
@@ -154,6 +197,7 @@ Dims make_dims(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, b
     LSRN_REQUIRE((size_t)d.k <= csr_max_k(), LSRN_EUNSUPPORTED,
                  "CSR path supports min(m, n) <= " + std::to_string(csr_max_k()));
     LSRN_REQUIRE(A->nnz >= 0, LSRN_EDIM, "nnz must be >= 0");
+    LSRN_REQUIRE(d.cnt < ((int64_t)1 << 31), LSRN_EDIM, "CSR shard must have fewer than 2^31 rows (int32 row indices)");
     LSRN_REQUIRE(d.cnt == 0 || A->rowptr != nullptr, LSRN_EINVAL, "A->rowptr is NULL");
     LSRN_REQUIRE(A->nnz == 0 || (A->colind != nullptr && A->val != nullptr), LSRN_EINVAL,
                  "A->colind / A->val is NULL");
@@ -190,10 +234,7 @@ int choose_nsplit(int64_t s, int64_t k, int64_t rows, int nsm) {
   int64_t mt, nt, bk;
   sketch_tile_counts(s, k, &mt, &nt, &bk);
   const int64_t tiles = mt * nt;
-  if (const char* e = std::getenv("LSRN_SKETCH_NSPLIT")) {       // tuning aid
-    const int f = std::atoi(e);
-    if (f >= 1) return f;
-  }
+  if (ovr().sketch_nsplit >= 1) return ovr().sketch_nsplit;      // override (testing / tuning)
   // Split-K over rows for whole waves of CTAs: the smallest split whose last wave
   // is >= 99 % full, else the fullest (partials capped at 4 GB).  c2 (500 tiles of
   // 32 x 512): 2 splits (96.5 %) 58.1 ms, 13 splits (99.8 %) 56.5 ms
@@ -234,12 +275,8 @@ struct SketchWs {
 // 32 MB, x1.5 each, <= 16 chunks) so that the first sketch launch starts after a
 // short copy and later chunks (copied at ~55 GB/s, sketched at ~29 GB/s of A)
 // stay ahead of the sketch.  Returns the chunk count (1: no streaming).
-int stream_chunks(const Dims& d, int64_t ld, int64_t* r0) {
+int stream_chunks(const Dims& d, int64_t ld, double first_mb, int64_t* r0) {
   const double row_bytes = 8.0 * (double)ld;
-  static const double first_mb = [] {
-    const char* e = std::getenv("LSRN_HOSTIO_CHUNK_MB");   // test / tuning knob: first chunk size
-    return (e && std::atof(e) > 0.0) ? std::atof(e) : 32.0;
-  }();
   if (8.0 * (double)d.cnt * (double)ld < 2.0 * first_mb * 1024 * 1024 || d.cnt < 512) return 1;
   int n = 0;
   int64_t row = 0;
@@ -259,7 +296,7 @@ SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_fla
                      int64_t ld = 0) {
   SketchWs w{};
   if (host_stream && d.cnt > 0) {
-    w.nchunk = stream_chunks(d, ld, w.chunk_r0);
+    w.nchunk = stream_chunks(d, ld, c->hostio_chunk_mb, w.chunk_r0);
     if (w.nchunk > 1) {
       w.nsplit = 1;
       for (int i = 0; i < w.nchunk; ++i)
@@ -356,9 +393,17 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
   c->launches += 2;
   std::vector<int64_t> tot((size_t)d.k);
   int bad = 0;
+  int64_t rp_ends[2] = {0, 0};   // rowptr[0], rowptr[cnt]: nnz must match before buffers sized from it are filled
   LSRN_CUDA(cudaMemcpyAsync(tot.data(), w.total, sizeof(int64_t) * d.k, cudaMemcpyDeviceToHost, st));
   LSRN_CUDA(cudaMemcpyAsync(&bad, w.bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (d.cnt > 0) {
+    LSRN_CUDA(cudaMemcpyAsync(&rp_ends[0], A->rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaMemcpyAsync(&rp_ends[1], A->rowptr + d.cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  }
   LSRN_CUDA(cudaStreamSynchronize(st));
+  LSRN_REQUIRE(rp_ends[1] - rp_ends[0] == A->nnz, LSRN_EDIM,
+               "CSR nnz = " + std::to_string(A->nnz) + " but rowptr[cnt] - rowptr[0] = " +
+                   std::to_string(rp_ends[1] - rp_ends[0]));
   LSRN_REQUIRE(bad == 0, LSRN_EINVAL,
                std::string("CSR A is not canonical:") + ((bad & 1) ? " column index outside [0, n);" : "") +
                    ((bad & 2) ? " column indices not strictly increasing within a row;" : "") +
@@ -529,23 +574,73 @@ SketchKey make_key(const lsrn_matrix* A_user, const Dims& d, uint64_t seed, cons
   return k;
 }
 
-void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
+// Collectives: NCCL on the context stream (capturable into the
+// iteration graph), or host-staged through the caller's callbacks
+// (lsrn_ctx_set_host_collectives: stream sync, D2H, callback, H2D).
+bool host_collectives(const lsrn_ctx* c) {
 #ifdef LSRN_WITH_NCCL
-  if (c->comm == nullptr) return;       // one rank without a communicator
-#else
-  if (c->nranks == 1) return;
+  if (c->comm != nullptr) return false;
 #endif
-#ifdef LSRN_WITH_NCCL
-  ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, c->comm, c->stream);
-  if (r != ncclSuccess) {
-    g_last_error = std::string("NCCL allreduce failed: ") + ncclGetErrorString(r);
-    throw Fail{LSRN_ENCCL};
+  return c->nranks > 1 && c->h_allreduce != nullptr;
+}
+
+void host_stage(lsrn_ctx* c, double* buf, int64_t count, bool to_host) {
+  if (to_host) {
+    if ((int64_t)c->h_buf.size() < count) c->h_buf.resize((size_t)count);
+    LSRN_CUDA(cudaMemcpyAsync(c->h_buf.data(), buf, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    LSRN_CUDA(cudaStreamSynchronize(c->stream));
+  } else {
+    LSRN_CUDA(cudaMemcpyAsync(buf, c->h_buf.data(), sizeof(double) * count, cudaMemcpyHostToDevice, c->stream));
+    LSRN_CUDA(cudaStreamSynchronize(c->stream));   // h_buf is pageable and reused by the next collective
   }
-#else
-  (void)buf;
-  (void)count;
-  throw Fail{set_error(LSRN_ENCCL, "built without NCCL")};
+}
+
+void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
+  if (count <= 0) return;
+  if (c->nranks > 1 || host_collectives(c)
+#ifdef LSRN_WITH_NCCL
+      || c->comm != nullptr
 #endif
+  )
+    c->collectives++;
+#ifdef LSRN_WITH_NCCL
+  if (c->comm != nullptr) {
+    ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, c->comm, c->stream);
+    if (r != ncclSuccess) {
+      g_last_error = std::string("NCCL allreduce failed: ") + ncclGetErrorString(r);
+      throw Fail{LSRN_ENCCL};
+    }
+    return;
+  }
+#endif
+  if (c->nranks == 1) return;
+  LSRN_REQUIRE(c->h_allreduce != nullptr, LSRN_ENCCL,
+               "nranks > 1 needs an NCCL id at lsrn_ctx_create or lsrn_ctx_set_host_collectives");
+  host_stage(c, buf, count, true);
+  LSRN_REQUIRE(c->h_allreduce(c->h_user, c->h_buf.data(), count) == 0, LSRN_ENCCL, "host allreduce callback failed");
+  host_stage(c, buf, count, false);
+}
+
+void broadcast(lsrn_ctx* c, double* buf, int64_t count, int root) {
+  if (count <= 0) return;
+  if (c->nranks > 1) c->collectives++;
+#ifdef LSRN_WITH_NCCL
+  if (c->comm != nullptr) {
+    ncclResult_t r = ncclBroadcast(buf, buf, (size_t)count, ncclDouble, root, c->comm, c->stream);
+    if (r != ncclSuccess) {
+      g_last_error = std::string("NCCL broadcast failed: ") + ncclGetErrorString(r);
+      throw Fail{LSRN_ENCCL};
+    }
+    return;
+  }
+#endif
+  if (c->nranks == 1) return;
+  LSRN_REQUIRE(c->h_bcast != nullptr, LSRN_ENCCL,
+               "nranks > 1 needs an NCCL id at lsrn_ctx_create or lsrn_ctx_set_host_collectives");
+  if (c->rank == root) host_stage(c, buf, count, true);
+  else if ((int64_t)c->h_buf.size() < count) c->h_buf.resize((size_t)count);
+  LSRN_REQUIRE(c->h_bcast(c->h_user, c->h_buf.data(), count, root) == 0, LSRN_ENCCL, "host broadcast callback failed");
+  if (c->rank != root) host_stage(c, buf, count, false);
 }
 
 // ------------------------------------------------------------------ SVD
@@ -560,50 +655,82 @@ void allreduce(lsrn_ctx* c, double* buf, int64_t count) {
 // 1800): 80 ms vs 231 ms for cuSOLVER gesvd with equal sigma / subspace
 // accuracy (profiles/r01_svd_options.jsonl).
 // cuSOLVER's symmetric eigensolvers accept n <= 32768, so for k > 16384 (c4,
-// k = 2e4) the SVD of R falls back to cuSOLVER gesvd (slower, same accuracy).
+// k = 2e4) the default is the polar route: gesvdp of R (polar decomposition
+// R = U_p H, then the k x k symmetric eigenproblem of H = V Sigma V^T), 13.4 s
+// on a 2e4 x 2e4 R against 47.5-72 s for gesvd, with residual ||RV - US|| / ||R||
+// 7e-15 and orthogonality 9e-15 (profiles/r02_svd_options.jsonl).  The polar
+// route loses accuracy on (numerically) rank-deficient R (on c2's rank-1800 R
+// gesvdp put the 200 null singular values at ~1e-8 sigma_1, above the rank
+// threshold, profiles/r01_svd_options.jsonl), so its result is accepted only
+// when every sigma_i >= 1e-6 sigma_1 (clearly full rank, kappa <= 1e6); else the
+// SVD is redone with gesvd of R, which the rank rule can trust.
 constexpr int64_t kMaxJW = 32768;
+constexpr double kPolarMinRatio = 1e-6;
 
 struct SvdWs {
-  double *W1, *tau, *JW, *S, *Nt;   // JW: Jordan-Wielandt matrix, or [R | VT] in the gesvd fallback
+  double *W1, *tau, *JW, *S, *Sd, *Nt;   // JW: Jordan-Wielandt matrix, or [R | VT] (gesvd), or [R | U | V] (polar)
+  double* flag;                          // non-finite flag (1 double, allreduced)
   void* work;
   size_t work_bytes, host_bytes;
   int* info;
-  bool jw;
+  int method;                            // LSRN_SVD_JW / _GESVD / _POLAR (polar may fall back to gesvd)
 };
 
-// 64-bit cuSOLVER API: the c4 shape (s x k = 4e4 x 2e4, JW 4e4 x 4e4) needs
-// workspaces beyond 2^31 elements.
+// 64-bit cuSOLVER API: the c4 shape (s x k = 4e4 x 2e4) needs workspaces beyond
+// 2^31 elements.
 SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   SvdWs w{};
-  size_t d1 = 0, h1 = 0, d2 = 0, h2 = 0;
+  const int64_t k = d.k;
+  w.method = c->svd_method;
+  if (w.method == LSRN_SVD_AUTO) w.method = (2 * k <= kMaxJW) ? LSRN_SVD_JW : LSRN_SVD_POLAR;
+  LSRN_REQUIRE(!(w.method == LSRN_SVD_JW && 2 * k > kMaxJW), LSRN_EUNSUPPORTED,
+               "LSRN_SVD_JW needs min(m, n) <= 16384 (cuSOLVER symmetric eigensolver limit)");
+  size_t d1 = 0, h1 = 0, d2 = 0, h2 = 0, d3 = 0, h3 = 0;
   int64_t meig = 0;
   double vl = 0.0, vu = 0.0;
-  LSRN_SOLVER(cusolverDnXgeqrf_bufferSize(c->solver, c->params, d.s, d.k, CUDA_R_64F, nullptr, d.s, CUDA_R_64F,
+  LSRN_SOLVER(cusolverDnXgeqrf_bufferSize(c->solver, c->params, d.s, k, CUDA_R_64F, nullptr, d.s, CUDA_R_64F,
                                           nullptr, CUDA_R_64F, &d1, &h1));
-  w.jw = 2 * d.k <= kMaxJW && !std::getenv("LSRN_SVD_GESVD");   // tuning / test aid: force the fallback
-  if (w.jw) {
+  if (w.method == LSRN_SVD_JW) {
     LSRN_SOLVER(cusolverDnXsyevdx_bufferSize(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
-                                             CUBLAS_FILL_MODE_LOWER, 2 * d.k, CUDA_R_64F, nullptr, 2 * d.k, &vl, &vu,
-                                             d.k + 1, 2 * d.k, &meig, CUDA_R_64F, nullptr, CUDA_R_64F, &d2, &h2));
+                                             CUBLAS_FILL_MODE_LOWER, 2 * k, CUDA_R_64F, nullptr, 2 * k, &vl, &vu,
+                                             k + 1, 2 * k, &meig, CUDA_R_64F, nullptr, CUDA_R_64F, &d2, &h2));
   } else {
-    LSRN_SOLVER(cusolverDnXgesvd_bufferSize(c->solver, c->params, 'N', 'A', d.k, d.k, CUDA_R_64F, nullptr, d.k,
-                                            CUDA_R_64F, nullptr, CUDA_R_64F, nullptr, 1, CUDA_R_64F, nullptr, d.k,
+    LSRN_SOLVER(cusolverDnXgesvd_bufferSize(c->solver, c->params, 'N', 'A', k, k, CUDA_R_64F, nullptr, k,
+                                            CUDA_R_64F, nullptr, CUDA_R_64F, nullptr, 1, CUDA_R_64F, nullptr, k,
                                             CUDA_R_64F, &d2, &h2));
+    if (w.method == LSRN_SVD_POLAR)
+      LSRN_SOLVER(cusolverDnXgesvdp_bufferSize(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, 1, k, k, CUDA_R_64F,
+                                               nullptr, k, CUDA_R_64F, nullptr, CUDA_R_64F, nullptr, k, CUDA_R_64F,
+                                               nullptr, k, CUDA_R_64F, &d3, &h3));
   }
-  w.work_bytes = std::max(d1, d2);
-  w.host_bytes = std::max(h1, h2);
-  w.W1 = ar.take<double>((size_t)d.s * d.k);
-  w.tau = ar.take<double>((size_t)d.k);
-  w.JW = ar.take<double>((size_t)(w.jw ? 4 : 2) * d.k * d.k);
-  w.S = ar.take<double>((size_t)2 * d.k);
+  w.work_bytes = std::max({d1, d2, d3});
+  w.host_bytes = std::max({h1, h2, h3});
+  w.W1 = ar.take<double>((size_t)d.s * k);
+  w.tau = ar.take<double>((size_t)k);
+  const int nblk = w.method == LSRN_SVD_JW ? 4 : (w.method == LSRN_SVD_POLAR ? 3 : 2);
+  w.JW = ar.take<double>((size_t)nblk * k * k);
+  w.S = ar.take<double>((size_t)2 * k);
+  w.Sd = ar.take<double>((size_t)k);
+  w.flag = ar.take<double>(2);
   w.work = ar.take<char>(w.work_bytes + 16);
-  w.Nt = ar.take<double>((size_t)d.k * d.k);
+  w.Nt = ar.take<double>((size_t)k * k);
   w.info = ar.take<int>(4);
   return w;
 }
 
-// Returns r; S_host receives the k singular values, descending.
-int64_t run_svd(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, std::vector<double>& S_host) {
+// rank rule (reading C4): r = #{sigma_i > max(s, k) 2^-52 sigma_1}
+int64_t rank_of(const std::vector<double>& S, int64_t s, int64_t k) {
+  const double tau = (double)std::max(s, k) * std::ldexp(1.0, -52) * S[0];
+  int64_t r = 0;
+  if (S[0] > 0.0)
+    for (int64_t i = 0; i < k; ++i)
+      if (S[i] > tau) ++r;
+  return r;
+}
+
+// geqrf of the sketch + SVD of R on this rank.  S_host receives the k singular
+// values, descending; Nt (r x k, row-major = N column-major) is formed.  Returns r.
+int64_t svd_local(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, std::vector<double>& S_host) {
   cudaStream_t st = c->stream;
   const int64_t k = d.k;
   LSRN_CUDA(launch_transpose(At, d.s, k, w.W1, st));
@@ -611,46 +738,118 @@ int64_t run_svd(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, st
   if (c->host_ws.size() < w.host_bytes + 16) c->host_ws.resize(w.host_bytes + 16);
   LSRN_SOLVER(cusolverDnXgeqrf(c->solver, c->params, d.s, k, CUDA_R_64F, w.W1, d.s, CUDA_R_64F, w.tau, CUDA_R_64F,
                                w.work, w.work_bytes, c->host_ws.data(), w.host_bytes, w.info));
-  int64_t meig = k;
   std::vector<double> ev((size_t)k, 0.0);
   int info[2] = {0, 0};
-  double* R = w.JW;                 // gesvd fallback: R (k x k) then VT (k x k)
-  double* VT = w.JW + (size_t)k * k;
-  if (w.jw) {
-    LSRN_CUDA(launch_build_jw(w.W1, d.s, k, w.JW, st));
-    c->launches++;
-    double vl = 0.0, vu = 0.0;
-    LSRN_SOLVER(cusolverDnXsyevdx(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
-                                  CUBLAS_FILL_MODE_LOWER, 2 * k, CUDA_R_64F, w.JW, 2 * k, &vl, &vu, k + 1, 2 * k, &meig,
-                                  CUDA_R_64F, w.S, CUDA_R_64F, w.work, w.work_bytes, c->host_ws.data(), w.host_bytes,
-                                  w.info + 1));
-  } else {
+  auto fetch = [&](const double* sv, const char* what, int64_t meig) {
+    LSRN_CUDA(cudaMemcpyAsync(ev.data(), sv, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaMemcpyAsync(info, w.info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaStreamSynchronize(st));
+    LSRN_REQUIRE(info[0] == 0 && info[1] == 0 && meig == k, LSRN_ESVD,
+                 std::string("cuSOLVER geqrf/") + what + " info = " + std::to_string(info[0]) + "/" +
+                     std::to_string(info[1]) + ", values " + std::to_string(meig));
+  };
+  double* R = w.JW;                          // gesvd / polar: R (k x k) first
+  auto gesvd = [&]() {
+    double* VT = w.JW + (size_t)k * k;
     LSRN_CUDA(launch_extract_r(w.W1, d.s, k, R, st));
     c->launches++;
     LSRN_SOLVER(cusolverDnXgesvd(c->solver, c->params, 'N', 'A', k, k, CUDA_R_64F, R, k, CUDA_R_64F, w.S, CUDA_R_64F,
                                  nullptr, 1, CUDA_R_64F, VT, k, CUDA_R_64F, w.work, w.work_bytes, c->host_ws.data(),
                                  w.host_bytes, w.info + 1));
-  }
-  LSRN_CUDA(cudaMemcpyAsync(ev.data(), w.S, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-  LSRN_CUDA(cudaMemcpyAsync(info, w.info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
-  LSRN_CUDA(cudaStreamSynchronize(st));
-  LSRN_REQUIRE(info[0] == 0 && info[1] == 0 && meig == k, LSRN_ESVD,
-               std::string("cuSOLVER geqrf/") + (w.jw ? "syevdx" : "gesvd") + " info = " + std::to_string(info[0]) +
-                   "/" + std::to_string(info[1]) + ", eigenpairs " + std::to_string(meig));
-  S_host.assign((size_t)k, 0.0);
-  for (int64_t i = 0; i < k; ++i) S_host[i] = std::max(0.0, w.jw ? ev[k - 1 - i] : ev[i]);
-  // rank rule (reading C4): r = #{sigma_i > max(s, k) 2^-52 sigma_1}
-  const double tau = (double)std::max(d.s, k) * std::ldexp(1.0, -52) * S_host[0];
-  int64_t r = 0;
-  if (S_host[0] > 0.0)
-    for (int64_t i = 0; i < k; ++i)
-      if (S_host[i] > tau) ++r;
-  LSRN_REQUIRE(r > 0, LSRN_ERANK0, "sketch has numerical rank 0");
-  if (w.jw)
-    LSRN_CUDA(launch_form_nt_jw(w.JW, 2 * k, w.S, k, r, w.Nt, st));
-  else
+    fetch(w.S, "gesvd", k);
+    c->svd_used = LSRN_SVD_GESVD;
+    S_host.assign((size_t)k, 0.0);
+    for (int64_t i = 0; i < k; ++i) S_host[i] = std::max(0.0, ev[i]);
+    const int64_t r = rank_of(S_host, d.s, k);
+    LSRN_REQUIRE(r > 0, LSRN_ERANK0, "sketch has numerical rank 0");
     LSRN_CUDA(launch_form_nt(VT, w.S, k, r, w.Nt, st));
-  c->launches++;
+    c->launches++;
+    return r;
+  };
+  if (w.method == LSRN_SVD_JW) {
+    int64_t meig = k;
+    double vl = 0.0, vu = 0.0;
+    LSRN_CUDA(launch_build_jw(w.W1, d.s, k, w.JW, st));
+    c->launches++;
+    LSRN_SOLVER(cusolverDnXsyevdx(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                  CUBLAS_FILL_MODE_LOWER, 2 * k, CUDA_R_64F, w.JW, 2 * k, &vl, &vu, k + 1, 2 * k, &meig,
+                                  CUDA_R_64F, w.S, CUDA_R_64F, w.work, w.work_bytes, c->host_ws.data(), w.host_bytes,
+                                  w.info + 1));
+    fetch(w.S, "syevdx", meig);
+    c->svd_used = LSRN_SVD_JW;
+    S_host.assign((size_t)k, 0.0);
+    for (int64_t i = 0; i < k; ++i) S_host[i] = std::max(0.0, ev[k - 1 - i]);   // ascending eigenvalues
+    const int64_t r = rank_of(S_host, d.s, k);
+    LSRN_REQUIRE(r > 0, LSRN_ERANK0, "sketch has numerical rank 0");
+    LSRN_CUDA(launch_form_nt_jw(w.JW, 2 * k, w.S, k, r, w.Nt, st));
+    c->launches++;
+    return r;
+  }
+  if (w.method == LSRN_SVD_POLAR) {
+    double* Up = w.JW + (size_t)k * k;
+    double* Vp = w.JW + 2 * (size_t)k * k;
+    LSRN_CUDA(launch_extract_r(w.W1, d.s, k, R, st));
+    c->launches++;
+    double herr = 0.0;
+    LSRN_SOLVER(cusolverDnXgesvdp(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, 1, k, k, CUDA_R_64F, R, k,
+                                  CUDA_R_64F, w.S, CUDA_R_64F, Up, k, CUDA_R_64F, Vp, k, CUDA_R_64F, w.work,
+                                  w.work_bytes, c->host_ws.data(), w.host_bytes, w.info + 1, &herr));
+    LSRN_CUDA(cudaMemcpyAsync(ev.data(), w.S, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaMemcpyAsync(info, w.info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaStreamSynchronize(st));
+    LSRN_REQUIRE(info[0] == 0, LSRN_ESVD, "cuSOLVER geqrf info = " + std::to_string(info[0]));
+    bool ok = info[1] == 0 && ev[0] > 0.0 && std::isfinite(ev[0]);
+    for (int64_t i = 0; ok && i < k; ++i)
+      ok = std::isfinite(ev[i]) && ev[i] >= kPolarMinRatio * ev[0] && (i == 0 || ev[i] <= ev[i - 1]);
+    if (ok) {
+      c->svd_used = LSRN_SVD_POLAR;
+      S_host.assign(ev.begin(), ev.end());
+      LSRN_CUDA(launch_form_nt_v(Vp, w.S, k, k, w.Nt, st));   // r = k (sigma_k >= 1e-6 sigma_1 >> threshold)
+      c->launches++;
+      return rank_of(S_host, d.s, k);
+    }
+    c->svd_polar_fallbacks++;
+  }
+  return gesvd();
+}
+
+// Alg. 1/2 steps 4-5 across ranks.  With one rank, or LSRN_OPT_BCAST_N = 0, every
+// rank computes the SVD itself.  Otherwise rank 0 computes it and broadcasts sigma
+// (k doubles) and N^T (r x k) -- the paper's MPI_Bcast of N -- so every
+// rank iterates with the same N bit for bit and derives the same r from the same
+// sigma.  Returns r; S_host = sigma descending on every rank.
+int64_t run_svd(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, std::vector<double>& S_host) {
+  const int64_t k = d.k;
+  if (c->nranks == 1 || !c->bcast_n) return svd_local(c, d, At, w, S_host);
+  cudaStream_t st = c->stream;
+  int64_t r = 0;
+  if (c->rank == 0) {
+    // a failure on rank 0 is still broadcast (sigma = NaN: SVD failure, 0: rank 0) so
+    // that no rank waits for an N that never comes
+    bool failed = false;
+    Fail fail{LSRN_OK};
+    try {
+      r = svd_local(c, d, At, w, S_host);
+    } catch (const Fail& f) {
+      if (f.code == LSRN_ECUDA || f.code == LSRN_ENCCL) throw;
+      failed = true;
+      fail = f;
+      S_host.assign((size_t)k, f.code == LSRN_ERANK0 ? 0.0 : std::nan(""));
+    }
+    LSRN_CUDA(cudaMemcpyAsync(w.Sd, S_host.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+    broadcast(c, w.Sd, k, 0);
+    LSRN_CUDA(cudaStreamSynchronize(st));    // S_host is pageable: the copy must finish before it goes out of scope
+    if (failed) throw fail;
+  } else {
+    broadcast(c, w.Sd, k, 0);
+    S_host.assign((size_t)k, 0.0);
+    LSRN_CUDA(cudaMemcpyAsync(S_host.data(), w.Sd, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaStreamSynchronize(st));
+    LSRN_REQUIRE(!std::isnan(S_host[0]), LSRN_ESVD, "the SVD failed on rank 0");
+    r = rank_of(S_host, d.s, k);
+    LSRN_REQUIRE(r > 0, LSRN_ERANK0, "sketch has numerical rank 0");
+  }
+  broadcast(c, w.Nt, r * k, 0);
   return r;
 }
 
@@ -699,6 +898,16 @@ struct Pass {
   IterWs& w;
   RowPassPlan plong, pshort;
   const CsrWs* cw = nullptr;   // CSR A: rowdot + colgather instead of the dense row pass
+  bool two_sync = false;       // LSRN_OPT_LSQR_SYNC = 1: reduce ||z||^2, then the vector (two collectives)
+
+  void reduce_out(double* out) {
+    if (two_sync) {
+      allreduce(c, out + d.k, 1);
+      allreduce(c, out, d.k);
+    } else {
+      allreduce(c, out, d.k + 1);
+    }
+  }
 
   // CSR long pass (tall only): z <- c1 z + c2 A t ; out = [A^T z (+ I block) ; ||z||^2]
   void long_pass_csr(double* z, const double* t, const double* coef, double* acc, const int* done, double* out) {
@@ -744,10 +953,10 @@ struct Pass {
         c->n_pass_ev += 2;
       }
       c->launches += 2;
-      allreduce(c, out, d.k + 1);
+      reduce_out(out);
       return;
     }
-    const bool v1 = std::getenv("LSRN_CSR_ROWDOT_V1") != nullptr;   // tuning aid: warp per row, full CSR
+    const bool v1 = ovr().csr_rowdot == 1;   // override: warp per row over the full CSR
     a.nblocks = v1 ? csr_rowdot_blocks(c->nsm) : csr_rowdot_hl_blocks(c->nsm, cw->ND);
     a.D = cw->D;
     a.heavy_cols = cw->heavy_cols;
@@ -786,7 +995,7 @@ struct Pass {
       c->n_pass_ev += 2;
     }
     c->launches += 2;
-    allreduce(c, out, d.k + 1);
+    reduce_out(out);
   }
 
   // long pass over X: z <- c1 z + c2 sX X t (+ I block), out = [P^T z ; ||z||^2]
@@ -835,7 +1044,7 @@ struct Pass {
     r.done = done;
     LSRN_CUDA(launch_colreduce(r, st));
     c->launches++;
-    allreduce(c, out, d.k + 1);
+    reduce_out(out);
   }
 
   // short pass over N^T: v <- c1 v + c2 N^T wv, out = [N v ; ||v||^2]
@@ -911,6 +1120,12 @@ lsrn_status lsrn_ctx_create(lsrn_ctx** out, void* stream, int nranks, int rank, 
     c->stream = static_cast<cudaStream_t>(stream);
     c->nranks = nranks;
     c->rank = rank;
+    if (c->stream == nullptr || c->stream == cudaStreamLegacy) {
+      // the legacy stream cannot be captured: run on an own stream joined to it per call
+      LSRN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+      for (auto& e : c->join_ev) LSRN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     LSRN_CUDA(cudaGetDevice(&c->device));
     LSRN_CUDA(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device));
     LSRN_SOLVER(cusolverDnCreate(&c->solver));
@@ -922,9 +1137,9 @@ lsrn_status lsrn_ctx_create(lsrn_ctx** out, void* stream, int nranks, int rank, 
     LSRN_CUDA(cudaEventCreateWithFlags(&c->io_ev, cudaEventDisableTiming));
     // nranks = 1 with an id: a one-rank communicator, so that the NCCL path (the
     // allreduces, also inside the captured iteration graph) runs on a single GPU
-    if (nranks > 1 || nccl_id != nullptr) {
+    // nranks > 1 without an id: collectives come from lsrn_ctx_set_host_collectives
+    if (nccl_id != nullptr) {
 #ifdef LSRN_WITH_NCCL
-      LSRN_REQUIRE(nccl_id != nullptr, LSRN_EINVAL, "nccl_id required for nranks > 1");
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
       ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
@@ -953,6 +1168,12 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->io_ev) cudaEventDestroy(c->io_ev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (auto& e : c->join_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->own_stream && c->stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
   if (c->params) cusolverDnDestroyParams(c->params);
   if (c->solver) cusolverDnDestroy(c->solver);
 #ifdef LSRN_WITH_NCCL
@@ -965,6 +1186,51 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* c) {
 lsrn_status lsrn_ctx_set_profiling(lsrn_ctx* c, int on) {
   if (!c) return set_error(LSRN_EINVAL, "ctx is NULL");
   c->profile = on != 0;
+  return LSRN_OK;
+}
+
+lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
+  if (!c) return set_error(LSRN_EINVAL, "ctx is NULL");
+  auto bad = [&]() {
+    return set_error(LSRN_EINVAL, "invalid value " + std::to_string(value) + " for option " + std::to_string(option));
+  };
+  auto in = [&](int64_t lo, int64_t hi) { return value >= lo && value <= hi; };
+  Overrides& o = c->ovr;
+  switch (option) {
+    case LSRN_OPT_PROFILING: if (!in(0, 1)) return bad(); c->profile = value != 0; break;
+    case LSRN_OPT_SVD: if (!in(LSRN_SVD_AUTO, LSRN_SVD_POLAR)) return bad(); c->svd_method = (int)value; break;
+    case LSRN_OPT_GRAPH_REUSE: if (!in(0, 1)) return bad(); c->graph_reuse = value != 0; break;
+    case LSRN_OPT_HOSTIO_CHUNK_MB: if (!in(1, 1 << 20)) return bad(); c->hostio_chunk_mb = (double)value; break;
+    case LSRN_OPT_LSQR_SYNC: if (!in(0, 1)) return bad(); c->lsqr_sync = (int)value; break;
+    case LSRN_OPT_BCAST_N: if (!in(0, 1)) return bad(); c->bcast_n = value != 0; break;
+    case LSRN_OPT_SKETCH_KERNEL: if (!in(-1, 1)) return bad(); o.sketch_kernel = (int)value; break;
+    case LSRN_OPT_SKETCH_TILE: if (!in(-1, 1)) return bad(); o.sketch_tile = (int)value; break;
+    case LSRN_OPT_SKETCH_MAXCL: if (!in(-1, 4)) return bad(); o.sketch_maxcl = (int)value; break;
+    case LSRN_OPT_SKETCH_NSPLIT: if (!in(-1, 64) || value == 0) return bad(); o.sketch_nsplit = (int)value; break;
+    case LSRN_OPT_ROWPASS_KEEP: if (!in(-1, 1)) return bad(); o.rowpass_keep = (int)value; break;
+    case LSRN_OPT_ROWPASS_OCC: if (!in(-1, 2) || value == 0) return bad(); o.rowpass_occ = (int)value; break;
+    case LSRN_OPT_ROWPASS_WIDE1: if (!in(-1, 1)) return bad(); o.rowpass_wide1 = (int)value; break;
+    case LSRN_OPT_ROWPASS_WIDE2: if (!in(-1, 1)) return bad(); o.rowpass_wide2 = (int)value; break;
+    case LSRN_OPT_ROWPASS_ASYNCX: if (!in(-1, 1)) return bad(); o.rowpass_asyncx = (int)value; break;
+    case LSRN_OPT_ROWPASS_NT: if (!(value == -1 || value == 256 || value == 512)) return bad(); o.rowpass_nt = (int)value; break;
+    case LSRN_OPT_ROWPASS_TR: if (!in(-1, 2) || value == 0) return bad(); o.rowpass_tr = (int)value; break;
+    case LSRN_OPT_ROWPASS_BUDGET_KB: if (!(value == -1 || in(16, 227))) return bad(); o.rowpass_budget_kb = (int)value; break;
+    case LSRN_OPT_ROWPASS_WIDE_SLICE: if (!(value == -1 || in(512, 1 << 20))) return bad(); o.rowpass_wide_slice = (int)value; break;
+    case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 2)) return bad(); o.csr_rowdot = (int)value; break;
+    case LSRN_OPT_CSR_SKETCH: if (!in(-1, 1)) return bad(); o.csr_sketch = (int)value; break;
+    default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
+  }
+  return LSRN_OK;
+}
+
+lsrn_status lsrn_ctx_set_host_collectives(lsrn_ctx* c, lsrn_host_allreduce_fn allreduce_fn, lsrn_host_bcast_fn bcast_fn,
+                                          void* user) {
+  if (!c) return set_error(LSRN_EINVAL, "ctx is NULL");
+  if ((allreduce_fn == nullptr) != (bcast_fn == nullptr))
+    return set_error(LSRN_EINVAL, "give both host collectives (or neither, to unset them)");
+  c->h_allreduce = allreduce_fn;
+  c->h_bcast = bcast_fn;
+  c->h_user = user;
   return LSRN_OK;
 }
 
@@ -1121,6 +1387,7 @@ void sketch_stage(lsrn_ctx* c, const lsrn_matrix* A_user, const lsrn_matrix* A, 
     c->sketch_cached = true;
   }
   LSRN_CUDA(cudaEventRecord(c->ev[3], st));
+  LSRN_CUDA(cudaGetLastError());   // every check precedes the first write to the caller's At
   finish_sketch(c, d, seed, P.S0, At);
 }
 
@@ -1131,6 +1398,8 @@ lsrn_matrix stage_inputs(lsrn_ctx* c, const lsrn_matrix* A_in, const lsrn_opts* 
   cudaStream_t st = c->stream;
   const Dims& d = P.d;
   if (P.csr) {
+    LSRN_REQUIRE(d.cnt == 0 || A_in->rowptr[d.cnt] - A_in->rowptr[0] == A_in->nnz, LSRN_EDIM,
+                 "CSR nnz does not equal rowptr[cnt] - rowptr[0]");
     if (d.cnt > 0)
       LSRN_CUDA(cudaMemcpyAsync(P.rpstage, A_in->rowptr, sizeof(int64_t) * (d.cnt + 1), cudaMemcpyHostToDevice, st));
     if (A_in->nnz > 0) {
@@ -1182,6 +1451,7 @@ double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
 
 lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in, const lsrn_opts* o, void* ws,
                        size_t ws_bytes, double* x_out, lsrn_report* rep, Solver solver) {
+  CallScope scope(c);
   try {
     LSRN_REQUIRE(c != nullptr, LSRN_EINVAL, "ctx is NULL");
     validate_opts(o);
@@ -1200,6 +1470,8 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
                  "adaptive LSQR on a sharded wide problem is not supported (use predictable mode)");
     cudaStream_t st = c->stream;
     c->launches = 0;
+    c->collectives = 0;
+    c->svd_used = 0;
     c->n_pass_ev = 0;
     const double* b = b_in;
     double* x = x_out;
@@ -1219,6 +1491,20 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     lsrn_matrix A = stage_inputs(c, A_in, o, PL);
     // ---- sketch (Alg. 1/2 step 3; §5 blocks)
     sketch_stage(c, A_in, &A, PL, o->seed, o->flags, ws, At);
+    // ---- non-finite inputs: NaN / Inf anywhere in A reaches the sketch (every
+    // G[i, j] is non-zero), so the s x k sketch and b are checked; the flag is
+    // allreduced so that every rank takes the same decision
+    LSRN_CUDA(cudaMemsetAsync(vw.flag, 0, sizeof(double), st));
+    LSRN_CUDA(launch_check_finite(At, d.s * d.k, vw.flag, st));
+    LSRN_CUDA(launch_check_finite(b, d.tall ? d.cnt : d.m, vw.flag, st));
+    c->launches += 2;
+    allreduce(c, vw.flag, 1);
+    {
+      double nf = 0.0;
+      LSRN_CUDA(cudaMemcpyAsync(&nf, vw.flag, sizeof(double), cudaMemcpyDeviceToHost, st));
+      LSRN_CUDA(cudaStreamSynchronize(st));
+      LSRN_REQUIRE(nf == 0.0, LSRN_ENONFINITE, "non-finite value (NaN / Inf) in b or in the sketch of A");
+    }
     // ---- SVD + N (steps 4-5), outside the hot path
     std::vector<double> S;
     const int64_t r = run_svd(c, d, At, vw, S);
@@ -1239,6 +1525,8 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
 
     // ---- iteration plans
     Pass P{c, d, &A, vw.Nt, r, iw, {}, {}};
+    P.two_sync = solver == SOLVER_LSQR && c->lsqr_sync == 1;
+    const bool eager = host_collectives(c);   // host round trips cannot live in a graph
     if (PL.csr)
       P.cw = &PL.cw;
     else
@@ -1347,23 +1635,28 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
                             (const void*)PL.cw.lcol, (const void*)PL.cw.lval})
         kp(q);
     ki(A.ld), ki(A.nnz), ki(r), ki(iters_graph), ki(passes), ki(solver), ki(o->mode), ki(c->profile ? 1 : 0);
-    ki((int64_t)c->pass_ev.size()), ki(PL.csr ? 1 : 0), ki(std::getenv("LSRN_CSR_ROWDOT_V1") ? 1 : 0);
+    ki((int64_t)c->pass_ev.size()), ki(PL.csr ? 1 : 0), ki(ovr().csr_rowdot), ki(P.two_sync ? 1 : 0);
     if (PL.csr) ki(PL.cw.nd), ki(PL.cw.ND), ki(PL.cw.ldd), ki(PL.cw.nnz_light);
     ki(d.tall ? 1 : 0), ki(d.m), ki(d.n), ki(d.L), ki(d.k), ki(d.s), ki(d.cnt), ki(d.lo), kd(d.sx), kd(d.si);
     ki(d.has_I ? 1 : 0), ki(d.Lz);
     kplan(P.plong), kplan(P.pshort);
-    const bool graph_hit = c->gexec && c->graph_key == gk && !std::getenv("LSRN_GRAPH_RECAPTURE");   // test aid
+    const bool graph_hit = !eager && c->gexec && c->graph_key == gk && c->graph_reuse;
     cudaGraph_t graph = nullptr;
+    const int coll_before = c->collectives;
     if (graph_hit) {
       c->launches += c->graph_launches;
       c->n_pass_ev = c->graph_pass_ev;
+      c->collectives += c->graph_collectives;
     } else {
     c->graph_key.clear();
     if (c->gexec) {
       cudaGraphExecDestroy(c->gexec);
       c->gexec = nullptr;
     }
-    LSRN_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    if (!eager)
+      LSRN_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    else
+      LSRN_CUDA(cudaEventRecord(c->ev[6], st));   // eager loop: runs right here
     try {
       const double* one = iw.consts;        // {1, 0, 0}
       const double* load = iw.consts + 3;   // {0, 1, 0}
@@ -1419,21 +1712,28 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
         }
       }
     } catch (...) {
-      cudaGraph_t g2 = nullptr;
-      cudaStreamEndCapture(st, &g2);
-      if (g2) cudaGraphDestroy(g2);
+      if (!eager) {
+        cudaGraph_t g2 = nullptr;
+        cudaStreamEndCapture(st, &g2);
+        if (g2) cudaGraphDestroy(g2);
+      }
       throw;
     }
-    LSRN_CUDA(cudaStreamEndCapture(st, &graph));
-    LSRN_CUDA(cudaGraphInstantiate(&c->gexec, graph, 0));
-    cudaGraphDestroy(graph);
-    c->graph_key = gk;
-    c->graph_launches = c->launches - launches_before;
-    c->graph_pass_ev = c->n_pass_ev;
+    if (!eager) {
+      LSRN_CUDA(cudaStreamEndCapture(st, &graph));
+      LSRN_CUDA(cudaGraphInstantiate(&c->gexec, graph, 0));
+      cudaGraphDestroy(graph);
+      c->graph_key = gk;
+      c->graph_launches = c->launches - launches_before;
+      c->graph_pass_ev = c->n_pass_ev;
+      c->graph_collectives = c->collectives - coll_before;
+    }
     }   // capture
     const int graph_launches = c->launches - launches_before;
-    LSRN_CUDA(cudaEventRecord(c->ev[6], st));
-    LSRN_CUDA(cudaGraphLaunch(c->gexec, st));
+    if (!eager) {
+      LSRN_CUDA(cudaEventRecord(c->ev[6], st));
+      LSRN_CUDA(cudaGraphLaunch(c->gexec, st));
+    }
     LSRN_CUDA(cudaEventRecord(c->ev[7], st));
     // ---- recover x (Alg. 1 step 7 / §5 x = z / lambda)
     if (d.tall) {
@@ -1471,9 +1771,8 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
       rep->t_svd = elapsed_s(c->ev[3], c->ev[4]);
       rep->t_iter = elapsed_s(c->ev[6], c->ev[7]);
       rep->t_total = elapsed_s(c->ev[0], c->ev[7]);
-    }
-    if (std::getenv("LSRN_DEBUG_EVENTS")) {   // stage boundaries ev[0..7] (diagnostics)
-      for (int i = 0; i < 7; ++i) std::fprintf(stderr, "ev%d-ev%d %.3f ms\n", i, i + 1, elapsed_s(c->ev[i], c->ev[i + 1]) * 1e3);
+      rep->svd_used = c->svd_used;
+      rep->collectives = c->collectives;
     }
     // ---- stats
     c->stats[0] = elapsed_s(c->ev[1], c->ev[2]) * 1e3;
@@ -1486,7 +1785,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     // (k <= 2048: single pass over the CSR, no CSC read in the iterations)
     // k > 2048: the heavy block D (8 B per heavy entry, nd per row) + the light CSR (12 B per entry,
     // 8 B row pointer) + u (16 B per row) + the light CSC (12 B per entry)
-    const bool hl = d.k > csr_rowdot_all_max_k() && !std::getenv("LSRN_CSR_ROWDOT_V1");
+    const bool hl = d.k > csr_rowdot_all_max_k() && ovr().csr_rowdot != 1;
     const double csc_bytes = d.k <= csr_rowdot_all_max_k() ? 0.0 : 12.0 * (double)PL.cw.nnz_light;
     const double nnz_b = hl ? 8.0 * (double)PL.cw.nd * (double)d.cnt + 12.0 * (double)PL.cw.nnz_light
                             : 12.0 * (double)A_in->nnz;
@@ -1515,6 +1814,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
 extern "C" {
 
 lsrn_status lsrn_workspace_size(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, size_t* bytes) {
+  CallScope scope(c);
   try {
     LSRN_REQUIRE(c != nullptr && bytes != nullptr, LSRN_EINVAL, "NULL argument");
     validate_opts(o);
@@ -1529,6 +1829,7 @@ lsrn_status lsrn_workspace_size(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_op
 
 lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double lambda, uint64_t seed, void* ws,
                         size_t ws_bytes, double* At, int64_t* s_out) {
+  CallScope scope(c);
   try {
     LSRN_REQUIRE(c != nullptr && At != nullptr && A != nullptr, LSRN_EINVAL, "ctx, A or At is NULL");
     lsrn_opts o{};
@@ -1546,8 +1847,7 @@ lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double 
     c->n_pass_ev = 0;
     c->stats_pending = false;
     c->stats[1] = c->stats[4] = 0.0;
-    sketch_stage(c, A, A, PL, seed, 0, ws, At);
-    LSRN_CUDA(cudaGetLastError());
+    sketch_stage(c, A, A, PL, seed, 0, ws, At);   // At is written by its last step only
     c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
     if (s_out) *s_out = d.s;
     return LSRN_OK;
@@ -1568,6 +1868,7 @@ lsrn_status lsrn_solve_cs(lsrn_ctx* c, const lsrn_matrix* A, const double* b, co
 
 lsrn_status lsrn_debug_box_muller(lsrn_ctx* c, const uint32_t* words, int64_t count, int mode, double* out) {
   if (!c || !words || !out) return set_error(LSRN_EINVAL, "NULL argument");
+  CallScope scope(c);
   if (mode != 0 && mode != 1) return set_error(LSRN_EINVAL, "mode must be 0 (table) or 1 (libm)");
   if (count <= 0) return LSRN_OK;
   cudaError_t e = launch_debug_box_muller(words, count, mode, out, c->stream);
@@ -1580,6 +1881,7 @@ lsrn_status lsrn_debug_rowpass(lsrn_ctx* c, const double* Y, int64_t R, int64_t 
                                double* ms_out) {
   if (!c || !Y || !t || !coef || !z || !out) return set_error(LSRN_EINVAL, "NULL argument");
   if (R <= 0 || C <= 0 || ld < C || reps < 1) return set_error(LSRN_EDIM, "need R, C > 0, ld >= C, reps >= 1");
+  CallScope scope(c);
   cudaStream_t st = c->stream;
   const RowPassPlan pl = plan_rowpass(R, C, ld, Y, c->nsm);
   double *wpart = nullptr, *npart = nullptr, *blockpart = nullptr;
@@ -1641,6 +1943,7 @@ lsrn_status lsrn_debug_gaussian(lsrn_ctx* c, uint64_t seed, const int64_t* rows,
                                 double* out) {
   if (!c || !rows || !cols || !out) return set_error(LSRN_EINVAL, "NULL argument");
   if (count <= 0) return LSRN_OK;
+  CallScope scope(c);
   cudaError_t e = launch_debug_gaussian(seed, rows, cols, count, out, c->stream);
   if (e != cudaSuccess) return set_error(LSRN_ECUDA, cudaGetErrorString(e));
   return LSRN_OK;

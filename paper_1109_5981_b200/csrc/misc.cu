@@ -5,6 +5,14 @@
 
 namespace lsrn {
 
+namespace {
+thread_local const Overrides* g_ovr = nullptr;
+const Overrides kNoOverrides{};
+}  // namespace
+const Overrides& ovr() { return g_ovr ? *g_ovr : kNoOverrides; }
+OverrideScope::OverrideScope(const Overrides* o) : prev(g_ovr) { g_ovr = o; }
+OverrideScope::~OverrideScope() { g_ovr = prev; }
+
 static unsigned grid_for(int64_t n, int threads = 256, int64_t cap = 148 * 16) {
   int64_t b = (n + threads - 1) / threads;
   if (b > cap) b = cap;
@@ -136,6 +144,34 @@ cudaError_t launch_extract_r(const double* qr, int64_t ld, int64_t k, double* R,
 cudaError_t launch_form_nt(const double* VT, const double* S, int64_t k, int64_t r, double* Nt, cudaStream_t st) {
   dim3 grid((unsigned)((k + 31) / 32), (unsigned)((r + 31) / 32));
   form_nt_kernel<<<grid, dim3(32, 8), 0, st>>>(VT, S, k, r, Nt);
+  return cudaGetLastError();
+}
+
+// V column-major k x k (column c = right singular vector c, as gesvdp returns it):
+// Nt[c][j] = V[j + c k] / S[c] -- row c of Nt is column c of V, scaled.
+__global__ void form_nt_v_kernel(const double* __restrict__ V, const double* __restrict__ S, int64_t k, int64_t r,
+                                 double* __restrict__ Nt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < r * k; e += (int64_t)gridDim.x * blockDim.x)
+    Nt[e] = V[e] / S[e / k];
+}
+
+cudaError_t launch_form_nt_v(const double* V, const double* S, int64_t k, int64_t r, double* Nt, cudaStream_t st) {
+  form_nt_v_kernel<<<grid_for(r * k), 256, 0, st>>>(V, S, k, r, Nt);
+  return cudaGetLastError();
+}
+
+// flag[0] = 1.0 if any p[i] (i < n) is NaN or +-Inf (flag is only ever set, never
+// cleared, so several arrays can be checked into one flag).
+__global__ void check_finite_kernel(const double* __restrict__ p, int64_t n, double* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(p[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) flag[0] = 1.0;
+}
+
+cudaError_t launch_check_finite(const double* p, int64_t n, double* flag, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  check_finite_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(p, n, flag);
   return cudaGetLastError();
 }
 

@@ -392,8 +392,8 @@ constexpr size_t kStageBudget = 192 * 1024;
 constexpr size_t kWideBudget = 224 * 1024;   // + ~2.5 KB static shared memory <= 227 KB
 }  // namespace
 
-// Tuning aids (env): LSRN_ROWPASS_OCC=1 (one CTA per SM, the whole stage budget),
-// LSRN_ROWPASS_KEEP=0/1 (force re-read / register tile).
+// Overrides (lsrn_ctx_set_option): rowpass_occ = 1 (one CTA per SM, the whole
+// stage budget), rowpass_keep = 0/1 (force re-read / register tile), ...
 bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, RowPassPlan* p) {
   // 16-byte aligned rows and an even slice width: every bulk copy is a multiple of 16 bytes
   if (C <= 0 || (C & 1) || (ld & 1) || (reinterpret_cast<uintptr_t>(Y) & 15)) return false;
@@ -404,8 +404,8 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   // up to 8192 doubles, one CTA per SM (deeper rings), asynchronous partial-dot exchange.
   const bool wide = C > kMaxSlice;
   int64_t max_slice = wide ? 2 * kMaxSlice : kMaxSlice;
-  if (const char* e = std::getenv("LSRN_ROWPASS_WIDE_SLICE"))   // tuning aid
-    if (wide) max_slice = std::max<int64_t>(512, std::atoll(e));
+  const Overrides& ov = ovr();
+  if (ov.rowpass_wide_slice > 0 && wide) max_slice = std::max<int64_t>(512, ov.rowpass_wide_slice);
   auto vpt_for = [](int64_t q) {
     int v = 1;
     while (512 * v < q) v = (v < 8) ? v * 2 : v + 4;              // 1, 2, 4, 8, 12, 16
@@ -424,18 +424,16 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   // threads x 10 column pairs (slices up to 10240 doubles), one CTA per SM, two
   // 1-row stages: 2e4 x 2e4 3.09 -> 3.99 TB/s (profiles/r01_rowpass_shape.log);
   // below 16384 the 256-thread 2-CTA plan is faster (16000: 5.77 vs 4.91 TB/s).
-  // LSRN_ROWPASS_WIDE2=0 (tuning aid) disables it.
+  // The rowpass_wide2 = 0 override disables it.
   // Rows of 8192-10240 doubles (c5, k = 1e4): ONE CTA of 512 threads x 10 column
   // pairs per row, no cluster and no partial-dot exchange, two 1-row stages (80 KB
   // each): 125000 x 1e4 4.44 -> 5.80 TB/s against the 2-CTA cluster pass
-  // (profiles/r01_rowpass_shape.log).  LSRN_ROWPASS_WIDE1=0 (tuning aid) disables it.
-  const char* w1env = std::getenv("LSRN_ROWPASS_WIDE1");
-  const bool wide1 = wide && C > 8192 && C <= 10240 && !(w1env && std::atoi(w1env) == 0);
+  // (profiles/r01_rowpass_shape.log).  The rowpass_wide1 = 0 override disables it.
+  const bool wide1 = wide && C > 8192 && C <= 10240 && ov.rowpass_wide1 != 0;
   if (wide1) cl = 1;
-  const char* w2env = std::getenv("LSRN_ROWPASS_WIDE2");
-  const bool wide2 = wide && C > 16384 && C <= 20480 && !(w2env && std::atoi(w2env) == 0);
+  const bool wide2 = wide && C > 16384 && C <= 20480 && ov.rowpass_wide2 != 0;
   if (wide2) cl = 2;
-  if (wide && C > 10240 && !wide2 && !std::getenv("LSRN_ROWPASS_WIDE_SLICE")) {
+  if (wide && C > 10240 && !wide2 && ov.rowpass_wide_slice <= 0) {
     for (int n = cl; n <= 16; ++n) {
       const int64_t q = slice(n);
       if ((double)q >= 0.9 * 512.0 * vpt_for(q)) {
@@ -453,33 +451,32 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   // reduction, exchange, stage release) is latency-bound, and the second CTA
   // hides it: c5 4.05 -> 4.43 TB/s (profiles/r01_rowpass_tune_c5c.jsonl) against
   // one CTA per SM with 4-5 stages.  Otherwise one CTA with (almost) all of shared
-  // memory so that >= 3 stages stay in flight.  Tuning aids: LSRN_ROWPASS_OCC,
-  // LSRN_ROWPASS_BUDGET_KB.
+  // memory so that >= 3 stages stay in flight.  Overrides: rowpass_occ,
+  // rowpass_budget_kb.
   int occ = 2;
   if (wide && 2 * (size_t)cq * 8 > kWideBudget / 2) occ = 1;
   if (wide2 || wide1) occ = 1;
-  if (const char* e = std::getenv("LSRN_ROWPASS_OCC")) occ = std::atoi(e) == 1 ? 1 : 2;
+  if (ov.rowpass_occ >= 1) occ = ov.rowpass_occ == 1 ? 1 : 2;
   size_t budget = wide ? (occ == 1 ? kWideBudget : kWideBudget / 2) : kStageBudget / occ;
-  if (const char* e = std::getenv("LSRN_ROWPASS_BUDGET_KB")) budget = (size_t)std::atoi(e) * 1024;
+  if (ov.rowpass_budget_kb > 0) budget = (size_t)ov.rowpass_budget_kb * 1024;
   int tr = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(budget / 3) / (cq * 8)));
   int t2 = 1;
   while (t2 * 2 <= tr) t2 *= 2;
   tr = t2;
-  if (const char* e = std::getenv("LSRN_ROWPASS_TR"))            // tuning aid (wide rows: 1 or 2)
-    if (wide) tr = std::atoi(e) == 2 ? 2 : 1;
+  if (ov.rowpass_tr >= 1 && wide) tr = ov.rowpass_tr == 2 ? 2 : 1;   // wide rows: 1 or 2
   const size_t stage_bytes = (size_t)tr * cq * 8;
   int nst = (int)std::min<size_t>(kMaxStages, budget / stage_bytes);
   // one stage being reduced, one waiting for its refill, >= 1 in flight; with two
   // CTAs per SM on wide rows (tuning aid) two stages each still keep two in flight per SM
   if (nst < 3 && !(wide && (occ == 2 || wide2 || wide1 || tr == 2) && nst == 2)) return false;
   bool keep = vpt * tr <= (occ == 2 ? 4 : 16);
-  if (const char* e = std::getenv("LSRN_ROWPASS_KEEP")) keep = std::atoi(e) != 0 && vpt * tr <= 16;
+  if (ov.rowpass_keep >= 0) keep = ov.rowpass_keep != 0 && vpt * tr <= 16;
   p->keep = keep ? 1 : 0;
   p->occ = occ;
   p->nt = 256;
-  // wide rows: pipelined asynchronous partial-dot exchange (LSRN_ROWPASS_ASYNCX=0: cluster barrier per tile)
+  // wide rows: pipelined asynchronous partial-dot exchange (override rowpass_asyncx = 0: cluster barrier per tile)
   p->async_x = 1;
-  if (const char* e = std::getenv("LSRN_ROWPASS_ASYNCX")) p->async_x = std::atoi(e) != 0;
+  if (ov.rowpass_asyncx >= 0) p->async_x = ov.rowpass_asyncx != 0;
   int nclusters = (nsm * occ) / cl;
   if (nclusters < 1) nclusters = 1;
   const int64_t tiles = (R + tr - 1) / tr;
@@ -493,7 +490,7 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   p->bulk = 1;
   p->cq = cq;
   p->nst = nst;
-  // Wide rows, tuning aid LSRN_ROWPASS_NT=512: 16 warps per CTA.  The c5 pass is
+  // Wide rows, override rowpass_nt = 512: 16 warps per CTA.  The c5 pass is
   // latency-bound (ncu: 12.5 % warps active; stalls on fixed-latency dependencies,
   // shared loads and the per-tile barrier, profiles/r01_ncu_c5_cluster.txt), but
   // neither 512 threads (3.76 TB/s) nor an mbarrier-only tile flow without the two
@@ -511,7 +508,7 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   }
   if (cl > 1 && p->async_x) {
     int nt = 256;
-    if (const char* e = std::getenv("LSRN_ROWPASS_NT")) nt = std::atoi(e) == 512 ? 512 : 256;
+    if (ov.rowpass_nt > 0) nt = ov.rowpass_nt == 512 ? 512 : 256;
     if (nt == 512) {
       int v = 4;
       while (v < 8 && 1024 * v < cq) v += 2;                     // 4, 6, 8 pairs per thread

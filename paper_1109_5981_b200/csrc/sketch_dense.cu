@@ -238,15 +238,10 @@ size_t sketch_dense_smem() { return sk::SMEM_BYTES; }
 
 cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st) {
   using namespace sk;
-  // Variant (tuning aid LSRN_SKETCH_IMPL = ws | batch | v1; LSRN_SKETCH_V1=1 = v1):
-  // ws = warp-specialized (sketch_ws.cu), batch = batched RNG phases (sketch_batch.cu),
-  // v1 = this kernel (also the path for unaligned X / odd ld).
-  const char* impl = std::getenv("LSRN_SKETCH_IMPL");
-  const char* v1 = std::getenv("LSRN_SKETCH_V1");
-  std::string which = impl ? impl : "ws";
-  if (v1 && v1[0] == '1') which = "v1";
-  if (which == "batch" && sketch_batch_supported(a)) return launch_sketch_batch(a, st);
-  if (which == "ws" && sketch_ws_supported(a)) return launch_sketch_ws(a, st);
+  // Variant: the warp-specialized kernel (sketch_ws.cu) whenever its alignment
+  // needs hold, else this kernel (odd ld / odd k / unaligned X); override
+  // sketch_kernel = 1 forces this kernel (tests compare both).
+  if (ovr().sketch_kernel != 1 && sketch_ws_supported(a)) return launch_sketch_ws(a, st);
   dim3 grid((unsigned)((a.k + BN - 1) / BN), (unsigned)((a.s + BM - 1) / BM), (unsigned)a.nsplit);
   const bool vec2 = (a.ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
   cudaError_t e;

@@ -112,7 +112,7 @@ template <class C, int CL>
 __global__ void __launch_bounds__(ws::THREADS, 1)
 sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
                  uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride,
-                 int diag, int accumulate) {
+                 int accumulate) {
   using namespace ws;
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, NSX = C::NSX, NSG = C::NSG;
   constexpr int A_LD = C::A_LD, G_LD = C::G_LD, X_STAGE = C::X_STAGE, G_STAGE = C::G_STAGE;
@@ -200,7 +200,7 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
         const int p = lane + 32 * t;
         const int qp = row0 / 2 + p / BK, kk = p % BK;
         z[t][0] = z[t][1] = 0.0;
-        if ((PAIRS_W % 32 == 0 || p < PAIRS_W) && kk < nrow && !(diag & 1))
+        if ((PAIRS_W % 32 == 0 || p < PAIRS_W) && kk < nrow)
           gaussian_pair(key, (uint64_t)(m0 / 2 + qp), (uint64_t)(jbase + kk), bmT, z[t][0], z[t][1]);
       }
 #pragma unroll
@@ -322,14 +322,11 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // LSRN_SKETCH_DIAG (timing experiments only, results are wrong): 1 = skip the RNG
-  int diag = 0;
-  if (const char* e = std::getenv("LSRN_SKETCH_DIAG")) diag = std::atoi(e);
   return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<C, CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
-                            a.rows_per_split, a.out, a.out_split_stride, diag, a.accumulate);
+                            a.rows_per_split, a.out, a.out_split_stride, a.accumulate);
 }
 
-// Tile shape (LSRN_SKETCH_TILE, tuning aid).  Measured on c2 (1e5 x 2000,
+// Tile shape (override sketch_tile).  Measured on c2 (1e5 x 2000,
 // profiles/r01_sketch_tile.jsonl), ms: 64 x 256 (BK 16, 4 + 4 stages) CL 1/2 ->
 // 65.7 / 60.3; 32 x 512 (BK 16, 3 X stages) CL 1/2 -> 58.1 / 61.1; 32 x 512 with
 // BK 8 (5 X stages) CL 1/2 -> 70.2 / 74.9; 16 x 1024 (BK 8, 3 X stages) -> 69.6
@@ -339,10 +336,7 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, cudaStream_t st) {
 using Tile0 = ws::Cfg<64, 256, 16, 4, 4>;
 using Tile1 = ws::Cfg<32, 512, 16, 3, 4>;
 
-int sketch_ws_tile() {   // read at every launch (tests switch it)
-  const char* e = std::getenv("LSRN_SKETCH_TILE");
-  return e ? std::atoi(e) : 1;
-}
+int sketch_ws_tile() { return ovr().sketch_tile == 0 ? 0 : 1; }
 
 void sketch_ws_tile_dims(int64_t* bm, int64_t* bn, int64_t* bk) {
   if (sketch_ws_tile() == 0) {
@@ -353,7 +347,7 @@ void sketch_ws_tile_dims(int64_t* bm, int64_t* bn, int64_t* bk) {
 }
 
 // Cluster size along N: the largest of {max_cl, ..., 2} dividing the N-tile count.
-// LSRN_SKETCH_MAXCL (tuning aid) caps it; default 2 for the 64 x 256 tile
+// The sketch_maxcl override caps it; default 2 for the 64 x 256 tile
 // (CL = 1/2/4/8 -> 82.6/69.3/72.3/83.0 ms on c2 in the first measurement,
 // profiles/r01_sketch_tune.jsonl: whole clusters must fit in a GPC, with CL = 8
 // only 76 % of the SM-cycles were active) and 1 for the 32 x 512 tile.
@@ -361,7 +355,7 @@ template <class C>
 static int cluster_for(int64_t k) {
   const int64_t nt = (k + C::BN - 1) / C::BN;
   int max_cl = C::BM == 64 ? 2 : 1;
-  if (const char* e = std::getenv("LSRN_SKETCH_MAXCL")) max_cl = std::atoi(e);
+  if (ovr().sketch_maxcl >= 1) max_cl = ovr().sketch_maxcl;
   for (int cl : {4, 2})
     if (cl <= max_cl && nt % cl == 0) return cl;
   return 1;

@@ -12,7 +12,11 @@ graph that contains them).  This module only
     uses the GLOBAL index j = lo + local in the Philox counter (C9):
     the sum of the partial sketches is independent of the rank count;
   * moves rank 0's NCCL unique id to every rank through torch.distributed
-    (`exchange_unique_id`), which the library turns into its communicator.
+    (`exchange_unique_id`), which the library turns into its communicator;
+  * or, without NCCL (`host_context`), hands the library host-staged
+    collectives over any torch.distributed backend (gloo, MPI): the library
+    copies the operand to the host and calls back for the sum / broadcast --
+    the paper's own MPI_Reduce / MPI_Bcast / MPI_Allreduce.
 
 Nothing here computes any part of the method.
 """
@@ -49,3 +53,24 @@ def context(stream=None, group=None):
         return lsrn.Context(stream=stream)
     nid = exchange_unique_id(lsrn.nccl_unique_id, group)
     return lsrn.Context(stream=stream, nranks=dist.get_world_size(group), rank=dist.get_rank(group), nccl_id=nid)
+
+
+def host_context(stream=None, group=None):
+    """An lsrn.Context over the ranks of `group` whose collectives are host-staged
+    through torch.distributed (lsrn_ctx_set_host_collectives): no NCCL communicator,
+    the iteration loop runs eagerly.  Works with the gloo backend (and on one GPU
+    shared by several processes, since no kernel waits on another rank's kernel)."""
+    import torch
+    from . import lsrn
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    ctx = lsrn.Context(stream=stream, nranks=world, rank=rank)
+
+    def allreduce(arr):
+        t = torch.from_numpy(arr)          # shares the library's host buffer
+        dist.all_reduce(t, group=group)
+
+    def bcast(arr, root):
+        t = torch.from_numpy(arr)
+        dist.broadcast(t, src=dist.get_global_rank(group, root) if group is not None else root, group=group)
+    ctx.set_host_collectives(allreduce, bcast)
+    return ctx

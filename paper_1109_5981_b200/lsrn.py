@@ -5,6 +5,7 @@ for device memory (tensors, the workspace), the CUDA stream and, for multi-GPU,
 to exchange the NCCL unique id through torch.distributed.  There is no CPU
 fallback: importing this module without the built library raises.
 """
+import contextlib
 import ctypes
 import os
 
@@ -26,7 +27,21 @@ STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE
 EXPORTS = ["lsrn_last_error", "lsrn_version", "lsrn_nccl_unique_id", "lsrn_ctx_create", "lsrn_ctx_destroy",
            "lsrn_ctx_set_profiling", "lsrn_workspace_size", "lsrn_sketch",
            "lsrn_solve_lsqr", "lsrn_solve_cs", "lsrn_debug_gaussian", "lsrn_debug_box_muller", "lsrn_debug_rowpass", "lsrn_last_stats",
-           "lsrn_choose_gamma"]
+           "lsrn_choose_gamma", "lsrn_ctx_set_option", "lsrn_ctx_set_host_collectives"]
+
+# lsrn_ctx_set_option keys (include/lsrn.h)
+OPTIONS = {"profiling": 1, "svd": 2, "graph_reuse": 3, "hostio_chunk_mb": 4, "lsqr_sync": 5, "bcast_n": 6,
+           "sketch_kernel": 100, "sketch_tile": 101, "sketch_maxcl": 102, "sketch_nsplit": 103,
+           "rowpass_keep": 110, "rowpass_occ": 111, "rowpass_wide1": 112, "rowpass_wide2": 113,
+           "rowpass_asyncx": 114, "rowpass_nt": 115, "rowpass_tr": 116, "rowpass_budget_kb": 117,
+           "rowpass_wide_slice": 118, "csr_rowdot": 120, "csr_sketch": 121}
+SVD_METHODS = {"auto": 0, "jw": 1, "gesvd": 2, "polar": 3}
+OPTION_DEFAULTS = {k: -1 for k in OPTIONS}
+OPTION_DEFAULTS.update(profiling=0, svd=0, graph_reuse=1, hostio_chunk_mb=32, lsqr_sync=0, bcast_n=1)
+
+HOST_ALLREDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64)
+HOST_BCAST = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                              ctypes.c_int)
 
 
 class LsrnError(RuntimeError):
@@ -52,7 +67,7 @@ class Report(ctypes.Structure):
                 ("converged", ctypes.c_int32), ("sigma_L", ctypes.c_double), ("sigma_U", ctypes.c_double),
                 ("alpha", ctypes.c_double), ("t_sketch", ctypes.c_double), ("t_allreduce", ctypes.c_double),
                 ("t_svd", ctypes.c_double), ("t_iter", ctypes.c_double), ("t_total", ctypes.c_double),
-                ("rnorm_est", ctypes.c_double)]
+                ("rnorm_est", ctypes.c_double), ("svd_used", ctypes.c_int32), ("collectives", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -90,6 +105,8 @@ def lib():
             "lsrn_debug_rowpass": [vp, vp, i64, i64, i64, vp, vp, dbl, vp, vp, vp, i32, ctypes.POINTER(dbl)],
             "lsrn_choose_gamma": [ctypes.POINTER(Report), i64, i64, dbl, i32, dbl, dbl,
                                   ctypes.POINTER(dbl), ctypes.POINTER(dbl)],
+            "lsrn_ctx_set_option": [vp, i32, i64],
+            "lsrn_ctx_set_host_collectives": [vp, HOST_ALLREDUCE, HOST_BCAST, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -102,7 +119,7 @@ def lib():
 def choose_gamma(probe, m, n, tol=1e-14, solver="lsqr", lo=1.2, hi=3.0):
     """lsrn_choose_gamma (NEXT-4, §6.3): the gamma minimising the stage-time
     model calibrated by a probe solve's report (a dict from Context.solve).  Host-only."""
-    rep = Report(**{f: probe[f] for f, _ in Report._fields_})
+    rep = Report(**{f: probe[f] for f, _ in Report._fields_ if f in probe})
     g, t = ctypes.c_double(), ctypes.c_double()
     _check(lib().lsrn_choose_gamma(ctypes.byref(rep), m, n, tol, 0 if solver == "lsqr" else 1, lo, hi,
                                    ctypes.byref(g), ctypes.byref(t)))
@@ -116,6 +133,33 @@ def _check(code):
 
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _check_vec(name, v, length, device, host):
+    """b / x_out: float64, contiguous, 1-D of the given length, on the device (or on the
+    CPU for host IO) -- the C ABI takes raw pointers and cannot check any of this."""
+    if not isinstance(v, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if v.dtype != torch.float64:
+        raise TypeError(f"{name} must be float64, got {v.dtype}")
+    if v.dim() != 1 or v.numel() != length:
+        raise ValueError(f"{name} must be 1-D of length {length}, got shape {tuple(v.shape)}")
+    if not v.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if host:
+        if v.device.type != "cpu":
+            raise ValueError(f"{name} must be a CPU tensor with host_io=True")
+    elif v.device != device:
+        raise ValueError(f"{name} must live on {device}, got {v.device}")
+
+
+def _check_matrix_device(X, device, host):
+    t = X.val if isinstance(X, Csr) else X
+    if host:
+        if t.device.type != "cpu":
+            raise ValueError("A must be on the CPU with host_io=True")
+    elif t.device != device:
+        raise ValueError(f"A must live on {device}, got {t.device}")
 
 
 def dense(X, m, n, lo=0, cnt=None):
@@ -172,17 +216,24 @@ def nccl_unique_id():
 class Context:
     """An lsrn_ctx bound to the current CUDA device and a torch stream."""
 
-    def __init__(self, stream=None, nranks=1, rank=0, nccl_id=None):
+    def __init__(self, stream=None, nranks=1, rank=0, nccl_id=None, null_stream=False):
         self.device = torch.device("cuda", torch.cuda.current_device())
-        # a dedicated (capturable) stream: the iteration loop is captured as a CUDA graph
-        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+        # a dedicated (capturable) stream: the iteration loop is captured as a CUDA graph.
+        # null_stream=True passes NULL (the legacy stream) to the library, which then
+        # runs on a stream of its own joined to the legacy stream at every call.
+        if null_stream:
+            self.stream = torch.cuda.default_stream(self.device)
+            handle = None
+        else:
+            self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+            handle = ctypes.c_void_p(self.stream.cuda_stream)
         h = ctypes.c_void_p()
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        _check(lib().lsrn_ctx_create(ctypes.byref(h), ctypes.c_void_p(self.stream.cuda_stream), nranks, rank,
-                                     idbuf))
+        _check(lib().lsrn_ctx_create(ctypes.byref(h), handle, nranks, rank, idbuf))
         self.h = h
         self.nranks, self.rank = nranks, rank
         self._ws = None
+        self._host_coll = None
 
     def close(self):
         if self.h:
@@ -197,6 +248,45 @@ class Context:
 
     def set_profiling(self, on=True):
         _check(lib().lsrn_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def set_option(self, name, value):
+        """lsrn_ctx_set_option by name (OPTIONS); svd also takes 'auto' / 'jw' / 'gesvd' / 'polar'."""
+        if name == "svd" and isinstance(value, str):
+            value = SVD_METHODS[value]
+        _check(lib().lsrn_ctx_set_option(self.h, OPTIONS[name], int(value)))
+
+    @contextlib.contextmanager
+    def options(self, **kv):
+        """Set options for the duration of a with-block, then restore their defaults."""
+        for k_, v_ in kv.items():
+            self.set_option(k_, v_)
+        try:
+            yield self
+        finally:
+            for k_ in kv:
+                self.set_option(k_, OPTION_DEFAULTS[k_])
+
+    def set_host_collectives(self, allreduce, bcast):
+        """Host-staged collectives (lsrn_ctx_set_host_collectives).  allreduce(arr) sums the
+        float64 numpy array arr in place over the ranks; bcast(arr, root) broadcasts it.
+        Python exceptions in the callbacks become LSRN_ENCCL."""
+        import numpy as np
+
+        def _ar(user, buf, count):
+            try:
+                allreduce(np.ctypeslib.as_array(buf, shape=(count,)))
+                return 0
+            except Exception:
+                return 1
+
+        def _bc(user, buf, count, root):
+            try:
+                bcast(np.ctypeslib.as_array(buf, shape=(count,)), root)
+                return 0
+            except Exception:
+                return 1
+        self._host_coll = (HOST_ALLREDUCE(_ar), HOST_BCAST(_bc))     # keep the thunks alive
+        _check(lib().lsrn_ctx_set_host_collectives(self.h, self._host_coll[0], self._host_coll[1], None))
 
     def workspace(self, nbytes):
         if self._ws is None or self._ws.numel() < nbytes:
@@ -229,6 +319,7 @@ class Context:
 
     def sketch(self, X, m, n, gamma=2.0, lam=0.0, seed=5981, lo=0, cnt=None):
         """Tall-form sketch At (s x k) of the shard X (dense or Csr); returns a new device tensor."""
+        _check_matrix_device(X, self.device, False)
         mat, _keep = describe(X, m, n, lo, cnt)
         k = min(m, n)
         s = int(torch.tensor(gamma * k, dtype=torch.float64).ceil().item())
@@ -246,7 +337,12 @@ class Context:
     def solve(self, X, b, m, n, solver="lsqr", gamma=2.0, lam=0.0, tol=1e-14, seed=5981, alpha=-1.0,
               mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False, reuse_sketch=False):
         """LSRN solve; X a long-index-major dense shard or a Csr row shard (device, or pinned host with host_io)."""
+        if solver not in ("lsqr", "cs"):
+            raise ValueError("solver must be 'lsqr' or 'cs'")
+        _check_matrix_device(X, self.device, host_io)
         if host_io and not isinstance(X, Csr):
+            if X.dtype != torch.float64:
+                raise TypeError("A must be float64")
             if X.dim() != 2 or (X.stride(1) != 1 and X.shape[1] > 1):   # a 1-column stride is immaterial
                 raise ValueError("X must be row-major 2-D")
             cnt_ = X.shape[0] if cnt is None else cnt
@@ -255,18 +351,19 @@ class Context:
             mat, _keep = describe(X, m, n, lo, cnt)
         tall = m >= n
         xlen = n if tall else mat.cnt
+        _check_vec("b", b, mat.cnt if tall else m, self.device, host_io)
         if x_out is None:
             x_out = torch.empty(xlen, dtype=torch.float64,
                                 device="cpu" if host_io else self.device,
                                 pin_memory=bool(host_io))
+        else:
+            _check_vec("x_out", x_out, xlen, self.device, host_io)
         opts = Opts(gamma=gamma, lambda_=lam, tol=tol, alpha=alpha, seed=seed,
                     mode=MODE_ADAPTIVE if mode == "adaptive" else MODE_PREDICTABLE, max_iter=max_iter,
                     flags=(HOST_IO if host_io else 0) | (REUSE_SKETCH if reuse_sketch else 0))
         ws = self.workspace(self.workspace_size(mat, opts))
         rep = Report()
         fn = lib().lsrn_solve_lsqr if solver == "lsqr" else lib().lsrn_solve_cs
-        if solver not in ("lsqr", "cs"):
-            raise ValueError("solver must be 'lsqr' or 'cs'")
         cur = self._enter()
         _check(fn(self.h, ctypes.byref(mat), _ptr(b), ctypes.byref(opts), _ptr(ws), ws.numel(), _ptr(x_out),
                   ctypes.byref(rep)))
@@ -276,6 +373,15 @@ class Context:
     def solve_path(self, X, b, m, n, lambdas, **kw):
         """Solve for a sequence of Tikhonov lambdas, sketching A once (§5):
         the first solve computes G A, the others reuse it (LSRN_REUSE_SKETCH)."""
+        # one workspace for the whole path: lambda > 0 adds the Tikhonov block to the long
+        # vectors, and a workspace reallocated mid-path would lose the cached sketch
+        mat, _keep = describe(X, m, n, kw.get("lo", 0), kw.get("cnt"))
+        need = 0
+        for lam in lambdas:
+            o = Opts(gamma=kw.get("gamma", 2.0), lambda_=lam, tol=kw.get("tol", 1e-14), alpha=kw.get("alpha", -1.0),
+                     seed=kw.get("seed", 5981), mode=MODE_PREDICTABLE, max_iter=0, flags=0)
+            need = max(need, self.workspace_size(mat, o))
+        self.workspace(need)
         out = []
         for i, lam in enumerate(lambdas):
             x, rep = self.solve(X, b, m, n, lam=lam, reuse_sketch=(i > 0), **kw)

@@ -34,13 +34,31 @@ def test_header_symbols_exported(libpath):
     assert b"sm_100a" in lsrn.lib().lsrn_version()
 
 
+def _sass_functions(libpath):
+    """{mangled kernel name: SASS text} from cuobjdump -sass (one entry per function)."""
+    sass = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
+    funcs = {}
+    for chunk in sass.split("Function : ")[1:]:
+        name, _, body = chunk.partition("\n")
+        funcs[name.strip()] = funcs.get(name.strip(), "") + body
+    return funcs
+
+
 def test_sass_is_sm100a_and_uses_dmma(libpath):
     out = subprocess.run(["cuobjdump", "-lelf", libpath], capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    sass = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
-    # the dense sketch (K2) runs on the fp64 tensor cores
-    body = sass.split("sketch_dense_kernel", 1)[1]
-    assert "DMMA.8x8x4" in body
+    funcs = _sass_functions(libpath)
+    # the dense sketch's default kernel (K2, warp-specialized) runs on the fp64 tensor
+    # cores, its X tiles arrive by TMA bulk copies completing on mbarriers
+    ws = {n: b for n, b in funcs.items() if "sketch_ws_kernel" in n}
+    assert ws, "no sketch_ws_kernel instance in the library"
+    for n, body in ws.items():
+        assert "DMMA.8x8x4" in body, n
+        assert "UBLKCP" in body, n
+        assert "SYNCS" in body, n
+    # the fallback kernel too
+    fb = {n: b for n, b in funcs.items() if "sketch_dense_kernel" in n}
+    assert fb and all("DMMA.8x8x4" in b for b in fb.values())
 
 
 def test_no_device_calls_without_gpu():
@@ -53,3 +71,31 @@ def test_no_device_calls_without_gpu():
     rc = lsrn.lib().lsrn_ctx_create(ctypes.byref(h), None, 1, 0, None)
     assert rc != 0
     assert lsrn.lib().lsrn_last_error()
+
+
+def test_binding_vector_checks_without_gpu():
+    """The binding's argument checks (the C ABI takes raw pointers and cannot check dtype,
+    length, contiguity or device)."""
+    import torch
+    from paper_1109_5981_b200 import lsrn
+    dev = torch.device("cuda", 0)
+    v = torch.zeros(10, dtype=torch.float64)
+    lsrn._check_vec("b", v, 10, dev, host=True)
+    with pytest.raises(TypeError):
+        lsrn._check_vec("b", v.float(), 10, dev, host=True)
+    with pytest.raises(ValueError):
+        lsrn._check_vec("b", v, 11, dev, host=True)
+    with pytest.raises(ValueError):
+        lsrn._check_vec("b", torch.zeros(10, 2, dtype=torch.float64)[:, 0], 10, dev, host=True)
+    with pytest.raises(ValueError):
+        lsrn._check_vec("b", v, 10, dev, host=False)          # CPU tensor where the device is required
+    with pytest.raises(ValueError):
+        lsrn._check_matrix_device(torch.zeros(3, 2, dtype=torch.float64), dev, host=False)
+
+
+def test_options_table_matches_header():
+    """Every LSRN_OPT_* of include/lsrn.h has a name in the binding's OPTIONS, same value."""
+    from paper_1109_5981_b200 import lsrn
+    src = open(HEADER).read()
+    hdr = {k.lower(): int(v) for k, v in re.findall(r"LSRN_OPT_([A-Z0-9_]+)\s*=\s*(\d+)", src)}
+    assert hdr == lsrn.OPTIONS

@@ -8,12 +8,12 @@ The oracle cannot redo a full-size solve in seconds, so these tests check
     against A^+ b directly; iteration counts against Thm 4.5 / Alg. 3 (P:643,
     P:694) and the rank against the generator's rank;
   * invariants at any size: x in range(A^T) and the normal equations.
-c2 runs by default (about a minute); c3 (3.2 GB), c4 (CSR, 1.4e8 nonzeros:
-sampled sketch and a full CS solve), c5 (80 GB) and t4 (NEXT-2) run when
-LSRN_FULLSIZE=1 (their SVD / sketch stages take long).
+  * at c2, the WHOLE sketch against the oracle's (relative Frobenius <= 1e-12,
+    the north star's bar), since the oracle finishes it in under a minute.
+Every BASELINE config runs: c2, c3 (3.2 GB), c4 (CSR, 1.4e8 nonzeros: sampled
+sketch and a full CS solve), c5 (80 GB) and t4 (NEXT-2), in the launch
+configuration bench.py times (default plans, one context).
 """
-import os
-
 import numpy as np
 import pytest
 import torch
@@ -24,7 +24,6 @@ from oracle.sketch import sketch_entries
 from synth.generate import SKETCH_SEED, make_problem
 
 pytestmark = pytest.mark.gpu
-FULL = os.environ.get("LSRN_FULLSIZE") == "1"
 
 
 @pytest.fixture(scope="module")
@@ -51,6 +50,19 @@ def _sampled_sketch_check(At, Xcol, s, L, sx=1.0, si=0.0, nsamp=12, seed=0):
     scale = np.array([sx * np.linalg.norm(cols_data[c]) + si for c in cols])
     err = np.abs(got - ref) / scale
     assert err.max() <= 1e-12, (err.max(), rows, cols)
+
+
+def test_c2_full_sketch_vs_oracle(ctx):
+    """The whole c2 sketch (4000 x 2000 from 1e5 x 2000) against the oracle's blocked
+    explicit-G product (oracle.sketch.sketch): relative Frobenius <= 1e-12."""
+    from oracle.sketch import sketch as orc_sketch
+    p = make_problem("c2", device="cuda")
+    At = ctx.sketch(p.X, p.m, p.n, 2.0, 0.0, seed=SKETCH_SEED).cpu().numpy()
+    X = p.X.cpu().numpy()
+    del p
+    ref = orc_sketch(X, 4000, SKETCH_SEED, block=8192, precise=True)
+    rel = np.linalg.norm(At - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-12, rel
 
 
 def test_c2_full(ctx):
@@ -82,7 +94,6 @@ def test_c2_full(ctx):
         assert leak <= 1e-10, leak
 
 
-@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
 def test_c3_full_tikhonov(ctx):
     p = make_problem("c3", device="cuda")
     m, n, lam = p.m, p.n, p.lam
@@ -102,7 +113,6 @@ def test_c3_full_tikhonov(ctx):
         assert float(torch.linalg.norm(res) / scale) <= 1e-12
 
 
-@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
 def test_c4_full_sketch(ctx):
     from paper_1109_5981_b200.lsrn import Csr
     p = make_problem("c4", device="cuda")
@@ -115,7 +125,6 @@ def test_c4_full_sketch(ctx):
     _sampled_sketch_check(At, col, At.shape[0], p.m, nsamp=8)
 
 
-@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
 def test_c4_full_solve(ctx):
     """c4 end to end with CS (the config's solver): Alg. 3's pass count from the Thm 4.4
     bounds at r = k = 2e4, s = 4e4, and the normal equations
@@ -134,7 +143,6 @@ def test_c4_full_solve(ctx):
     assert np.linalg.norm(g) <= 10 * 2e-14 * an * np.linalg.norm(b)
 
 
-@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
 def test_c5_full(ctx):
     p = make_problem("c5", device="cuda")
     m, n = p.m, p.n
@@ -155,7 +163,6 @@ def test_c5_full(ctx):
     assert float(torch.linalg.norm(g)) <= 10 * 2e-14 * an * float(torch.linalg.norm(p.b))
 
 
-@pytest.mark.skipif(not FULL, reason="LSRN_FULLSIZE=1 runs the large configs")
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
 def test_t4_full(ctx, solver):
     """NEXT-2 at its full size (1024 x 4e6, the CSR of A^T, 21 nonzeros per column of A):

@@ -47,3 +47,21 @@ def test_one_rank_nccl_equals_plain(pair, name, solver):
     assert r1["iters"] == r2["iters"] and r1["r"] == r2["r"]
     assert torch.equal(x1, x2)
     assert np.isfinite(x2.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_one_rank_nccl_lsqr_two_collectives(pair, name):
+    """LSRN_OPT_LSQR_SYNC = 1 (textbook LSQR: ||u||^2 reduced first, then the vector,
+    P:301-304) issues two NCCL allreduces per half-step instead of one packed one;
+    the arithmetic is unchanged, so x equals the packed run bit for bit."""
+    plain, nccl = pair
+    p = small(name)
+    X, b = p.X.cuda(), p.b.cuda()
+    x1, r1 = nccl.solve(X, b, p.m, p.n, solver="lsqr", lam=p.lam)
+    with nccl.options(lsqr_sync=1):
+        x2, r2 = nccl.solve(X, b, p.m, p.n, solver="lsqr", lam=p.lam)
+    assert torch.equal(x1, x2) and r1["iters"] == r2["iters"]
+    # sketch allreduce + non-finite flag + one (packed) or two per long pass
+    passes = r1["iters"] + 1
+    assert r1["collectives"] == 2 + passes, r1["collectives"]
+    assert r2["collectives"] == 2 + 2 * passes, r2["collectives"]

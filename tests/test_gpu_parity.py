@@ -10,8 +10,6 @@ Tolerances (north star):
 """
 import math
 
-import os
-
 import numpy as np
 import pytest
 import torch
@@ -168,15 +166,20 @@ def test_single_column_or_row(ctx, shape):
 
 
 @pytest.mark.parametrize("name", ["c2", "c3"])
-def test_svd_gesvd_fallback_small(ctx, monkeypatch, name):
-    """The SVD fallback used when the Jordan-Wielandt matrix exceeds cuSOLVER's limit
-    (k > 16384, c4) -- geqrf + gesvd of R -- forced at small size: same rank, counts and
-    solution as the oracle (rank-deficient c2 and Tikhonov c3)."""
-    monkeypatch.setenv("LSRN_SVD_GESVD", "1")
+@pytest.mark.parametrize("method", ["gesvd", "polar"])
+def test_svd_methods_small(ctx, name, method):
+    """The SVD methods used when the Jordan-Wielandt matrix exceeds cuSOLVER's limit
+    (k > 16384, c4): polar (gesvdp of R, accepted only for clearly full-rank R) and
+    gesvd of R, forced at small size: same rank, counts and solution as the oracle
+    (rank-deficient c2 -- where the polar result must be rejected and redone with
+    gesvd -- and Tikhonov c3)."""
     p = small(name)
     A = p.dense_A().numpy()
     b = p.b.numpy()
-    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs", lam=p.lam)
+    with ctx.options(svd=method):
+        x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs", lam=p.lam)
+    # c2's sketch has rank 1800 < k: the polar result is rejected and redone with gesvd
+    assert rep["svd_used"] == (2 if method == "gesvd" or name == "c2" else 3)
     orc = orc_solve(A, b, solver="cs", lam=p.lam)
     assert rep["r"] == orc["r"] and rep["iters"] == orc["iters"]
     sv = np.linalg.svd(A, compute_uv=False)
@@ -243,35 +246,24 @@ def test_host_io_matches_device(ctx):
 
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
 def test_host_io_streamed(ctx, solver):
-    """LSRN_HOST_IO with A streamed in chunks (each sketched as soon as its copy lands; the
-    chunk size is read once per process, so a subprocess sets it): same solution as the
-    device-resident call up to the split-K summation order of the sketch."""
-    import subprocess
-    import sys
-    code = (
-        "import torch, numpy as np\n"
-        "from paper_1109_5981_b200 import lsrn\n"
-        "g = torch.Generator().manual_seed(5)\n"
-        "m, n = 40000, 60\n"
-        "X = torch.randn(m, n, generator=g, dtype=torch.float64)\n"
-        "b = torch.randn(m, generator=g, dtype=torch.float64)\n"
-        "c = lsrn.Context()\n"
-        f"xd, rd = c.solve(X.cuda(), b.cuda(), m, n, solver='{solver}')\n"
-        f"xh, rh = c.solve(X.pin_memory(), b.pin_memory(), m, n, solver='{solver}', host_io=True)\n"
-        "xs = np.linalg.lstsq(X.numpy(), b.numpy(), rcond=None)[0]\n"
-        "assert rd['iters'] == rh['iters'], (rd, rh)\n"
-        "e1 = float(np.linalg.norm(xd.cpu().numpy() - xh.numpy()) / np.linalg.norm(xs))\n"
-        "e2 = float(np.linalg.norm(xh.numpy() - xs) / np.linalg.norm(xs))\n"
-        "assert e1 <= 1e-12 and e2 <= 1e-10, (e1, e2)\n"
-        "print('ok', e1, e2)\n"
-    )
-    env = dict(os.environ, LSRN_HOSTIO_CHUNK_MB="2")      # 19.2 MB of A -> 10 chunks
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    """LSRN_HOST_IO with A streamed in chunks (each sketched as soon as its copy lands):
+    same solution as the device-resident call up to the split-K summation order of the
+    sketch.  A 2 MB first chunk cuts the 19.2 MB A into 10 chunks."""
+    g = torch.Generator().manual_seed(5)
+    m, n = 40000, 60
+    X = torch.randn(m, n, generator=g, dtype=torch.float64)
+    b = torch.randn(m, generator=g, dtype=torch.float64)
+    with ctx.options(hostio_chunk_mb=2):
+        xd, rd = ctx.solve(X.cuda(), b.cuda(), m, n, solver=solver)
+        xh, rh = ctx.solve(X.pin_memory(), b.pin_memory(), m, n, solver=solver, host_io=True)
+    xs = np.linalg.lstsq(X.numpy(), b.numpy(), rcond=None)[0]
+    assert rd["iters"] == rh["iters"]
+    e1 = float(np.linalg.norm(xd.cpu().numpy() - xh.numpy()) / np.linalg.norm(xs))
+    e2 = float(np.linalg.norm(xh.numpy() - xs) / np.linalg.norm(xs))
+    assert e1 <= 1e-12 and e2 <= 1e-10, (e1, e2)
 
 
-def test_graph_cache_matches_fresh_context(ctx, monkeypatch):
+def test_graph_cache_matches_fresh_context(ctx):
     """The iteration graph is reused when nothing it holds by value changed; a sequence that
     changes solver, Tikhonov lambda, the SVD path (workspace carve-up) and back must give,
     solve by solve, bit-for-bit the result of a fresh context (which always captures)."""
@@ -279,15 +271,15 @@ def test_graph_cache_matches_fresh_context(ctx, monkeypatch):
     p = small("c2")
     X, b = p.X.cuda(), p.b.cuda()
     steps = [dict(solver="lsqr"), dict(solver="lsqr"), dict(solver="cs"), dict(solver="lsqr", lam=0.3),
-             dict(solver="lsqr", lam=0.3), dict(solver="lsqr", env="1"), dict(solver="lsqr"), dict(solver="cs")]
+             dict(solver="lsqr", lam=0.3), dict(solver="lsqr", svd="gesvd"), dict(solver="lsqr"), dict(solver="cs"),
+             dict(solver="lsqr", svd="polar")]
     for st_ in steps:
-        kw = {k_: v_ for k_, v_ in st_.items() if k_ != "env"}
-        if "env" in st_:
-            monkeypatch.setenv("LSRN_SVD_GESVD", "1")
-        else:
-            monkeypatch.delenv("LSRN_SVD_GESVD", raising=False)
-        x1, r1 = ctx.solve(X, b, p.m, p.n, **kw)
+        kw = {k_: v_ for k_, v_ in st_.items() if k_ != "svd"}
+        svd = st_.get("svd", "auto")
+        with ctx.options(svd=svd):
+            x1, r1 = ctx.solve(X, b, p.m, p.n, **kw)
         fresh = lsrn.Context()
+        fresh.set_option("svd", svd)
         x2, r2 = fresh.solve(X, b, p.m, p.n, **kw)
         fresh.close()
         assert r1["iters"] == r2["iters"] and torch.equal(x1, x2), st_
@@ -300,57 +292,52 @@ def test_repeat_solves_bitwise(ctx):
     assert torch.equal(x1, x2)
 
 
-@pytest.mark.parametrize("tile,maxcl,n", [("0", 1, 1000), ("0", 2, 1024), ("0", 4, 1024), ("0", 4, 2048),
-                                          ("0", 2, 1536), ("1", 1, 1000), ("1", 2, 1024), ("1", 2, 1536),
-                                          ("1", 1, 3000), ("batch", 0, 1000), ("batch", 0, 2048)])
-def test_sketch_tiles_and_clusters(ctx, monkeypatch, tile, maxcl, n):
+@pytest.mark.parametrize("tile,maxcl,n", [(0, 1, 1000), (0, 2, 1024), (0, 4, 1024), (0, 4, 2048),
+                                          (0, 2, 1536), (1, 1, 1000), (1, 2, 1024), (1, 2, 1536),
+                                          (1, 1, 3000)])
+def test_sketch_tiles_and_clusters(ctx, tile, maxcl, n):
     """Every tile shape / G-sharing cluster size of the warp-specialized sketch (64 x 256 with
-    CL = 1, 2, 4; 32 x 512 with CL = 1, 2; LSRN_SKETCH_TILE / _MAXCL are read at each launch)
-    and the batched-RNG variant give the same sketch, ragged N tiles included."""
-    if tile == "batch":
-        monkeypatch.setenv("LSRN_SKETCH_IMPL", "batch")
-    else:
-        monkeypatch.setenv("LSRN_SKETCH_TILE", tile)
-        monkeypatch.setenv("LSRN_SKETCH_MAXCL", str(maxcl))
+    CL = 1, 2, 4; 32 x 512 with CL = 1, 2; options sketch_tile / sketch_maxcl) gives the
+    same sketch, ragged N tiles included."""
     m = n + 300
     g = torch.Generator().manual_seed(n)
     X = torch.randn(m, n, generator=g, dtype=torch.float64)
-    At = ctx.sketch(X.cuda(), m, n, 1.1, 0.0, seed=77).cpu().numpy()
+    with ctx.options(sketch_tile=tile, sketch_maxcl=maxcl):
+        At = ctx.sketch(X.cuda(), m, n, 1.1, 0.0, seed=77).cpu().numpy()
     p = orc_plan(m, n, 1.1, 0.0)
     ref = orc_sketch(X.numpy(), p["s"], 77)
     assert _relfro(At, ref) <= 1e-12
 
 
-@pytest.mark.parametrize("env", [{"LSRN_SVD_GESVD": "1"}, {"LSRN_ROWPASS_KEEP": "0"}, {"LSRN_ROWPASS_OCC": "1"},
-                                 {"LSRN_ROWPASS_OCC": "1", "LSRN_ROWPASS_KEEP": "1"}, {"LSRN_SKETCH_V1": "1"},
-                                 {"LSRN_SKETCH_IMPL": "batch"}, {"LSRN_SKETCH_IMPL": "ws"}])
-def test_tuning_variants_match(ctx, monkeypatch, env):
-    """Kernel variants selected by the tuning switches solve c1 to the same tolerance."""
-    for k_, v_ in env.items():
-        monkeypatch.setenv(k_, v_)
+@pytest.mark.parametrize("opts", [dict(svd="gesvd"), dict(svd="polar"), dict(rowpass_keep=0), dict(rowpass_occ=1),
+                                  dict(rowpass_occ=1, rowpass_keep=1), dict(sketch_kernel=1), dict(sketch_kernel=0),
+                                  dict(sketch_nsplit=3), dict(graph_reuse=0)])
+def test_tuning_variants_match(ctx, opts):
+    """Kernel variants selected by the plan overrides (lsrn_ctx_set_option) solve c1 to the
+    same tolerance."""
     p = make_problem("c1")
     A = p.X.numpy()
-    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs")
+    with ctx.options(**opts):
+        x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs")
     orc = orc_solve(A, p.b.numpy(), solver="cs", extended=True)
     assert rep["iters"] == orc["iters"]
     _check_solution(A, x.cpu().numpy(), orc["x"], p.meta["kappa"])
 
 
-@pytest.mark.parametrize("n,env", [(4100, {}), (9000, {}), (9000, {"LSRN_ROWPASS_WIDE1": "0"}),
-                                   (9000, {"LSRN_ROWPASS_WIDE1": "0", "LSRN_ROWPASS_ASYNCX": "0"})])
+@pytest.mark.parametrize("n,opts", [(4100, {}), (9000, {}), (9000, {"rowpass_wide1": 0}),
+                                    (9000, {"rowpass_wide1": 0, "rowpass_asyncx": 0})])
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
-def test_wide_rows_vs_pseudoinverse(ctx, monkeypatch, n, env, solver):
+def test_wide_rows_vs_pseudoinverse(ctx, n, opts, solver):
     """k > 4096: one CTA per row up to 8192 doubles (256 threads) and up to 10240 (512
     threads); with LSRN_ROWPASS_WIDE1=0 each row is split over a 2-CTA cluster (partial
-    dots exchanged with st.async, or with a cluster barrier when LSRN_ROWPASS_ASYNCX=0).
+    dots exchanged with st.async, or with a cluster barrier when rowpass_asyncx = 0).
     The generator's factors give x* = V diag(1/sigma) U^T b exactly."""
-    for k_, v_ in env.items():
-        monkeypatch.setenv(k_, v_)
     p = make_problem("c1", m=n + 1900, n=n, keep_factors=True)
     U, V, sig = p.meta["U"].numpy(), p.meta["V"].numpy(), p.meta["sigma"].numpy()
     b = p.b.numpy()
     xstar = V @ ((U.T @ b) / sig)
-    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver=solver, gamma=1.5)
+    with ctx.options(**opts):
+        x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver=solver, gamma=1.5)
     assert rep["r"] == n
     dx = x.cpu().numpy() - xstar
     # Thm 4.5's A-norm form (P:656-662) is kappa-free; the 2-norm carries the fp64

@@ -1,3 +1,5 @@
+import os
+import sys
 """Long-pass (K6) timing on a c2/c5-shaped solve under tuning env settings."""
 import json, os, sys
 sys.path.insert(0, os.getcwd())
@@ -13,6 +15,9 @@ else:
     p = make_problem(cfg, device="cuda"); m, n = p.m, p.n
     X, b = p.X, p.b
 ctx = lsrn.Context()
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _opts import apply_env_options  # noqa: E402
+apply_env_options(ctx)
 ctx.set_profiling(True)
 out = []
 with torch.cuda.stream(ctx.stream):
@@ -21,5 +26,5 @@ with torch.cuda.stream(ctx.stream):
         st = ctx.stats()
         out.append((st["long_pass_ms"], rep["t_iter"], st["long_pass_bytes"]))
 lp, ti, by = min(out)
-print(json.dumps({"cfg": cfg, "env": {k: v for k, v in os.environ.items() if k.startswith("LSRN_")},
+print(json.dumps({"cfg": cfg, "env": {k: v for k, v in os.environ.items() if k.startswith("LSRN_OPT_")},
                   "long_pass_ms": lp, "gbs": by / lp / 1e6, "t_iter_s": ti, "iters": rep["iters"]}))

@@ -1,3 +1,5 @@
+import os
+import sys
 """Time the dense sketch on the c2 shape under tuning env settings (one process per setting)."""
 import json, os, sys, time
 sys.path.insert(0, os.getcwd())
@@ -7,6 +9,9 @@ m, n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000, int(sys.argv[2]) if le
 torch.manual_seed(0)
 X = torch.randn(m, n, dtype=torch.float64, device="cuda")
 ctx = lsrn.Context()
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _opts import apply_env_options  # noqa: E402
+apply_env_options(ctx)
 with torch.cuda.stream(ctx.stream):
     for _ in range(2):
         ctx.sketch(X, m, n)
@@ -17,5 +22,5 @@ with torch.cuda.stream(ctx.stream):
         e0.record(ctx.stream); ctx.sketch(X, m, n); e1.record(ctx.stream); torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
 s = int(2 * n)
-print(json.dumps({"m": m, "n": n, "env": {k: v for k, v in os.environ.items() if k.startswith("LSRN_")},
+print(json.dumps({"m": m, "n": n, "env": {k: v for k, v in os.environ.items() if k.startswith("LSRN_OPT_")},
                   "ms_min": min(ms), "tflops": 2 * s * n * m / min(ms) / 1e9}))
