@@ -40,12 +40,26 @@ def plan(m, n, gamma, lam=0.0):
                 sigma_x=sigma_x, sigma_i=sigma_i)
 
 
-def sketch(X, s, seed, sigma_x=1.0, sigma_i=0.0, block=4096, precise=True):
+def sketch(X, s, seed, sigma_x=1.0, sigma_i=0.0, block=None, precise=True):
     """Ãt = sigma_X (G[:, :L] X) + sigma_I G[:, L:L+k]  (s x k), X dense or scipy CSR.
 
-    A plain blocked sum over the long index: G is generated block by block
-    (never the whole s x L at once) and multiplied with a library matmul.
+    The oracle's sketch is the naive-loop C code (oracle/c/lsrn_oracle.c,
+    orc_sketch_dense / orc_sketch_csr): for every sketch row i and column c the sum
+    over the long index in increasing order, in fixed blocks of 256 (C17), with
+    G[i, j] evaluated in long double (C9).  `block` and `precise` are accepted for
+    the explicit-G variant below (precise=False selects it with fp64 libm normals).
     """
+    from . import _c
+    if not precise:
+        return sketch_blas(X, s, seed, sigma_x, sigma_i, block=block or 4096, precise=False)
+    if hasattr(X, "toarray") and not isinstance(X, np.ndarray):
+        return _c.sketch_csr(X, s, seed, sigma_x, sigma_i)
+    return _c.sketch_dense(X, s, seed, sigma_x, sigma_i)
+
+
+def sketch_blas(X, s, seed, sigma_x=1.0, sigma_i=0.0, block=4096, precise=True):
+    """The same product through explicit G blocks and a library matmul (a pin of the
+    naive loops: same definition, different summation order)."""
     L, k = X.shape
     acc = np.zeros((s, k), dtype=np.float64)
     for j0 in range(0, L, block):

@@ -333,6 +333,133 @@ csr_sketch_light_kernel(const int64_t* __restrict__ colptr, const int32_t* __res
   }
 }
 
+// Generate-once light sketch (csr_sketch_slab_kernel).  The per-nonzero kernel
+// above regenerates G[:, j] for every light nonzero of row j (21x the s L normals
+// on t4).  Here a CTA owns IB = 32 sketch rows (lane = sketch row) and a tile of
+// CW = 512 columns (warp w: columns w*32 .. w*32+31, one register accumulator per
+// column per lane), and walks a range of CJ = 256-row chunks of the long index:
+//   phase G: all threads generate the chunk's G tile Gs[jj][ii] (CJ x IB, 64 KB of
+//            shared memory) -- each G[i, j] ONCE per column tile;
+//   phase S: warp w, for each of its 32 columns c, runs over the column's CSC
+//            entries that fall in the chunk (a contiguous sub-range of the CSC
+//            column: cp[J][c] .. cp[J+1][c]) and accumulates acc[c] += Gs[jj][lane] a.
+// Normals generated = s L x (number of column tiles), independent of nnz; the
+// FMA side costs one shared load per (sketch row, nonzero).  Partial results of
+// the long-index splits go to part[split][c][i] and are summed in fixed order
+// (csr_slab_finish_kernel): deterministic, no atomics.
+namespace slab {
+constexpr int IB = 32;                // sketch rows per CTA (= lanes)
+constexpr int NW = 16;                // warps per CTA
+constexpr int THREADS = NW * 32;
+constexpr int CPW = 32;               // columns per warp (register accumulators)
+constexpr int CW = NW * CPW;          // 512 columns per CTA tile
+constexpr int CJ = 256;               // long-index rows per chunk
+constexpr size_t SMEM = (size_t)CJ * IB * sizeof(double) + bm::TAB_SIZE * sizeof(double);
+}  // namespace slab
+
+__global__ void __launch_bounds__(slab::THREADS, 1)
+csr_sketch_slab_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                       const double* __restrict__ cval, const int* __restrict__ colmap,
+                       const int32_t* __restrict__ cp, int64_t k, int64_t rows, int64_t lo, int64_t s,
+                       uint64_t seed, int64_t chunks_per_split, int64_t nchunks, double* __restrict__ part) {
+  using namespace slab;
+  extern __shared__ __align__(16) double smem[];
+  double* Gs = smem;                          // [CJ][IB]
+  double* bmT = smem + (size_t)CJ * IB;
+  bm_load_table(bmT);
+  const uint2 key = philox_key(seed);
+  const int64_t I = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = (int64_t)blockIdx.y * CW + (int64_t)warp * CPW;
+  const int64_t myc = c0 + lane;              // this lane's column, for the pointer loads
+  const bool col_ok = myc < k && colmap[myc] < 0;
+  const int64_t mybase = col_ok ? colptr[myc] : 0;
+  double acc[CPW];
+#pragma unroll
+  for (int t = 0; t < CPW; ++t) acc[t] = 0.0;
+  const int64_t J0 = (int64_t)blockIdx.z * chunks_per_split;
+  const int64_t J1 = min(nchunks, J0 + chunks_per_split);
+  for (int64_t J = J0; J < J1; ++J) {
+    const int64_t jrow0 = J * CJ;
+    __syncthreads();                          // previous chunk's phase S done with Gs (and the table loaded)
+    for (int p = threadIdx.x; p < CJ * (IB / 2); p += THREADS) {
+      const int jj = p / (IB / 2), pp = p % (IB / 2);
+      const int64_t j = jrow0 + jj;
+      double z0 = 0.0, z1 = 0.0;
+      if (j < rows) gaussian_pair(key, (uint64_t)(I * (IB / 2) + pp), (uint64_t)(lo + j), bmT, z0, z1);
+      *reinterpret_cast<double2*>(&Gs[jj * IB + 2 * pp]) = make_double2(z0, z1);
+    }
+    __syncthreads();
+    int32_t mye0 = 0, mye1 = 0;
+    if (col_ok) {
+      mye0 = __ldg(cp + J * k + myc);
+      mye1 = __ldg(cp + (J + 1) * k + myc);
+    }
+    const int32_t jr0 = (int32_t)jrow0;
+#pragma unroll
+    for (int t = 0; t < CPW; ++t) {
+      const int64_t base = __shfl_sync(0xffffffffu, mybase, t);
+      const int32_t e0 = __shfl_sync(0xffffffffu, mye0, t), e1 = __shfl_sync(0xffffffffu, mye1, t);
+      double a = acc[t];
+      int32_t e = e0;
+      for (; e + 1 < e1; e += 2) {            // two entries per step: loads issued back to back
+        const int32_t r0 = __ldg(rowidx + base + e), r1 = __ldg(rowidx + base + e + 1);
+        const double v0 = __ldg(cval + base + e), v1 = __ldg(cval + base + e + 1);
+        a = fma(Gs[(r0 - jr0) * IB + lane], v0, a);
+        a = fma(Gs[(r1 - jr0) * IB + lane], v1, a);
+      }
+      if (e < e1) a = fma(Gs[(__ldg(rowidx + base + e) - jr0) * IB + lane], __ldg(cval + base + e), a);
+      acc[t] = a;
+    }
+  }
+  const int64_t i = I * IB + lane;
+  if (i < s) {
+#pragma unroll
+    for (int t = 0; t < CPW; ++t) {
+      const int64_t c = c0 + t;
+      if (c < k) part[((int64_t)blockIdx.z * k + c) * s + i] = acc[t];
+    }
+  }
+}
+
+// cp[J][c] = number of CSC entries of light column c with row < J * CJ, J = 0..nchunks
+// (warp per column; rows within a CSC column are ascending).  Heavy columns: 0.
+__global__ void csr_chunkptr_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                                    const int* __restrict__ colmap, int64_t k, int64_t nchunks,
+                                    int32_t* __restrict__ cp) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= k) return;
+  const int64_t e0 = colmap[c] < 0 ? colptr[c] : 0, e1 = colmap[c] < 0 ? colptr[c + 1] : 0;
+  const int64_t n = e1 - e0;
+  for (int64_t t = lane; t <= n; t += 32) {
+    // chunks J in (chunk(t - 1), chunk(t)] start at entry t (chunk(-1) = -1, chunk(n) = nchunks)
+    const int64_t hi = t < n ? rowidx[e0 + t] / slab::CJ : nchunks;
+    const int64_t lo_ = t > 0 ? rowidx[e0 + t - 1] / slab::CJ : -1;
+    for (int64_t J = lo_ + 1; J <= hi; ++J) cp[J * k + c] = (int32_t)t;
+  }
+}
+
+// At[i][c] = sum_split part[split][c][i] for the light columns (fixed split order);
+// 32 x 32 tiles through shared memory so that both sides are coalesced.
+__global__ void csr_slab_finish_kernel(const double* __restrict__ part, int nsplit, int64_t s, int64_t k,
+                                       const int* __restrict__ colmap, double* __restrict__ At) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t c = c0 + r, i = i0 + threadIdx.x;
+    double v = 0.0;
+    if (c < k && i < s)
+      for (int sp = 0; sp < nsplit; ++sp) v += part[((int64_t)sp * k + c) * s + i];
+    tile[r][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, c = c0 + threadIdx.x;
+    if (i < s && c < k && colmap[c] < 0) At[i * k + c] = tile[threadIdx.x][r];
+  }
+}
+
 // At[i][H[h]] = sum_split part[split][i][h]   (fixed split order)
 __global__ void csr_heavy_finish_kernel(const double* __restrict__ part, int nsplit, int64_t s, int nd, int ND,
                                         const int* __restrict__ heavy_cols, int64_t k, double* __restrict__ At) {
@@ -865,10 +992,37 @@ cudaError_t launch_csr_sketch(const CsrSketchArgs& a, cudaStream_t st, int nsm) 
     csr_heavy_finish_kernel<<<grid_cap(a.s * a.nd, 256, (int64_t)nsm * 16), 256, 0, st>>>(
         a.part, a.nsplit, a.s, a.nd, a.ND, a.heavy_cols, a.k, a.At);
   }
+  if (a.skip_light) return cudaSuccess;        // light part by the generate-once slab kernel
   const int cpc = 4;
   dim3 g2(row_blocks, (unsigned)((a.k + cpc - 1) / cpc));
   csr_sketch_light_kernel<<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.k, a.lo, a.s, a.seed, cpc,
                                               a.At);
+  return cudaGetLastError();
+}
+
+int64_t csr_slab_chunk_rows() { return slab::CJ; }
+int64_t csr_slab_tile_cols() { return slab::CW; }
+int64_t csr_slab_row_blocks(int64_t s) { return (s + slab::IB - 1) / slab::IB; }
+
+cudaError_t launch_csr_chunkptr(const int64_t* colptr, const int32_t* rowidx, const int* colmap, int64_t k,
+                                int64_t nchunks, int32_t* cp, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  csr_chunkptr_kernel<<<(unsigned)((k * 32 + 255) / 256), 256, 0, st>>>(colptr, rowidx, colmap, k, nchunks, cp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_sketch_slab(const CsrSlabArgs& a, cudaStream_t st) {
+  using namespace slab;
+  cudaError_t e = cudaFuncSetAttribute(csr_sketch_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  if (e != cudaSuccess) return e;
+  const int64_t cps = (a.nchunks + a.nsplit - 1) / a.nsplit;
+  dim3 grid((unsigned)csr_slab_row_blocks(a.s), (unsigned)((a.k + CW - 1) / CW), (unsigned)a.nsplit);
+  csr_sketch_slab_kernel<<<grid, THREADS, SMEM, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, a.k, a.rows, a.lo,
+                                                      a.s, a.seed, cps, a.nchunks, a.part);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 g2((unsigned)((a.s + 31) / 32), (unsigned)((a.k + 31) / 32));
+  csr_slab_finish_kernel<<<g2, dim3(32, 8), 0, st>>>(a.part, a.nsplit, a.s, a.k, a.colmap, a.At);
   return cudaGetLastError();
 }
 

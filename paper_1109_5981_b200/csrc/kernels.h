@@ -175,8 +175,30 @@ struct CsrSketchArgs {
   const int32_t* rowidx;
   const double* cval;
   double* At;              // s x k (row-major), fully written
+  int skip_light = 0;      // 1: leave the light columns to launch_csr_sketch_slab
 };
 cudaError_t launch_csr_sketch(const CsrSketchArgs& a, cudaStream_t st, int nsm);
+// Generate-once light sketch (csr.cu, csr_sketch_slab_kernel): the light part of
+// At from the CSC copy with the per-chunk column pointers cp[J][c] (launch_csr_chunkptr);
+// part: [nsplit][k][s] scratch; the heavy columns of At are left to the heavy path.
+struct CsrSlabArgs {
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  const double* cval;
+  const int* colmap;
+  const int32_t* cp;        // [nchunks + 1][k]
+  int64_t k, rows, lo, s, nchunks;
+  uint64_t seed;
+  int nsplit;
+  double* part;             // [nsplit][k][s]
+  double* At;
+};
+int64_t csr_slab_chunk_rows();
+int64_t csr_slab_tile_cols();
+int64_t csr_slab_row_blocks(int64_t s);
+cudaError_t launch_csr_chunkptr(const int64_t* colptr, const int32_t* rowidx, const int* colmap, int64_t k,
+                                int64_t nchunks, int32_t* cp, cudaStream_t st);
+cudaError_t launch_csr_sketch_slab(const CsrSlabArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_add_gblock(double* At, int64_t s, int64_t k, int64_t L, double si, uint64_t seed,
                                      cudaStream_t st, int nsm);
 

@@ -327,6 +327,12 @@ struct CsrWs {
   int32_t* rowidx;
   double *cval, *D, *part, *npart, *wpart;
   int64_t *lrowptr, *lchunk_cnt, *lchunk_off;   // light-column CSR (iteration pass, k > 2048)
+  // generate-once light sketch (csr_sketch_slab_kernel): per-chunk CSC pointers + split partials
+  bool slab = false;
+  int slab_nsplit = 1;
+  int64_t slab_nchunks = 0;
+  int32_t* cp = nullptr;
+  double* slab_part = nullptr;
   int32_t* lcol;
   double* lval;
   int nsplit;
@@ -367,6 +373,23 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
   const size_t wp_heavy = (size_t)csr_rowdot_blocks(c->nsm) * kMaxHeavy;
   const size_t wp_all = d.k <= csr_rowdot_all_max_k() ? (size_t)csr_rowdot_all_blocks(c->nsm, d.k) * d.k : 0;
   w.wpart = ar.take<double>(std::max(wp_heavy, wp_all));
+  // Light sketch: the generate-once slab kernel generates each G[i, j] once per
+  // 512-column tile, the per-nonzero kernel once per light nonzero of row j; the
+  // slab kernel is chosen when the tiles are fewer than half the nonzeros per row
+  // (t4: 2 tiles vs 21 nonzeros; c4: 40 tiles vs 70) -- override csr_sketch.
+  const int64_t tiles = (d.k + csr_slab_tile_cols() - 1) / csr_slab_tile_cols();
+  const double nnz_row = d.cnt > 0 ? (double)A->nnz / (double)d.cnt : 0.0;
+  w.slab = d.cnt > 0 && A->nnz > 0 &&
+           (ovr().csr_sketch == 1 || (ovr().csr_sketch != 0 && 2.0 * (double)tiles <= nnz_row));
+  if (w.slab) {
+    w.slab_nchunks = (d.cnt + csr_slab_chunk_rows() - 1) / csr_slab_chunk_rows();
+    const int64_t ctas = csr_slab_row_blocks(d.s) * tiles;
+    int64_t ns = (3 * (int64_t)c->nsm + ctas - 1) / ctas;
+    ns = std::max<int64_t>(1, std::min<int64_t>({ns, 16, w.slab_nchunks}));
+    w.slab_nsplit = (int)ns;
+    w.cp = ar.take<int32_t>((size_t)(w.slab_nchunks + 1) * d.k);
+    w.slab_part = ar.take<double>((size_t)w.slab_nsplit * d.k * d.s);
+  }
   return w;
 }
 
@@ -437,6 +460,10 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
   b.lchunk_off = w.lchunk_off;
   LSRN_CUDA(launch_csr_fill(b, st));
   c->launches += 2;
+  if (w.slab) {
+    LSRN_CUDA(launch_csr_chunkptr(w.colptr, w.rowidx, w.colmap, d.k, w.slab_nchunks, w.cp, st));
+    c->launches++;
+  }
   LSRN_CUDA(cudaStreamSynchronize(st));   // host vectors above are pageable: keep them alive until copied
 }
 
@@ -461,8 +488,28 @@ void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double*
   a.rowidx = w.rowidx;
   a.cval = w.cval;
   a.At = At;
+  a.skip_light = w.slab ? 1 : 0;
   LSRN_CUDA(launch_csr_sketch(a, c->stream, c->nsm));
-  c->launches += (w.nd > 0 ? 3 : 1);
+  c->launches += (w.nd > 0 ? 2 : 0) + (w.slab ? 0 : 1);
+  if (w.slab) {
+    CsrSlabArgs sa{};
+    sa.colptr = w.colptr;
+    sa.rowidx = w.rowidx;
+    sa.cval = w.cval;
+    sa.colmap = w.colmap;
+    sa.cp = w.cp;
+    sa.k = d.k;
+    sa.rows = d.cnt;
+    sa.lo = d.lo;
+    sa.s = d.s;
+    sa.nchunks = w.slab_nchunks;
+    sa.seed = seed;
+    sa.nsplit = w.slab_nsplit;
+    sa.part = w.slab_part;
+    sa.At = At;
+    LSRN_CUDA(launch_csr_sketch_slab(sa, c->stream));
+    c->launches += 2;
+  }
 }
 
 // Raw sketch S0 = G[:, lo:lo+cnt] X_shard of a dense shard (split-K partials summed in fixed order).

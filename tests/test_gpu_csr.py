@@ -67,10 +67,16 @@ def _relfro(a, b):
     (2500, 100, 3, 80, 0.0, 0),      # 80 dense columns: capped at 64 heavy, 16 dense ones stay light
     (3000, 90, 4, 20, 0.5, 0),       # heavy ND=32 + tall Tikhonov block
     (777, 61, 2, 3, 0.0, 5),         # odd s = 122? (gamma 2 -> 122), ragged everything
+    (2597, 1300, 9, 0, 0.0, 3),      # 3 column tiles of the slab kernel, ragged last chunk and tile
+    (1100, 530, 4, 40, 0.25, 0),     # 2 tiles, heavy + light, Tikhonov block
 ])
-def test_csr_sketch_vs_oracle(ctx, m, n, nnz_row, dense_cols, lam, empty):
+@pytest.mark.parametrize("light", [0, 1])
+def test_csr_sketch_vs_oracle(ctx, m, n, nnz_row, dense_cols, lam, empty, light):
+    """light = 0: per-nonzero light sketch (G[:, j] regenerated per nonzero); light = 1:
+    the generate-once slab kernel (each G[i, j] once per 512-column tile)."""
     A = _random_csr(m, n, nnz_row, dense_cols, 1e3, empty, seed=m + n)
-    At = ctx.sketch(_gpu_csr(A), m, n, 2.0, lam, seed=5981).cpu().numpy()
+    with ctx.options(csr_sketch=light):
+        At = ctx.sketch(_gpu_csr(A), m, n, 2.0, lam, seed=5981).cpu().numpy()
     p = orc_plan(m, n, 2.0, lam)
     ref = orc_sketch(A, p["s"], 5981, p["sigma_x"], p["sigma_i"])
     assert _relfro(At, ref) <= 1e-12
@@ -84,13 +90,15 @@ def test_csr_sketch_equals_dense_sketch(ctx):
     assert _relfro(a1, a2) <= 1e-13
 
 
-def test_csr_sketch_shards_sum_to_full(ctx):
+@pytest.mark.parametrize("light", [0, 1])
+def test_csr_sketch_shards_sum_to_full(ctx, light):
     m, n = 3100, 70
     A = _random_csr(m, n, 4, 5, 100.0, 0, seed=2)
-    full = ctx.sketch(_gpu_csr(A), m, n).cpu().numpy()
-    acc = np.zeros_like(full)
-    for lo, hi in [(0, 999), (999, 1000), (1000, 3100)]:
-        acc += ctx.sketch(_gpu_csr(A[lo:hi]), m, n, lo=lo, cnt=hi - lo).cpu().numpy()
+    with ctx.options(csr_sketch=light):
+        full = ctx.sketch(_gpu_csr(A), m, n).cpu().numpy()
+        acc = np.zeros_like(full)
+        for lo, hi in [(0, 999), (999, 1000), (1000, 3100)]:
+            acc += ctx.sketch(_gpu_csr(A[lo:hi]), m, n, lo=lo, cnt=hi - lo).cpu().numpy()
     assert _relfro(acc, full) <= 1e-13
 
 
