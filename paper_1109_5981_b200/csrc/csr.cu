@@ -354,7 +354,14 @@ constexpr int THREADS = NW * 32;
 constexpr int CPW = 32;               // columns per warp (register accumulators)
 constexpr int CW = NW * CPW;          // 512 columns per CTA tile
 constexpr int CJ = 256;               // long-index rows per chunk
-constexpr size_t SMEM = (size_t)CJ * IB * sizeof(double) + bm::TAB_SIZE * sizeof(double);
+constexpr int SW = 256;               // staged entries per warp and chunk (16 B each)
+// shared memory: Gs[CJ][IB] | Box-Muller table | entries [NW][SW] (double2) |
+//                column bases [NW][32] (int64) | column offsets [NW][33] (int)
+constexpr size_t OFF_TAB = (size_t)CJ * IB * 8;
+constexpr size_t OFF_ENT = (OFF_TAB + (size_t)bm::TAB_SIZE * 8 + 15) / 16 * 16;
+constexpr size_t OFF_BASE = OFF_ENT + (size_t)NW * SW * 16;
+constexpr size_t OFF_SOFF = OFF_BASE + (size_t)NW * 32 * 8;
+constexpr size_t SMEM = OFF_SOFF + (size_t)NW * 33 * 4;
 }  // namespace slab
 
 __global__ void __launch_bounds__(slab::THREADS, 1)
@@ -364,12 +371,16 @@ csr_sketch_slab_kernel(const int64_t* __restrict__ colptr, const int32_t* __rest
                        uint64_t seed, int64_t chunks_per_split, int64_t nchunks, double* __restrict__ part) {
   using namespace slab;
   extern __shared__ __align__(16) double smem[];
+  char* sm = reinterpret_cast<char*>(smem);
   double* Gs = smem;                          // [CJ][IB]
-  double* bmT = smem + (size_t)CJ * IB;
+  double* bmT = reinterpret_cast<double*>(sm + OFF_TAB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* ent = reinterpret_cast<double2*>(sm + OFF_ENT) + (size_t)warp * SW;
+  int64_t* sbase = reinterpret_cast<int64_t*>(sm + OFF_BASE) + (size_t)warp * 32;
+  int32_t* soff = reinterpret_cast<int32_t*>(sm + OFF_SOFF) + (size_t)warp * 33;
   bm_load_table(bmT);
   const uint2 key = philox_key(seed);
   const int64_t I = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = (int64_t)blockIdx.y * CW + (int64_t)warp * CPW;
   const int64_t myc = c0 + lane;              // this lane's column, for the pointer loads
   const bool col_ok = myc < k && colmap[myc] < 0;
@@ -381,7 +392,43 @@ csr_sketch_slab_kernel(const int64_t* __restrict__ colptr, const int32_t* __rest
   const int64_t J1 = min(nchunks, J0 + chunks_per_split);
   for (int64_t J = J0; J < J1; ++J) {
     const int64_t jrow0 = J * CJ;
+    const int32_t jr0 = (int32_t)jrow0;
+    // Stage this warp's entries of the chunk first (one round of independent loads for
+    // all 32 columns, overlapping other warps' work, instead of a dependent round trip
+    // per column): lane t's column occupies ent[soff[t] .. soff[t+1]) as {value,
+    // Gs row offset} pairs.  More than SW entries: direct loads below.
+    int32_t e0 = 0, e1 = 0;
+    if (col_ok) {
+      e0 = __ldg(cp + J * k + myc);
+      e1 = __ldg(cp + (J + 1) * k + myc);
+    }
+    int32_t incl = e1 - e0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const bool staged = total <= SW;
+    if (staged) {
+      soff[lane + 1] = incl;
+      if (lane == 0) soff[0] = 0;
+      sbase[lane] = mybase + e0;
+      __syncwarp();
+#pragma unroll 1
+      for (int32_t f = lane; f < total; f += 32) {
+        int lo_t = 0, hi_t = 31;                  // column t with soff[t] <= f < soff[t + 1]
+#pragma unroll
+        for (int it = 0; it < 5; ++it) {
+          const int mid = (lo_t + hi_t + 1) >> 1;
+          if (soff[mid] <= f) lo_t = mid; else hi_t = mid - 1;
+        }
+        const int64_t g = sbase[lo_t] + (f - soff[lo_t]);
+        ent[f] = make_double2(__ldg(cval + g), __longlong_as_double((long long)(__ldg(rowidx + g) - jr0)));
+      }
+    }
     __syncthreads();                          // previous chunk's phase S done with Gs (and the table loaded)
+#pragma unroll 2
     for (int p = threadIdx.x; p < CJ * (IB / 2); p += THREADS) {
       const int jj = p / (IB / 2), pp = p % (IB / 2);
       const int64_t j = jrow0 + jj;
@@ -390,26 +437,30 @@ csr_sketch_slab_kernel(const int64_t* __restrict__ colptr, const int32_t* __rest
       *reinterpret_cast<double2*>(&Gs[jj * IB + 2 * pp]) = make_double2(z0, z1);
     }
     __syncthreads();
-    int32_t mye0 = 0, mye1 = 0;
-    if (col_ok) {
-      mye0 = __ldg(cp + J * k + myc);
-      mye1 = __ldg(cp + (J + 1) * k + myc);
-    }
-    const int32_t jr0 = (int32_t)jrow0;
+    if (staged) {
 #pragma unroll
-    for (int t = 0; t < CPW; ++t) {
-      const int64_t base = __shfl_sync(0xffffffffu, mybase, t);
-      const int32_t e0 = __shfl_sync(0xffffffffu, mye0, t), e1 = __shfl_sync(0xffffffffu, mye1, t);
-      double a = acc[t];
-      int32_t e = e0;
-      for (; e + 1 < e1; e += 2) {            // two entries per step: loads issued back to back
-        const int32_t r0 = __ldg(rowidx + base + e), r1 = __ldg(rowidx + base + e + 1);
-        const double v0 = __ldg(cval + base + e), v1 = __ldg(cval + base + e + 1);
-        a = fma(Gs[(r0 - jr0) * IB + lane], v0, a);
-        a = fma(Gs[(r1 - jr0) * IB + lane], v1, a);
+      for (int t = 0; t < CPW; ++t) {
+        const int q1 = soff[t + 1];
+        double a = acc[t];
+#pragma unroll 1
+        for (int q = soff[t]; q < q1; ++q) {
+          const double2 ev = ent[q];             // broadcast
+          a = fma(Gs[(int)__double_as_longlong(ev.y) * IB + lane], ev.x, a);
+        }
+        acc[t] = a;
       }
-      if (e < e1) a = fma(Gs[(__ldg(rowidx + base + e) - jr0) * IB + lane], __ldg(cval + base + e), a);
-      acc[t] = a;
+      __syncwarp();                            // ent / soff restaged by the next chunk
+    } else {
+#pragma unroll
+      for (int t = 0; t < CPW; ++t) {
+        const int64_t base = __shfl_sync(0xffffffffu, mybase, t);
+        const int32_t f0 = __shfl_sync(0xffffffffu, e0, t), f1 = __shfl_sync(0xffffffffu, e1, t);
+        double a = acc[t];
+#pragma unroll 1
+        for (int32_t e = f0; e < f1; ++e)
+          a = fma(Gs[(__ldg(rowidx + base + e) - jr0) * IB + lane], __ldg(cval + base + e), a);
+        acc[t] = a;
+      }
     }
   }
   const int64_t i = I * IB + lane;

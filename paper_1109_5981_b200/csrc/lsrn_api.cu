@@ -137,6 +137,7 @@ struct lsrn_ctx {
   std::vector<cudaEvent_t> pass_ev;   // pairs around long-pass kernels
   int n_pass_ev = 0;
   bool stats_pending = false;   // stats[1], [2], [4] not yet computed from the pass events
+  bool sketch_pending = false;  // stats[0] of the last lsrn_sketch not yet read from ev[1], ev[2]
   double stats[8] = {};
   int launches = 0;
 };
@@ -713,6 +714,7 @@ void broadcast(lsrn_ctx* c, double* buf, int64_t count, int root) {
 // SVD is redone with gesvd of R, which the rank rule can trust.
 constexpr int64_t kMaxJW = 32768;
 constexpr double kPolarMinRatio = 1e-6;
+constexpr int64_t kPolarMinK = 4096;
 
 struct SvdWs {
   double *W1, *tau, *JW, *S, *Sd, *Nt;   // JW: Jordan-Wielandt matrix, or [R | VT] (gesvd), or [R | U | V] (polar)
@@ -720,7 +722,8 @@ struct SvdWs {
   void* work;
   size_t work_bytes, host_bytes;
   int* info;
-  int method;                            // LSRN_SVD_JW / _GESVD / _POLAR (polar may fall back to gesvd)
+  int method;                            // LSRN_SVD_JW / _GESVD / _POLAR (polar may fall back)
+  bool fallback_jw;                      // a rejected polar result is redone with JW (else gesvd)
 };
 
 // 64-bit cuSOLVER API: the c4 shape (s x k = 4e4 x 2e4) needs workspaces beyond
@@ -729,7 +732,11 @@ SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   SvdWs w{};
   const int64_t k = d.k;
   w.method = c->svd_method;
-  if (w.method == LSRN_SVD_AUTO) w.method = (2 * k <= kMaxJW) ? LSRN_SVD_JW : LSRN_SVD_POLAR;
+  // auto: the polar route from k = 4096 up (c5, k = 1e4: 2.5 s against 4.4 s for the
+  // Jordan-Wielandt eigenproblem, profiles/r02_svd_c5.jsonl), falling back to JW (or
+  // gesvd above its limit) when the polar result is rejected; JW below (c2: 80 ms)
+  if (w.method == LSRN_SVD_AUTO) w.method = (k >= kPolarMinK || 2 * k > kMaxJW) ? LSRN_SVD_POLAR : LSRN_SVD_JW;
+  w.fallback_jw = (w.method == LSRN_SVD_POLAR) && (2 * k <= kMaxJW);
   LSRN_REQUIRE(!(w.method == LSRN_SVD_JW && 2 * k > kMaxJW), LSRN_EUNSUPPORTED,
                "LSRN_SVD_JW needs min(m, n) <= 16384 (cuSOLVER symmetric eigensolver limit)");
   size_t d1 = 0, h1 = 0, d2 = 0, h2 = 0, d3 = 0, h3 = 0;
@@ -737,14 +744,18 @@ SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   double vl = 0.0, vu = 0.0;
   LSRN_SOLVER(cusolverDnXgeqrf_bufferSize(c->solver, c->params, d.s, k, CUDA_R_64F, nullptr, d.s, CUDA_R_64F,
                                           nullptr, CUDA_R_64F, &d1, &h1));
-  if (w.method == LSRN_SVD_JW) {
+  if (w.method == LSRN_SVD_JW || w.fallback_jw) {
     LSRN_SOLVER(cusolverDnXsyevdx_bufferSize(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
                                              CUBLAS_FILL_MODE_LOWER, 2 * k, CUDA_R_64F, nullptr, 2 * k, &vl, &vu,
                                              k + 1, 2 * k, &meig, CUDA_R_64F, nullptr, CUDA_R_64F, &d2, &h2));
-  } else {
+  }
+  if (w.method != LSRN_SVD_JW) {
+    size_t d4 = 0, h4 = 0;
     LSRN_SOLVER(cusolverDnXgesvd_bufferSize(c->solver, c->params, 'N', 'A', k, k, CUDA_R_64F, nullptr, k,
                                             CUDA_R_64F, nullptr, CUDA_R_64F, nullptr, 1, CUDA_R_64F, nullptr, k,
-                                            CUDA_R_64F, &d2, &h2));
+                                            CUDA_R_64F, &d4, &h4));
+    d2 = std::max(d2, d4);
+    h2 = std::max(h2, h4);
     if (w.method == LSRN_SVD_POLAR)
       LSRN_SOLVER(cusolverDnXgesvdp_bufferSize(c->solver, c->params, CUSOLVER_EIG_MODE_VECTOR, 1, k, k, CUDA_R_64F,
                                                nullptr, k, CUDA_R_64F, nullptr, CUDA_R_64F, nullptr, k, CUDA_R_64F,
@@ -754,7 +765,7 @@ SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   w.host_bytes = std::max({h1, h2, h3});
   w.W1 = ar.take<double>((size_t)d.s * k);
   w.tau = ar.take<double>((size_t)k);
-  const int nblk = w.method == LSRN_SVD_JW ? 4 : (w.method == LSRN_SVD_POLAR ? 3 : 2);
+  const int nblk = (w.method == LSRN_SVD_JW || w.fallback_jw) ? 4 : (w.method == LSRN_SVD_POLAR ? 3 : 2);
   w.JW = ar.take<double>((size_t)nblk * k * k);
   w.S = ar.take<double>((size_t)2 * k);
   w.Sd = ar.take<double>((size_t)k);
@@ -813,7 +824,7 @@ int64_t svd_local(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, 
     c->launches++;
     return r;
   };
-  if (w.method == LSRN_SVD_JW) {
+  auto jw = [&]() {
     int64_t meig = k;
     double vl = 0.0, vu = 0.0;
     LSRN_CUDA(launch_build_jw(w.W1, d.s, k, w.JW, st));
@@ -831,7 +842,8 @@ int64_t svd_local(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, 
     LSRN_CUDA(launch_form_nt_jw(w.JW, 2 * k, w.S, k, r, w.Nt, st));
     c->launches++;
     return r;
-  }
+  };
+  if (w.method == LSRN_SVD_JW) return jw();
   if (w.method == LSRN_SVD_POLAR) {
     double* Up = w.JW + (size_t)k * k;
     double* Vp = w.JW + 2 * (size_t)k * k;
@@ -856,6 +868,7 @@ int64_t svd_local(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, 
       return rank_of(S_host, d.s, k);
     }
     c->svd_polar_fallbacks++;
+    if (w.fallback_jw) return jw();
   }
   return gesvd();
 }
@@ -1290,6 +1303,11 @@ extern "C" {
 
 lsrn_status lsrn_last_stats(lsrn_ctx* c, double* out, int cap) {
   if (!c || !out) return set_error(LSRN_EINVAL, "NULL argument");
+  if (c->sketch_pending) {
+    c->sketch_pending = false;
+    cudaEventSynchronize(c->ev[2]);
+    c->stats[0] = elapsed_s(c->ev[1], c->ev[2]) * 1e3;
+  }
   if (c->stats_pending) {
     c->stats_pending = false;
     double lp = 0.0;
@@ -1823,6 +1841,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     }
     // ---- stats
     c->stats[0] = elapsed_s(c->ev[1], c->ev[2]) * 1e3;
+    c->sketch_pending = false;
     // per-pass kernel times are read lazily by lsrn_last_stats (the events stay valid
     // until the next call): no host work between back-to-back solves
     c->stats_pending = true;
@@ -1895,6 +1914,7 @@ lsrn_status lsrn_sketch(lsrn_ctx* c, const lsrn_matrix* A, double gamma, double 
     c->stats_pending = false;
     c->stats[1] = c->stats[4] = 0.0;
     sketch_stage(c, A, A, PL, seed, 0, ws, At);   // At is written by its last step only
+    c->sketch_pending = true;                      // stats[0] read lazily from ev[1], ev[2]
     c->stats[6] = 2.0 * (double)d.s * (double)d.k * (double)d.cnt;
     if (s_out) *s_out = d.s;
     return LSRN_OK;

@@ -168,18 +168,19 @@ def test_single_column_or_row(ctx, shape):
 @pytest.mark.parametrize("name", ["c2", "c3"])
 @pytest.mark.parametrize("method", ["gesvd", "polar"])
 def test_svd_methods_small(ctx, name, method):
-    """The SVD methods used when the Jordan-Wielandt matrix exceeds cuSOLVER's limit
-    (k > 16384, c4): polar (gesvdp of R, accepted only for clearly full-rank R) and
-    gesvd of R, forced at small size: same rank, counts and solution as the oracle
-    (rank-deficient c2 -- where the polar result must be rejected and redone with
-    gesvd -- and Tikhonov c3)."""
+    """The SVD methods of the large-k configs, forced at small size: polar (gesvdp of R,
+    the default from k = 4096, accepted only for clearly full-rank R) and gesvd of R (the
+    fallback above the Jordan-Wielandt limit, k > 16384): same rank, counts and solution
+    as the oracle (rank-deficient c2 -- where the polar result must be rejected and
+    redone -- and Tikhonov c3)."""
     p = small(name)
     A = p.dense_A().numpy()
     b = p.b.numpy()
     with ctx.options(svd=method):
         x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs", lam=p.lam)
-    # c2's sketch has rank 1800 < k: the polar result is rejected and redone with gesvd
-    assert rep["svd_used"] == (2 if method == "gesvd" or name == "c2" else 3)
+    # c2's sketch has rank 1800 < k: the polar result is rejected and redone with the
+    # Jordan-Wielandt eigensolver (k <= 16384)
+    assert rep["svd_used"] == (2 if method == "gesvd" else (1 if name == "c2" else 3))
     orc = orc_solve(A, b, solver="cs", lam=p.lam)
     assert rep["r"] == orc["r"] and rep["iters"] == orc["iters"]
     sv = np.linalg.svd(A, compute_uv=False)

@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out/r02
+python -m pytest tests/test_gpu_csr.py -m gpu -x -q -p no:cacheprovider -k "sketch" > gpurun_out/r02/pytest_csr.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r02/pytest_csr.log
+tail -3 gpurun_out/r02/pytest_csr.log
+python tools/diag/csr_sketch_variants.py t4 3 > gpurun_out/r02/slab_t4.jsonl 2>&1
+cat gpurun_out/r02/slab_t4.jsonl
