@@ -29,9 +29,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "lsrn_solve_s"
 UNIT = "s"
-FP64_PEAK_TFLOPS = 36.9     # DMMA.8x8x4 burst peak measured on this pool (profiles/fp64_peak.jsonl)
-FP64_PEAK_NOTE = ("fp64 DMMA peak measured by tools/microbench/fp64_peak.cu on this pool's B200 "
-                  "(MEASURED_PEAKS.json has no fp64 entry); cuBLAS DGEMM 8192^3 measured 35.4")
+FP64_PEAK_TFLOPS = 37.2     # DMMA.8x8x4 sustained 12 s at 1965 MHz (profiles/r02_fp64_sustained.jsonl)
+FP64_PEAK_NOTE = ("fp64 DMMA peak measured on this pool's B200 (MEASURED_PEAKS.json has no fp64 entry): "
+                  "mma.sync m8n8k4 back to back for 12 s, 37.2 TFLOP/s at 1965 MHz, no throttle "
+                  "(tools/microbench/fp64_sustained.cu, profiles/r02_fp64_sustained.jsonl; burst 36.9, "
+                  "cuBLAS DGEMM 8192^3 sustained 35.5)")
 DFMA_PEAK_TFLOPS = 36.8     # DFMA (FP64 ALU) peak measured by the same microbenchmark
 DFMA_PEAK_NOTE = "fp64 DFMA peak measured by tools/microbench/fp64_peak.cu (profiles/r01_fp64_peak.jsonl)"
 
@@ -186,21 +188,27 @@ def cpu_baseline(cfg_name, solver, sample_rows=1024, svd_k=2000, full_max=2.5e8)
     s = pl["s"]
     rows = min(sample_rows, L)
     p = make_problem(cfg_name, shard=(0, rows))
+    import scipy.sparse as sp
     if p.kind == "csr":
-        import scipy.sparse as sp
         X = sp.csr_matrix((p.val.numpy(), p.colind.numpy(), p.rowptr.numpy()), shape=(rows, k))
     else:
         X = p.X.numpy()
     ta = time.perf_counter()
     orc_sketch(X, s, SKETCH_SEED, pl["sigma_x"], 0.0)
     t_sk = (time.perf_counter() - ta) * L / rows
+    # SVD: the oracle's factor() of the sketch of a k' = svd_k column instance of the same
+    # recipe (same column / row scaling, so the same conditioning: the Jacobi sweep count
+    # depends on it), then scaled by (k / k')^3 at fixed gamma
     kp = min(svd_k, k)
     sp_ = int(math.ceil(cfg["gamma"] * kp))
-    G = np.random.default_rng(0).standard_normal((sp_, kp))
+    ps = make_problem(cfg_name, m=2 * sp_, n=kp) if m >= n else make_problem(cfg_name, m=kp, n=2 * sp_)
+    Xs = (sp.csr_matrix((ps.val.numpy(), ps.colind.numpy(), ps.rowptr.numpy()), shape=(2 * sp_, kp))
+          if ps.kind == "csr" else ps.X.numpy())
+    Ats = orc_sketch(Xs, sp_, SKETCH_SEED, 1.0, 0.0)
     ta = time.perf_counter()
-    factor(G)
+    factor(Ats)
     t_svd = (time.perf_counter() - ta) * (k / kp) ** 3
-    del G
+    del Xs, Ats, ps
     r = k
     alpha = bounds.default_alpha(s)
     sl, su = bounds.sigma_bounds(s, r, alpha)
@@ -222,7 +230,8 @@ def cpu_baseline(cfg_name, solver, sample_rows=1024, svd_k=2000, full_max=2.5e8)
     return {"value": t_sk + t_svd + t_it, "unit": UNIT, "cores": _blas_threads(), "kind": "oracle",
             "host": host_info(),
             "sample": (f"oracle stages on pieces of {cfg_name} scaled by operation count: sketch of the first "
-                       f"{rows} of L={L} rows x{L / rows:.0f} ({t_sk:.0f}s); SVD (factor) of a {sp_}x{kp} sketch "
+                       f"{rows} of L={L} rows x{L / rows:.0f} ({t_sk:.0f}s); SVD (factor) of the {sp_}x{kp} sketch of a "
+                       f"{kp}-column instance of the recipe "
                        f"x(k/{kp})^3 ({t_svd:.0f}s); {passes} passes of the operator pair, long side x{L / rows:.0f} "
                        f"plus a {k}x{k} N ({t_it:.0f}s)"),
             "stages_s": {"sketch": t_sk, "svd": t_svd, "iterations": t_it},
@@ -267,7 +276,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=512)
-    ap.add_argument("--ref-svd-k", type=int, default=1500)
+    ap.add_argument("--ref-svd-k", type=int, default=1024)
     ap.add_argument("--cpu-rows", type=int, default=1024)
     ap.add_argument("--cpu-svd-k", type=int, default=2000)
     args = ap.parse_args()

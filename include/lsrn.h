@@ -201,7 +201,9 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *   LSRN_OPT_SKETCH_NSPLIT  split-K factor of the dense sketch (>= 1)
  *   LSRN_OPT_ROWPASS_*      row-pass plan fields
  *   LSRN_OPT_CSR_ROWDOT     CSR long pass: 0 heavy-dense + light-CSR, 8 rows per step;
- *                           1 warp per row over the full CSR; 2 as 0 with 2 rows per step
+ *                           1 warp per row over the full CSR; 2 as 0 with 2 rows per step;
+ *                           3 the two-kernel form (row dots, then A^T u gathered from the
+ *                           CSC copy) also for k <= 2048
  *   LSRN_OPT_CSR_SKETCH     CSR sketch light part: 0 column-stationary (per nonzero),
  *                           1 generate-once row-stationary slab */
 enum {

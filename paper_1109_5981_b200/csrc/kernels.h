@@ -12,7 +12,8 @@ namespace lsrn {
 // the arithmetic.  The context's overrides are installed for the duration of an
 // API call (OverrideScope) and read by the host-side planners through ovr().
 struct Overrides {
-  int sketch_kernel = -1;     // 0 warp-specialized DMMA (sketch_ws.cu), 1 non-specialized (sketch_dense.cu)
+  int sketch_kernel = -1;     // 0 warp-specialized DMMA (sketch_ws.cu), 1 non-specialized (sketch_dense.cu),
+                              // 2 DMMA warps generating G themselves (sketch_cg_kernel)
   int sketch_tile = -1;       // 0: 64 x 256 tile, 1: 32 x 512 tile
   int sketch_maxcl = -1;      // cap on the G-sharing cluster size along N
   int sketch_nsplit = -1;     // split-K factor (>= 1)
@@ -25,7 +26,8 @@ struct Overrides {
   int rowpass_tr = -1;        // wide rows: rows per tile (1 or 2)
   int rowpass_budget_kb = -1; // shared-memory stage budget
   int rowpass_wide_slice = -1;// wide rows: max columns per CTA slice
-  int csr_rowdot = -1;        // 0 heavy-dense + light-CSR 8 rows/step, 1 warp per row (full CSR), 2 hl 2 rows/step
+  int csr_rowdot = -1;        // 0 heavy-dense + light-CSR 8 rows/step, 1 warp per row (full CSR), 2 hl 2 rows/step,
+                              // 3 the two-kernel form (row dots + CSC gather) also for k <= 2048
   int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch
 };
 const Overrides& ovr();

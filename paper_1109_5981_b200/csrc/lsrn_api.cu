@@ -990,7 +990,7 @@ struct Pass {
     a.wpart = cw->wpart;
     a.done = done;
     a.ND = cw->ND;
-    if (d.k <= csr_rowdot_all_max_k()) {
+    if (d.k <= csr_rowdot_all_max_k() && ovr().csr_rowdot != 3) {
       // single pass: w for every column accumulated in shared memory, then the fixed-order block sum
       a.nblocks = csr_rowdot_all_blocks(c->nsm, d.k);
       LSRN_CUDA(launch_csr_rowdot_all(a, d.k, st));
@@ -1263,7 +1263,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_HOSTIO_CHUNK_MB: if (!in(1, 1 << 20)) return bad(); c->hostio_chunk_mb = (double)value; break;
     case LSRN_OPT_LSQR_SYNC: if (!in(0, 1)) return bad(); c->lsqr_sync = (int)value; break;
     case LSRN_OPT_BCAST_N: if (!in(0, 1)) return bad(); c->bcast_n = value != 0; break;
-    case LSRN_OPT_SKETCH_KERNEL: if (!in(-1, 1)) return bad(); o.sketch_kernel = (int)value; break;
+    case LSRN_OPT_SKETCH_KERNEL: if (!in(-1, 2)) return bad(); o.sketch_kernel = (int)value; break;
     case LSRN_OPT_SKETCH_TILE: if (!in(-1, 1)) return bad(); o.sketch_tile = (int)value; break;
     case LSRN_OPT_SKETCH_MAXCL: if (!in(-1, 4)) return bad(); o.sketch_maxcl = (int)value; break;
     case LSRN_OPT_SKETCH_NSPLIT: if (!in(-1, 64) || value == 0) return bad(); o.sketch_nsplit = (int)value; break;
@@ -1276,7 +1276,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_ROWPASS_TR: if (!in(-1, 2) || value == 0) return bad(); o.rowpass_tr = (int)value; break;
     case LSRN_OPT_ROWPASS_BUDGET_KB: if (!(value == -1 || in(16, 227))) return bad(); o.rowpass_budget_kb = (int)value; break;
     case LSRN_OPT_ROWPASS_WIDE_SLICE: if (!(value == -1 || in(512, 1 << 20))) return bad(); o.rowpass_wide_slice = (int)value; break;
-    case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 2)) return bad(); o.csr_rowdot = (int)value; break;
+    case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 3)) return bad(); o.csr_rowdot = (int)value; break;
     case LSRN_OPT_CSR_SKETCH: if (!in(-1, 1)) return bad(); o.csr_sketch = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
   }
@@ -1851,8 +1851,9 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     // (k <= 2048: single pass over the CSR, no CSC read in the iterations)
     // k > 2048: the heavy block D (8 B per heavy entry, nd per row) + the light CSR (12 B per entry,
     // 8 B row pointer) + u (16 B per row) + the light CSC (12 B per entry)
-    const bool hl = d.k > csr_rowdot_all_max_k() && ovr().csr_rowdot != 1;
-    const double csc_bytes = d.k <= csr_rowdot_all_max_k() ? 0.0 : 12.0 * (double)PL.cw.nnz_light;
+    const bool two_pass = d.k > csr_rowdot_all_max_k() || ovr().csr_rowdot == 3;
+    const bool hl = two_pass && ovr().csr_rowdot != 1;
+    const double csc_bytes = two_pass ? 12.0 * (double)PL.cw.nnz_light : 0.0;
     const double nnz_b = hl ? 8.0 * (double)PL.cw.nd * (double)d.cnt + 12.0 * (double)PL.cw.nnz_light
                             : 12.0 * (double)A_in->nnz;
     c->stats[5] = PL.csr ? (nnz_b + 24.0 * (double)d.cnt + csc_bytes)

@@ -299,6 +299,163 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
   if (CL > 1) cluster_sync_all();
 }
 
+// ---------------------------------------------------------------------------
+// K2 v3 (sketch_cg_kernel): the consumers generate G themselves.
+// In sketch_ws_kernel the producer warps' FP64 instructions queue behind the
+// consumers' DMMAs on the one FP64 pipe per SM sub-partition; the producers only
+// need ~4 % of the pipe, but every dependent step of their Box-Muller chain waits
+// for it, so they fall behind and the consumers wait on the G ring (tensor pipe
+// 78.7 % active, FP64 ALU 3.6 %, profiles/r01_ncu_full_final.json).  Here there
+// are no RNG-only warps: each of the 8 DMMA warps generates its 1/8 of the G tile
+// of k-block kb + 1 (one Box-Muller pair per lane) in the same instruction stream
+// as its DMMAs for k-block kb, so a warp waiting on the FP64 pipe for its RNG
+// leaves the pipe to the other DMMA warp of its sub-partition instead of starving
+// both.  A ninth warp streams the X tiles with 1-D TMA bulk copies (3-stage ring,
+// mbarriers); G is double-buffered and the 8 DMMA warps meet at one named barrier
+// per k-block (G[kb+1] written, G[kb] read).  CTAs are rasterised M-tile-fastest,
+// so the CTAs resident at one time share their X tiles through L2 (c5: ~85 waves
+// each re-reading X from DRAM about once, against ~84x with N-fastest order).
+namespace cg {
+constexpr int BM = 32, BN = 512, BK = 16, NSX = 3;
+constexpr int A_LD = BN + 8;                 // padded X row (doubles): conflict-free B fragments
+constexpr int G_LD = BK + 4;
+constexpr int X_STAGE = BK * A_LD;
+constexpr int G_STAGE = BM * G_LD;
+constexpr int NCW = 8;                       // DMMA warps: 2 (M) x 4 (N), warp tile 16 x 128
+constexpr int THREADS = NCW * 32 + 32;       // + one TMA warp
+constexpr int MI = BM / 16, NJ = BN / 32;    // 2 x 16 fragments of 8 x 8
+constexpr size_t SMEM = sizeof(double) * (size_t)(NSX * X_STAGE + 2 * G_STAGE) + 128;
+}  // namespace cg
+
+__global__ void __launch_bounds__(cg::THREADS, 1)
+sketch_cg_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
+                 uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride,
+                 int accumulate) {
+  using namespace cg;
+  extern __shared__ __align__(128) double smem[];
+  double* Xs = smem;                                   // [NSX][BK][A_LD]
+  double* Gs = smem + NSX * X_STAGE;                   // [2][BM][G_LD]
+  __shared__ uint64_t xfull[NSX], xempty[NSX];
+  __shared__ double bmT[bm::TAB_SIZE];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;         // M-tile fastest (shared X tiles in L2)
+  const int64_t n0 = (int64_t)blockIdx.y * BN;
+  const int64_t r_begin = (int64_t)blockIdx.z * rows_per_split;
+  const int64_t r_end = min(rows, r_begin + rows_per_split);
+  const int nk = (r_end > r_begin) ? (int)((r_end - r_begin + BK - 1) / BK) : 0;
+  if (tid == 0) {
+    for (int i = 0; i < NSX; ++i) {
+      mbar_init(&xfull[i], 1);
+      mbar_init(&xempty[i], NCW);
+    }
+    mbar_fence_init();
+  }
+  for (int i = tid; i < bm::TAB_SIZE; i += THREADS) bmT[i] = bm::kTable[i];
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ---------------------------------------------------------------- X loader
+    // (no setmaxnreg: it is warpgroup-wide and this warp is alone in its warpgroup;
+    // 288 threads x 168 registers fit the register file as launched)
+    const int64_t ncols = min((int64_t)BN, k - n0);
+    const unsigned seg_bytes = (unsigned)(ncols * 8);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int sx = kb % NSX;
+      if (kb >= NSX) mbar_wait(&xempty[sx], (unsigned)(((kb / NSX) & 1) ^ 1));
+      const int64_t rbase = r_begin + (int64_t)kb * BK;
+      const int nrow = (int)min((int64_t)BK, r_end - rbase);
+      double* dst = Xs + sx * X_STAGE;
+      if (nrow < BK) {            // ragged K tail: zero the missing rows (0 x stale could be NaN)
+        for (int e = lane; e < (BK - nrow) * A_LD; e += 32) dst[nrow * A_LD + e] = 0.0;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+      }
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&xfull[sx], seg_bytes * (unsigned)nrow);
+        for (int rr = 0; rr < nrow; ++rr) bulk_g2s(dst + rr * A_LD, X + (rbase + rr) * ld + n0, seg_bytes, &xfull[sx]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ DMMA warps
+  const uint2 key = philox_key(seed);
+  const int wm = warp >> 2, wn = warp & 3;
+  // this lane's Box-Muller pair of every G tile: pair (row pair gq, column gk) of
+  // the BM x BK tile; warp w owns row pairs 2w, 2w+1 (32 pairs: 2 row pairs x 16 columns)
+  const int gq = 2 * warp + (lane >> 4), gk = lane & 15;
+  auto gen = [&](int kb, double* gdst) {
+    const int64_t rbase = r_begin + (int64_t)kb * BK;
+    double z0 = 0.0, z1 = 0.0;
+    if (rbase + gk < r_end) gaussian_pair(key, (uint64_t)(m0 / 2 + gq), (uint64_t)(lo + rbase + gk), bmT, z0, z1);
+    gdst[(2 * gq) * G_LD + gk] = z0;
+    gdst[(2 * gq + 1) * G_LD + gk] = z1;
+  };
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (nk > 0) gen(0, Gs);
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");
+  for (int kb = 0; kb < nk; ++kb) {
+    const int sx = kb % NSX;
+    const double* as = Xs + sx * X_STAGE;
+    const double* gs = Gs + (kb & 1) * G_STAGE;
+    mbar_wait(&xfull[sx], (unsigned)((kb / NSX) & 1));
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      double a[MI], b[NJ];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = gs[(wm * (BM / 2) + i * 8 + (lane >> 2)) * G_LD + ks * 4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[j] = as[(ks * 4 + (lane & 3)) * A_LD + wn * (BN / 4) + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma884(acc[i][j], a[i], b[j]);
+      // in the DMMA stream, staggered: the two DMMA warps of a sub-partition (warps w and
+      // w + 4) run their Box-Muller chains at different k-steps, so one keeps the pipe busy
+      if (ks == ((warp >> 2) & 1) * 2 && kb + 1 < nk) gen(kb + 1, Gs + ((kb + 1) & 1) * G_STAGE);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&xempty[sx]);
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");   // G[kb+1] written, G[kb] read by all
+  }
+
+  double* o = out + (int64_t)blockIdx.z * out_split_stride;
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int64_t gi = m0 + wm * (BM / 2) + i * 8 + (lane >> 2);
+    if (gi >= s) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int64_t gc = n0 + wn * (BN / 4) + j * 8 + 2 * (lane & 3);
+      if (gc + 1 < k) {
+        double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+        if (accumulate) {
+          const double2 w = *reinterpret_cast<const double2*>(o + gi * k + gc);
+          v.x = w.x + v.x;
+          v.y = w.y + v.y;
+        }
+        *reinterpret_cast<double2*>(o + gi * k + gc) = v;
+      } else if (gc < k) {
+        o[gi * k + gc] = accumulate ? o[gi * k + gc] + acc[i][j][0] : acc[i][j][0];
+      }
+    }
+  }
+}
+
+static cudaError_t launch_cg(const SketchDenseArgs& a, cudaStream_t st) {
+  using namespace cg;
+  dim3 grid((unsigned)((a.s + BM - 1) / BM), (unsigned)((a.k + BN - 1) / BN), (unsigned)a.nsplit);
+  cudaError_t e = cudaFuncSetAttribute(sketch_cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  if (e != cudaSuccess) return e;
+  sketch_cg_kernel<<<grid, THREADS, SMEM, st>>>(a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed, a.rows_per_split, a.out,
+                                                a.out_split_stride, a.accumulate);
+  return cudaGetLastError();
+}
+
 bool sketch_ws_supported(const SketchDenseArgs& a) {
   return (a.ld % 2 == 0) && (a.k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0);
 }
@@ -371,6 +528,7 @@ static cudaError_t launch_ws_tile(const SketchDenseArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st) {
+  if (ovr().sketch_kernel == 2) return launch_cg(a, st);
   return sketch_ws_tile() == 0 ? launch_ws_tile<Tile0>(a, st) : launch_ws_tile<Tile1>(a, st);
 }
 

@@ -64,11 +64,14 @@ def test_gaussian_entries(ctx):
     (2100, 2048, 1.2, 0.0, 2),      # 8 N-tiles: 8-CTA cluster, padded ld
     (1601, 1536, 1.1, 0.5, 0),      # 6 N-tiles: 2-CTA clusters, Tikhonov block, ragged K
 ])
-def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad):
+@pytest.mark.parametrize("kernel", [-1, 2])
+def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad, kernel):
+    """kernel -1: the planner's choice; 2: sketch_cg_kernel (DMMA warps generate G)."""
     g = torch.Generator().manual_seed(m * 7 + n)
     Xfull = torch.randn(m, n + ld_pad, generator=g, dtype=torch.float64)
     X = Xfull[:, :n]
-    At = ctx.sketch(X.cuda() if ld_pad == 0 else Xfull.cuda()[:, :n], m, n, gamma, lam, seed=5981).cpu().numpy()
+    with ctx.options(sketch_kernel=kernel):
+        At = ctx.sketch(X.cuda() if ld_pad == 0 else Xfull.cuda()[:, :n], m, n, gamma, lam, seed=5981).cpu().numpy()
     p = orc_plan(m, n, gamma, lam)
     ref = orc_sketch(X.numpy(), p["s"], 5981, p["sigma_x"], p["sigma_i"])
     assert At.shape == ref.shape
@@ -312,6 +315,7 @@ def test_sketch_tiles_and_clusters(ctx, tile, maxcl, n):
 
 @pytest.mark.parametrize("opts", [dict(svd="gesvd"), dict(svd="polar"), dict(rowpass_keep=0), dict(rowpass_occ=1),
                                   dict(rowpass_occ=1, rowpass_keep=1), dict(sketch_kernel=1), dict(sketch_kernel=0),
+                                  dict(sketch_kernel=2),
                                   dict(sketch_nsplit=3), dict(graph_reuse=0)])
 def test_tuning_variants_match(ctx, opts):
     """Kernel variants selected by the plan overrides (lsrn_ctx_set_option) solve c1 to the
@@ -341,12 +345,16 @@ def test_wide_rows_vs_pseudoinverse(ctx, n, opts, solver):
         x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver=solver, gamma=1.5)
     assert rep["r"] == n
     dx = x.cpu().numpy() - xstar
-    # Thm 4.5's A-norm form is kappa-free; the 2-norm carries the fp64
-    # floor ~ kappa u sqrt(n) of any two implementations (C18), here n >= 4100
+    # DESIGN.md reading C18(b), measured (profiles/r02_c18_floor.jsonl): the fp64 error of
+    # an LSRN solve against the exact x* grows like sqrt(n) at fixed kappa -- the oracle's
+    # own fp64 LSQR reaches 1.4e-12 sqrt(n) in the A-norm form of Thm 4.5 and
+    # 0.2-0.6 sqrt(n) kappa u in the 2-norm for n = 250..4100 (long-double products: 2e-13
+    # and 1e-10).  Gates: A-norm max(1e-11, 1.5e-12 sqrt n), 2-norm max(1e-9, sqrt(n) kappa u).
+    kappa = float(sig[0] / sig[-1])
     an = np.linalg.norm(sig * (V.T @ dx)) / np.linalg.norm(sig * (V.T @ xstar))
-    assert an <= 1e-10, an
+    assert an <= max(1e-11, 1.5e-12 * np.sqrt(n)), an
     rel = np.linalg.norm(dx) / np.linalg.norm(xstar)
-    assert rel <= 1e-8, rel
+    assert rel <= max(1e-9, np.sqrt(n) * kappa * U), rel
 
 
 def _edge_words(rng, n):
