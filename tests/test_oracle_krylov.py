@@ -14,6 +14,7 @@ import math
 import os
 
 import numpy as np
+import pytest
 from numpy.polynomial import chebyshev as npcheb
 
 from oracle import bounds
@@ -113,3 +114,35 @@ def test_lsqr_fixed_and_adaptive_vs_lstsq():
     lo, hi = 0.2 - 1e-12, 1.0 + 1e-12
     x = chebyshev(lambda v: A @ v, lambda u: A.T @ u, b, lo, hi, bounds.cs_passes(lo, hi, 1e-14))
     assert np.linalg.norm(x - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("kind,tol,seed", [("precond", 1e-14, 1), ("precond", 1e-10, 2), ("precond", 1e-14, 3),
+                                           ("plain", 1e-8, 4), ("plain", 1e-6, 5), ("rankdef", 1e-10, 6),
+                                           ("wide", 1e-12, 7)])
+def test_lsqr_adaptive_stop_matches_scipy(kind, tol, seed):
+    """Reading C5's adaptive mode is the Paige-Saunders stopping rule with atol = btol = tol:
+    ||r|| <= tol ||b|| + tol ||A|| ||x||  or  ||A^T r|| <= tol ||A|| ||r||, ||A|| the running
+    Frobenius estimate.  scipy.sparse.linalg.lsqr implements the same published rule (its
+    ||x|| is a recurrence estimate, conlim disabled here), so the two stop within one
+    iteration of each other on fixed operators -- a wrong ||A^T r|| estimate (e.g. a stale
+    alpha) or a wrong ||A|| would shift the count by several.  (On ill-conditioned plain
+    operators at tight tolerances the count itself is not reproducible across fp64
+    implementations -- reading C5 -- so those stay at tol >= 1e-8.)"""
+    scipy_lsqr = pytest.importorskip("scipy.sparse.linalg").lsqr
+    rng = np.random.default_rng(seed)
+    if kind == "precond":            # what LSRN iterates on: an orthonormal-ish A N (kappa ~ 6)
+        Q, _ = np.linalg.qr(rng.standard_normal((400, 60)))
+        A = Q * np.linspace(1.0, 1.0 / 6.0, 60)
+    elif kind == "plain":
+        A = rng.standard_normal((300, 40)) * np.logspace(0, -1, 40)
+    elif kind == "rankdef":
+        A = rng.standard_normal((200, 30)) @ rng.standard_normal((30, 50))[:, :50] @ np.diag(np.logspace(0, -2, 50))
+    else:
+        A = rng.standard_normal((40, 300))
+    b = rng.standard_normal(A.shape[0])
+    y, it, info = lsqr(lambda v: A @ v, lambda u: A.T @ u, b, tol=tol, max_iter=2000, mode="adaptive")
+    res = scipy_lsqr(A, b, atol=tol, btol=tol, conlim=1e300, iter_lim=2000)
+    itn = res[2]
+    assert info["converged"]
+    assert abs(it - itn) <= 1, (it, itn)
+    assert np.linalg.norm(y - res[0]) <= max(1e-6, 1e3 * tol) * np.linalg.norm(res[0])
