@@ -124,8 +124,11 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
   __shared__ double bmT[bm::TAB_SIZE];                 // Box-Muller tables (producers)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  // Without clusters the grid is M-tile-fastest: the CTAs resident at one time then
+  // share one X column stripe and read it from L2.  (N-fastest, the cluster layout,
+  // re-read X from DRAM once per M-tile: 49 TB per c5 sketch, ncu r02.)
+  const int64_t n0 = (int64_t)(CL == 1 ? blockIdx.y : blockIdx.x) * BN;
+  const int64_t m0 = (int64_t)(CL == 1 ? blockIdx.x : blockIdx.y) * BM;
   const int64_t r_begin = (int64_t)blockIdx.z * rows_per_split;
   const int64_t r_end = min(rows, r_begin + rows_per_split);
   const int nk = (r_end > r_begin) ? (int)((r_end - r_begin + BK - 1) / BK) : 0;
@@ -463,7 +466,8 @@ bool sketch_ws_supported(const SketchDenseArgs& a) {
 template <class C, int CL>
 static cudaError_t launch_ws_t(const SketchDenseArgs& a, cudaStream_t st) {
   using namespace ws;
-  dim3 grid((unsigned)((a.k + C::BN - 1) / C::BN), (unsigned)((a.s + C::BM - 1) / C::BM), (unsigned)a.nsplit);
+  const unsigned ntn = (unsigned)((a.k + C::BN - 1) / C::BN), ntm = (unsigned)((a.s + C::BM - 1) / C::BM);
+  dim3 grid(CL == 1 ? ntm : ntn, CL == 1 ? ntn : ntm, (unsigned)a.nsplit);   // see the kernel: raster order
   cudaError_t e = cudaFuncSetAttribute(sketch_ws_kernel<C, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)C::SMEM);
   if (e != cudaSuccess) return e;

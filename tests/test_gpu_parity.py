@@ -354,7 +354,7 @@ def test_wide_rows_vs_pseudoinverse(ctx, n, opts, solver):
     an = np.linalg.norm(sig * (V.T @ dx)) / np.linalg.norm(sig * (V.T @ xstar))
     assert an <= max(1e-11, 1.5e-12 * np.sqrt(n)), an
     rel = np.linalg.norm(dx) / np.linalg.norm(xstar)
-    assert rel <= max(1e-9, np.sqrt(n) * kappa * U), rel
+    assert rel <= max(1e-9, np.sqrt(n) * kappa * 2.0 ** -53), rel
 
 
 def _edge_words(rng, n):
