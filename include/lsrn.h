@@ -313,8 +313,9 @@ lsrn_status lsrn_debug_gaussian(lsrn_ctx* ctx, uint64_t seed, const int64_t* row
 /* Testing aid (K1 parity on chosen Philox outputs): for t < count, the
  * Box-Muller pair (z0, z1) of the four 32-bit Philox words words[4t .. 4t+3]
  * (w0 = words[4t] | words[4t+1] << 32, w1 = words[4t+2] | words[4t+3] << 32,
- * §8(c) C9) into out[2t], out[2t+1].  mode 0: the table-driven transform the
- * kernels use; mode 1: CUDA libm (log, sqrt, sincospi).  Device arrays. */
+ * §8(c) C9) into out[2t], out[2t+1].  mode 0: the table-driven fp64 transform
+ * (CSR sketch, Tikhonov blocks); mode 1: CUDA libm (log, sqrt, sincospi); mode 2:
+ * the integer fixed-point transform of the dense sketch.  Device arrays. */
 lsrn_status lsrn_debug_box_muller(lsrn_ctx* ctx, const uint32_t* words, int64_t count, int mode, double* out);
 
 /* Testing / tuning aid (K5/K6 parity): one fused row pass of the iterations

@@ -1937,7 +1937,7 @@ lsrn_status lsrn_solve_cs(lsrn_ctx* c, const lsrn_matrix* A, const double* b, co
 lsrn_status lsrn_debug_box_muller(lsrn_ctx* c, const uint32_t* words, int64_t count, int mode, double* out) {
   if (!c || !words || !out) return set_error(LSRN_EINVAL, "NULL argument");
   CallScope scope(c);
-  if (mode != 0 && mode != 1) return set_error(LSRN_EINVAL, "mode must be 0 (table) or 1 (libm)");
+  if (mode < 0 || mode > 2) return set_error(LSRN_EINVAL, "mode must be 0 (fp64 table), 1 (libm) or 2 (integer)");
   if (count <= 0) return LSRN_OK;
   cudaError_t e = launch_debug_box_muller(words, count, mode, out, c->stream);
   if (e != cudaSuccess) return set_error(LSRN_ECUDA, cudaGetErrorString(e));

@@ -11,6 +11,7 @@
 // counter-based stream lets every CTA (and every GPU) regenerate exactly the
 // tile it needs from (seed, i, j), so the sketch is tiling- and shard-invariant.
 #pragma once
+#include "bm_int_tables.h"
 #include "bm_tables.h"
 #include "common.cuh"
 
@@ -164,6 +165,114 @@ LSRN_DEV void box_muller_tab(uint4 o, const double* T, double& z0, double& z1) {
   z1 = rho * sn;
 }
 
+// ---- integer (fixed-point) Box-Muller (K1 v3, measured and not used by the sketch) --
+// The same transform with the polynomial work on the integer pipe, meant to take
+// the Box-Muller FP64 instructions off the pipe the dense sketch's DMMAs use:
+// there the table-driven transform's ~49 FP64-pipe instructions per pair cost 15 %
+// of the sketch (c5 shard: 1.75 s with it, 1.53 s with Philox only, 1.47 s with
+// neither).  This version needs only 8 FP64 instructions + 1 MUFU per pair, but ~250
+// integer multiply instructions (64-bit products as IMAD.WIDE chains), and the
+// sketch got slower: 2.02 s (1.95 s with only sin / cos in integers)
+// (profiles/r02_rng_cost.jsonl).  It stays as lsrn_debug_box_muller mode 2, tested
+// against the oracle.  Tables / constants: bm_int_tables.h
+// (tools/gen_bm_int_tables.py, 60 digits).  An integer model of these exact
+// operations is within 3e-16 max(1, |z|) of 60-digit references on random and
+// edge-case words.
+//   sin / cos (2 pi u2): u2 = n2 2^-53; quadrant k = n2 >> 51, table j = next 6 bits,
+//     d = low 45 bits, b = (pi/2) d 2^-51 < pi/128 in Q64 (umulhi(d << 14, K_B));
+//     sin b, cos b by Horner in Q64 (degree 7 / 8); angle addition with the Q63
+//     table values; the quadrant rotation on the results' signs.
+//   x = -2 ln u1, n1 = (w0 >> 11) + 1 = 2^e m: r = m invc_i - 1 exact in Q61
+//     (invc_i = CI_i / 512, the fp64 transform's table); x = A + B with
+//     A = 2 (53 - e) ln 2 + 2 ln invc_i (Q57 integers, A = 0 exactly when u1 -> 1)
+//     and B = -2 r log1p(r)/r, the series log1p(r)/r = sum (-r)^k / (k + 1) in Q62;
+//     B is formed in fp64 from the exact integer r, so x keeps its relative
+//     precision as u1 -> 1.
+LSRN_DEV void bm_int_load_table(uint64_t* Ts) {
+  for (int i = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); i < bmi::TAB_WORDS;
+       i += blockDim.x * blockDim.y * blockDim.z)
+    Ts[i] = bmi::kTable[i];
+}
+
+// v 2^-scale for an unsigned 64-bit v, rounded to nearest (ties to even), built from
+// the bits (no integer -> double conversion on the FP64 pipe).  v = 0 -> 0.
+LSRN_DEV double bmi_u64_to_double(uint64_t v, int scale) {
+  const int lz = __clzll(static_cast<long long>(v));
+  const uint64_t t = v << (lz & 63);
+  uint64_t m = t >> 11;                                          // 53 bits, bit 52 set
+  const uint64_t rem = t & 0x7FFull;
+  m += (rem > 0x400ull) | ((rem == 0x400ull) & (m & 1ull));      // a carry to 2^53 bumps the exponent
+  const uint64_t ex = static_cast<uint64_t>(63 - lz - scale + 1023);
+  const uint64_t bits = (ex << 52) + (m - (1ull << 52));
+  return v == 0 ? 0.0 : __longlong_as_double(static_cast<long long>(bits));
+}
+
+// the same with the sign bit set when neg (a sign flip without an FP64 instruction)
+LSRN_DEV double bmi_u64_to_double_sgn(uint64_t v, int scale, bool neg) {
+  const double d = bmi_u64_to_double(v, scale);
+  return __longlong_as_double(__double_as_longlong(d) | (static_cast<long long>(neg) << 63));
+}
+
+LSRN_DEV uint64_t bmi_mul63(uint64_t a, uint64_t b) {            // (a b) >> 63
+  return (__umul64hi(a, b) << 1) | ((a * b) >> 63);
+}
+
+LSRN_DEV void box_muller_int(uint4 o, const uint64_t* T, double& z0, double& z1) {
+  // ---- sin / cos (2 pi u2)
+  const uint64_t w1 = (static_cast<uint64_t>(o.w) << 32) | o.z;
+  const uint64_t n2 = w1 >> 11;
+  const int k = static_cast<int>(n2 >> 51);
+  const int j = static_cast<int>((n2 >> 45) & 63);
+  const uint64_t dm = n2 & ((1ull << 45) - 1);
+  const uint64_t bq = __umul64hi(dm << 14, bmi::K_B);           // b in Q64
+  const uint64_t b2 = __umul64hi(bq, bq);
+  uint64_t t = bmi::S5 - __umul64hi(b2, bmi::S7);
+  t = bmi::S3 - __umul64hi(b2, t);
+  t = __umul64hi(b2, t);
+  const uint64_t sb = (bq - __umul64hi(bq, t)) >> 1;             // sin b, Q63
+  uint64_t u = bmi::C6 - __umul64hi(b2, bmi::C8);
+  u = bmi::C4 - __umul64hi(b2, u);
+  u = bmi::C2 - __umul64hi(b2, u);
+  u = __umul64hi(b2, u);
+  const uint64_t cb = (1ull << 63) - (u >> 1);                   // cos b, Q63
+  const uint64_t sa = T[j], ca = T[64 + j];
+  const uint64_t S = bmi_mul63(sa, cb) + bmi_mul63(ca, sb);      // sin(a + b), Q63
+  const uint64_t C = bmi_mul63(ca, cb) - bmi_mul63(sa, sb);      // cos(a + b) > 0, Q63
+  // rotate by k quarter turns: (sin, cos) = (S, C), (C, -S), (-S, -C), (-C, S)
+  const double sn = bmi_u64_to_double_sgn((k & 1) ? C : S, 63, k >= 2);
+  const double cs = bmi_u64_to_double_sgn((k & 1) ? S : C, 63, k == 1 || k == 2);
+  // ---- x = -2 ln u1
+  const uint64_t w0 = (static_cast<uint64_t>(o.y) << 32) | o.x;
+  const uint64_t n1 = (w0 >> 11) + 1ull;                        // 1 .. 2^53
+  const int e = 63 - __clzll(static_cast<long long>(n1));      // 0 .. 53
+  const uint64_t mant = (n1 << ((52 - e) & 63)) & ((1ull << 52) - 1);
+  const int i = static_cast<int>(mant >> 45);
+  const int64_t R = static_cast<int64_t>(((1ull << 52) + mant) * T[256 + i]) - (1ll << 61);   // r in Q61, exact
+  const int64_t R8 = R * 8;                                      // r in Q64 (|R8| < 2^57)
+  int64_t p = bmi::PK8;                                          // log1p(r)/r by Horner, Q62
+  p = bmi::PK7 - __mul64hi(R8, p);
+  p = bmi::PK6 - __mul64hi(R8, p);
+  p = bmi::PK5 - __mul64hi(R8, p);
+  p = bmi::PK4 - __mul64hi(R8, p);
+  p = bmi::PK3 - __mul64hi(R8, p);
+  p = bmi::PK2 - __mul64hi(R8, p);
+  p = bmi::PK1 - __mul64hi(R8, p);
+  p = bmi::PK0 - __mul64hi(R8, p);
+  const uint64_t A = static_cast<uint64_t>(53 - e) * bmi::TWO_LN2_Q57 + T[128 + i];   // Q57, >= 0
+  const uint64_t aR = static_cast<uint64_t>(R < 0 ? -R : R);
+  const double mRd = bmi_u64_to_double_sgn(aR, 0, R > 0);        // -r 2^61, exact (or 1 ulp if |R| >= 2^53)
+  const double x = fma(mRd, bmi_u64_to_double(static_cast<uint64_t>(p), 122), bmi_u64_to_double(A, 57));
+  // u1 = 1 (n1 = 2^53): x = 0 -> rho = 0; bm_sqrt's own zero test replaced by an integer one
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x));
+  const double s0 = x * y0;
+  const double ee = fma(-s0, y0, 1.0);
+  const double rho0 = fma(s0 * ee, fma(ee, 0.375, 0.5), s0);    // sqrt(x), as bm_sqrt
+  const double rho = (e == 53 || __double_as_longlong(x) == 0) ? 0.0 : rho0;
+  z0 = rho * cs;
+  z1 = rho * sn;
+}
+
 LSRN_DEV uint4 philox_counter(uint2 key, uint64_t q, uint64_t j) {
   return philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(j),
                                   static_cast<uint32_t>(j >> 32), 0u), key);
@@ -172,6 +281,11 @@ LSRN_DEV uint4 philox_counter(uint2 key, uint64_t q, uint64_t j) {
 // The normal pair (G[2q, j], G[2q+1, j]); T = shared-memory copy of bm::kTable.
 LSRN_DEV void gaussian_pair(uint2 key, uint64_t q, uint64_t j, const double* T, double& z0, double& z1) {
   box_muller_tab(philox_counter(key, q, j), T, z0, z1);
+}
+
+// The same pair through the integer transform; T = shared-memory copy of bmi::kTable.
+LSRN_DEV void gaussian_pair_int(uint2 key, uint64_t q, uint64_t j, const uint64_t* T, double& z0, double& z1) {
+  box_muller_int(philox_counter(key, q, j), T, z0, z1);
 }
 
 }  // namespace lsrn

@@ -214,11 +214,14 @@ __global__ void debug_gaussian_kernel(uint64_t seed, const int64_t* __restrict__
   }
 }
 
-// Box-Muller on given Philox words (4 per entry): mode 0 table-driven, 1 libm.
+// Box-Muller on given Philox words (4 per entry): mode 0 table-driven fp64, 1 libm,
+// 2 integer fixed-point (the dense sketch's transform).
 __global__ void debug_box_muller_kernel(const uint32_t* __restrict__ words, int64_t count, int mode,
                                         double* __restrict__ out) {
   __shared__ double bmT[bm::TAB_SIZE];
+  __shared__ uint64_t bmI[bmi::TAB_WORDS];
   bm_load_table(bmT);
+  bm_int_load_table(bmI);
   __syncthreads();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -226,6 +229,8 @@ __global__ void debug_box_muller_kernel(const uint32_t* __restrict__ words, int6
     double z0, z1;
     if (mode == 0)
       box_muller_tab(o, bmT, z0, z1);
+    else if (mode == 2)
+      box_muller_int(o, bmI, z0, z1);
     else
       box_muller_libm(o, z0, z1);
     out[2 * t] = z0;

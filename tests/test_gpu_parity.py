@@ -384,10 +384,11 @@ def _edge_words(rng, n):
     return w.astype(np.uint32)
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 def test_box_muller_words_vs_oracle(ctx, mode):
-    """K1's transform (mode 0: table-driven, the kernels' path; 1: CUDA libm) on chosen
-    Philox words against the oracle's long-double Box-Muller (reading C9)."""
+    """K1's transform (mode 0: table-driven fp64, the CSR kernels' path; 1: CUDA libm;
+    2: integer fixed-point, the dense sketch's path) on chosen Philox words against the
+    oracle's long-double Box-Muller (reading C9)."""
     from oracle.gaussian import box_muller, uniforms_from_words
     rng = np.random.default_rng(17)
     w = _edge_words(rng, 20000)
