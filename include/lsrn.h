@@ -226,6 +226,7 @@ enum {
   LSRN_OPT_ROWPASS_TR = 116,
   LSRN_OPT_ROWPASS_BUDGET_KB = 117,
   LSRN_OPT_ROWPASS_WIDE_SLICE = 118,
+  LSRN_OPT_ROWPASS_PF = 119,
   LSRN_OPT_CSR_ROWDOT = 120,
   LSRN_OPT_CSR_SKETCH = 121
 };

@@ -92,6 +92,11 @@ LSRN_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+// Prefetch `bytes` (multiple of 16) at src into L2 (no completion to wait for).
+LSRN_DEV void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // 1-D bulk copy global -> this CTA's shared memory, completion on `bar` (bytes % 16 == 0).
 LSRN_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(

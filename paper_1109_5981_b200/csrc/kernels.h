@@ -26,6 +26,7 @@ struct Overrides {
   int rowpass_tr = -1;        // wide rows: rows per tile (1 or 2)
   int rowpass_budget_kb = -1; // shared-memory stage budget
   int rowpass_wide_slice = -1;// wide rows: max columns per CTA slice
+  int rowpass_pf = -1;        // L2 prefetch distance (tiles) of the bulk row pass, 0 = off
   int csr_rowdot = -1;        // 0 heavy-dense + light-CSR 8 rows/step, 1 warp per row (full CSR), 2 hl 2 rows/step,
                               // 3 the two-kernel form (row dots + CSC gather) also for k <= 2048
   int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch
@@ -87,6 +88,7 @@ struct RowPassPlan {
   int occ = 1;                      // bulk: CTAs per SM
   int async_x = 0;                  // bulk, cl > 1: pipelined st.async partial-dot exchange
   int nt = 256;                     // bulk: threads per CTA (wide rows: 256, or 512 as a tuning aid)
+  int pf = 0;                       // bulk: L2 prefetch distance in tiles beyond the ring (0 = off)
 };
 // allow_bulk = false forces the register-load kernel (tests compare both)
 RowPassPlan plan_rowpass(int64_t R, int64_t C, int64_t ld, const double* Y, int nsm, bool allow_bulk = true);

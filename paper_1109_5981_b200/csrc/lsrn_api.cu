@@ -1276,6 +1276,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_ROWPASS_TR: if (!in(-1, 2) || value == 0) return bad(); o.rowpass_tr = (int)value; break;
     case LSRN_OPT_ROWPASS_BUDGET_KB: if (!(value == -1 || in(16, 227))) return bad(); o.rowpass_budget_kb = (int)value; break;
     case LSRN_OPT_ROWPASS_WIDE_SLICE: if (!(value == -1 || in(512, 1 << 20))) return bad(); o.rowpass_wide_slice = (int)value; break;
+    case LSRN_OPT_ROWPASS_PF: if (!in(-1, 8)) return bad(); o.rowpass_pf = (int)value; break;
     case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 3)) return bad(); o.csr_rowdot = (int)value; break;
     case LSRN_OPT_CSR_SKETCH: if (!in(-1, 1)) return bad(); o.csr_sketch = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
@@ -1681,7 +1682,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     auto kplan = [&](const RowPassPlan& q) {
       for (int64_t v : {(int64_t)q.vpt, (int64_t)q.cl, (int64_t)q.tr, (int64_t)q.nclusters, (int64_t)q.vec,
                         q.rows_per_cluster, (int64_t)q.bulk, q.cq, (int64_t)q.nst, (int64_t)q.keep, (int64_t)q.occ,
-                        (int64_t)q.async_x, (int64_t)q.nt})
+                        (int64_t)q.async_x, (int64_t)q.nt, (int64_t)q.pf})
         ki(v);
     };
     kp(A.val), kp(A.rowptr), kp(A.colind), kp(ws), kp(b), kp(x), kp(c->pass_ev.empty() ? nullptr : c->pass_ev.data());

@@ -47,7 +47,7 @@ constexpr int kMaxStages = 8;
 // doubles per thread) instead of re-reading shared memory; OCC: CTAs per SM.
 template <int P, int TR, bool KEEP, int OCC, int NT = THREADS>
 __global__ void __launch_bounds__(NT, OCC)
-rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq, int nst) {
+rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq, int nst, int pf) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kMaxStages];
   constexpr int NWARP_ = NT / 32;
@@ -83,6 +83,12 @@ rowpass_bulk_kernel(RowPassArgs a, int64_t rows_per_cluster, int CL, int64_t Cq,
     mbar_arrive_expect_tx(&full[st], row_bytes * (unsigned)nr);
     for (int tr = 0; tr < nr; ++tr)
       bulk_g2s(stage + ((int64_t)st * TR + tr) * stage_ld, a.Y + (rb + tr) * a.ld + c0, row_bytes, &full[st]);
+    // L2 prefetch `pf` tiles beyond the one just issued: with only two shared-memory
+    // stages of 80 KB rows (c5) the DRAM latency of the next refill is otherwise exposed
+    if (pf > 0) {
+      const int64_t pb = rb + (int64_t)pf * TR;
+      for (int tr = 0; tr < TR && pb + tr < r1; ++tr) bulk_prefetch_l2(a.Y + (pb + tr) * a.ld + c0, row_bytes);
+    }
   };
 
   if (tid == 0) {
@@ -473,6 +479,12 @@ bool plan_rowpass_bulk(int64_t R, int64_t C, int64_t ld, const double* Y, int ns
   if (ov.rowpass_keep >= 0) keep = ov.rowpass_keep != 0 && vpt * tr <= 16;
   p->keep = keep ? 1 : 0;
   p->occ = occ;
+  // L2 prefetch distance (tiles beyond the shared-memory ring) for two-stage rings:
+  // c5's 80 KB rows, 125000 x 1e4 through lsrn_debug_rowpass: pf 0 / 1 / 2 / 3 ->
+  // 5.80 / 7.04 / 6.99 / 6.27 TB/s (profiles/r02_rowpass_pf.jsonl; a read-only stream
+  // exceeds the 6.46 TB/s measured for a copy); deeper rings gain nothing (c2: 6.49 either way)
+  p->pf = nst <= 2 ? 1 : 0;
+  if (ov.rowpass_pf >= 0) p->pf = ov.rowpass_pf;
   p->nt = 256;
   // wide rows: pipelined asynchronous partial-dot exchange (override rowpass_asyncx = 0: cluster barrier per tile)
   p->async_x = 1;
@@ -543,7 +555,7 @@ static cudaError_t launch_bulk_k(const RowPassArgs& a, const RowPassPlan& p, cud
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, p.rows_per_cluster, p.cl, p.cq, p.nst);
+  return cudaLaunchKernelEx(&cfg, kern, a, p.rows_per_cluster, p.cl, p.cq, p.nst, p.pf);
 }
 
 template <int P, int TR, int OCC, int NT = THREADS>
