@@ -97,6 +97,13 @@ LSRN_DEV void bulk_prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// L2 prefetch of [begin, end) rounded out to 16-byte boundaries (empty ranges ignored).
+LSRN_DEV void prefetch_l2_range(const void* begin, const void* end) {
+  const uintptr_t b = reinterpret_cast<uintptr_t>(begin) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(end) + 15) & ~uintptr_t(15);
+  if (e > b) bulk_prefetch_l2(reinterpret_cast<const void*>(b), static_cast<unsigned>(e - b));
+}
+
 // 1-D bulk copy global -> this CTA's shared memory, completion on `bar` (bytes % 16 == 0).
 LSRN_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
