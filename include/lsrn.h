@@ -199,7 +199,10 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *   LSRN_OPT_SKETCH_TILE    0: 64 x 256 tile, 1: 32 x 512 tile (default)
  *   LSRN_OPT_SKETCH_MAXCL   cap on the G-sharing cluster size
  *   LSRN_OPT_SKETCH_NSPLIT  split-K factor of the dense sketch (>= 1)
- *   LSRN_OPT_ROWPASS_*      row-pass plan fields
+ *   LSRN_OPT_SKETCH_X_L2    1: X tiles of the dense sketch loaded with an L2 evict_last policy
+ *   LSRN_OPT_SKETCH_CHUNKS  dense sketch of a device-resident A: number of row chunks
+ *                           launched in stream order (default: one per 4 GB of A, <= 16)
+ *   LSRN_OPT_ROWPASS_*      row-pass plan fields; _PF: L2 prefetch distance
  *   LSRN_OPT_CSR_ROWDOT     CSR long pass: 0 heavy-dense + light-CSR, 8 rows per step;
  *                           1 warp per row over the full CSR; 2 as 0 with 2 rows per step;
  *                           3 the two-kernel form (row dots, then A^T u gathered from the
@@ -217,6 +220,8 @@ enum {
   LSRN_OPT_SKETCH_TILE = 101,
   LSRN_OPT_SKETCH_MAXCL = 102,
   LSRN_OPT_SKETCH_NSPLIT = 103,
+  LSRN_OPT_SKETCH_X_L2 = 104,
+  LSRN_OPT_SKETCH_CHUNKS = 105,
   LSRN_OPT_ROWPASS_KEEP = 110,
   LSRN_OPT_ROWPASS_OCC = 111,
   LSRN_OPT_ROWPASS_WIDE1 = 112,

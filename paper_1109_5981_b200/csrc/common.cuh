@@ -97,6 +97,21 @@ LSRN_DEV void bulk_prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// An L2 cache policy "evict last" for the whole access (createpolicy), and a 1-D bulk
+// copy global -> shared that carries it: for data several CTAs re-read through L2.
+LSRN_DEV uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+LSRN_DEV void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // L2 prefetch of [begin, end) rounded out to 16-byte boundaries (empty ranges ignored).
 LSRN_DEV void prefetch_l2_range(const void* begin, const void* end) {
   const uintptr_t b = reinterpret_cast<uintptr_t>(begin) & ~uintptr_t(15);

@@ -17,6 +17,8 @@ struct Overrides {
   int sketch_tile = -1;       // 0: 64 x 256 tile, 1: 32 x 512 tile
   int sketch_maxcl = -1;      // cap on the G-sharing cluster size along N
   int sketch_nsplit = -1;     // split-K factor (>= 1)
+  int sketch_x_l2 = -1;       // 1: X tiles loaded with an L2 evict_last policy
+  int sketch_chunks = -1;     // device-resident A: row chunks launched one after the other (0/1 = one launch)
   int rowpass_keep = -1;      // 0/1: re-read / register-kept row tile
   int rowpass_occ = -1;       // 1/2 CTAs per SM
   int rowpass_wide1 = -1;     // 0 disables the single 512-thread CTA plan for 8192 < k <= 10240

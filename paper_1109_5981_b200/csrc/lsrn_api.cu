@@ -267,6 +267,7 @@ struct SketchWs {
   // nsplit inside the chunk) as soon as it lands and accumulated into the nsplit partials
   int nchunk = 0;
   int64_t chunk_r0[kMaxChunks + 1] = {};   // chunk i = rows [chunk_r0[i], chunk_r0[i+1])
+  bool host_stream = false;                 // chunks wait on their H2D copy events
 };
 
 // Host-IO streaming: A is copied in chunks of >= 128 MB on a second stream and
@@ -298,6 +299,31 @@ SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_fla
   SketchWs w{};
   if (host_stream && d.cnt > 0) {
     w.nchunk = stream_chunks(d, ld, c->hostio_chunk_mb, w.chunk_r0);
+    if (w.nchunk > 1) {
+      w.host_stream = true;
+      w.nsplit = 1;
+      for (int i = 0; i < w.nchunk; ++i)
+        w.nsplit = std::max(w.nsplit, choose_nsplit(d.s, d.k, w.chunk_r0[i + 1] - w.chunk_r0[i], c->nsm));
+      w.part = ar.take<double>((size_t)w.nsplit * d.s * d.k);
+      return w;
+    }
+    w.nchunk = 0;
+  }
+  // Device-resident A larger than 4 GB: one launch per row chunk of <= 4 GB (<= 16
+  // chunks), accumulated in stream order.  Within a launch the resident CTAs (one X
+  // column stripe, M-tile-fastest raster) read the same rows at nearly the same time
+  // and share them through L2; one launch over all of c5's 1e6 rows let them drift
+  // apart (each CTA runs ~170 ms) and re-read X from DRAM 27 TB per sketch.
+  const double a_bytes = 8.0 * (double)d.cnt * (double)ld;
+  int nch = (int)std::ceil(a_bytes / 4.0e9);
+  if (ovr().sketch_chunks >= 0) nch = ovr().sketch_chunks;
+  nch = std::min(nch, kMaxChunks);
+  if (d.cnt > 0 && nch > 1 && d.cnt >= 16 * (int64_t)nch) {
+    int64_t per = (d.cnt + nch - 1) / nch;
+    per = (per + 15) / 16 * 16;
+    w.nchunk = 0;
+    for (int64_t row = 0; row < d.cnt && w.nchunk < kMaxChunks; row += per) w.chunk_r0[w.nchunk++] = row;
+    w.chunk_r0[w.nchunk] = d.cnt;
     if (w.nchunk > 1) {
       w.nsplit = 1;
       for (int i = 0; i < w.nchunk; ++i)
@@ -516,13 +542,13 @@ void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double*
 // Raw sketch S0 = G[:, lo:lo+cnt] X_shard of a dense shard (split-K partials summed in fixed order).
 void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed, const SketchWs& w, double* At) {
   cudaStream_t st = c->stream;
-  if (w.nchunk > 1) {          // one launch per H2D chunk, each after its copy event
+  if (w.nchunk > 1) {          // one launch per row chunk (host IO: each after its copy event)
     LSRN_CUDA(launch_fill(w.part, 0.0, (int64_t)w.nsplit * d.s * d.k, st));
     c->launches++;
     for (int i = 0; i < w.nchunk; ++i) {
       const int64_t r0 = w.chunk_r0[i];
       const int64_t nr = w.chunk_r0[i + 1] - r0;
-      LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[i], 0));
+      if (w.host_stream) LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[i], 0));
       SketchDenseArgs a{};
       a.X = A->val + r0 * A->ld;
       a.ld = A->ld;
@@ -1266,6 +1292,8 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_SKETCH_KERNEL: if (!in(-1, 2)) return bad(); o.sketch_kernel = (int)value; break;
     case LSRN_OPT_SKETCH_TILE: if (!in(-1, 1)) return bad(); o.sketch_tile = (int)value; break;
     case LSRN_OPT_SKETCH_MAXCL: if (!in(-1, 4)) return bad(); o.sketch_maxcl = (int)value; break;
+    case LSRN_OPT_SKETCH_X_L2: if (!in(-1, 1)) return bad(); o.sketch_x_l2 = (int)value; break;
+    case LSRN_OPT_SKETCH_CHUNKS: if (!in(-1, 16)) return bad(); o.sketch_chunks = (int)value; break;
     case LSRN_OPT_SKETCH_NSPLIT: if (!in(-1, 64) || value == 0) return bad(); o.sketch_nsplit = (int)value; break;
     case LSRN_OPT_ROWPASS_KEEP: if (!in(-1, 1)) return bad(); o.rowpass_keep = (int)value; break;
     case LSRN_OPT_ROWPASS_OCC: if (!in(-1, 2) || value == 0) return bad(); o.rowpass_occ = (int)value; break;
@@ -1445,7 +1473,7 @@ void sketch_stage(lsrn_ctx* c, const lsrn_matrix* A_user, const lsrn_matrix* A, 
       run_sketch(c, A, d, seed, P.sw, P.S0);
   }
   // streamed host IO: everything after the sketch reads all of A
-  if (P.sw.nchunk > 1) LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[P.sw.nchunk - 1], 0));
+  if (P.sw.host_stream && P.sw.nchunk > 1) LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[P.sw.nchunk - 1], 0));
   LSRN_CUDA(cudaEventRecord(c->ev[2], st));
   if (!reuse) {
     allreduce(c, P.S0, d.s * d.k);
@@ -1475,7 +1503,7 @@ lsrn_matrix stage_inputs(lsrn_ctx* c, const lsrn_matrix* A_in, const lsrn_opts* 
     A.rowptr = P.rpstage;
     A.colind = P.cistage;
     A.val = P.Astage;
-  } else if (P.sw.nchunk > 1) {
+  } else if (P.sw.host_stream && P.sw.nchunk > 1) {
     // chunks on the copy stream (after everything already queued on the main stream,
     // which may still read the staging buffer); the sketch waits per chunk
     LSRN_CUDA(cudaEventRecord(c->io_ev, st));
@@ -1545,7 +1573,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     if (o->flags & LSRN_HOST_IO) {
       // streamed A: b goes first on the copy stream (st waits for the last chunk of A
       // before the iterations); st itself then issues no H2D copy the sketch could queue behind
-      cudaStream_t bs = PL.sw.nchunk > 1 ? c->copy_stream : st;
+      cudaStream_t bs = (PL.sw.host_stream && PL.sw.nchunk > 1) ? c->copy_stream : st;
       if (bs != st) {
         LSRN_CUDA(cudaEventRecord(c->io_ev, st));
         LSRN_CUDA(cudaStreamWaitEvent(bs, c->io_ev, 0));

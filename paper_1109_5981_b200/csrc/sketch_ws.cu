@@ -112,7 +112,7 @@ template <class C, int CL>
 __global__ void __launch_bounds__(ws::THREADS, 1)
 sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
                  uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride,
-                 int accumulate) {
+                 int accumulate, int x_evict_last) {
   using namespace ws;
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, NSX = C::NSX, NSG = C::NSG;
   constexpr int A_LD = C::A_LD, G_LD = C::G_LD, X_STAGE = C::X_STAGE, G_STAGE = C::G_STAGE;
@@ -170,6 +170,7 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
     const int row0 = (int)qrank * SLICE_ROWS + warp * ROWS_W;   // first G row of this warp in the tile
     const int64_t ncols = min((int64_t)BN, k - n0);      // even (k even, n0 multiple of BN)
     const unsigned seg_bytes = (unsigned)(ncols * 8);
+    const uint64_t xpol = x_evict_last ? l2_policy_evict_last() : 0ull;
     for (int kb = 0; kb < nk; ++kb) {
       const int sx = kb % NSX, sg = kb % NSG;
       const unsigned px = (unsigned)(((kb / NSX) & 1) ^ 1), pg = (unsigned)(((kb / NSG) & 1) ^ 1);
@@ -185,7 +186,12 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
         }
         if (lane == 0) {
           mbar_arrive_expect_tx(&xfull[sx], seg_bytes * (unsigned)nrow);
-          for (int rr = 0; rr < nrow; ++rr) bulk_g2s(dst + rr * A_LD, X + (rbase + rr) * ld + n0, seg_bytes, &xfull[sx]);
+          if (x_evict_last) {
+            for (int rr = 0; rr < nrow; ++rr)
+              bulk_g2s_hint(dst + rr * A_LD, X + (rbase + rr) * ld + n0, seg_bytes, &xfull[sx], xpol);
+          } else {
+            for (int rr = 0; rr < nrow; ++rr) bulk_g2s(dst + rr * A_LD, X + (rbase + rr) * ld + n0, seg_bytes, &xfull[sx]);
+          }
         }
       }
       // G stage sg must be free on every CTA of the cluster, and (CL > 1) the bulk
@@ -484,7 +490,8 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<C, CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
-                            a.rows_per_split, a.out, a.out_split_stride, a.accumulate);
+                            a.rows_per_split, a.out, a.out_split_stride, a.accumulate,
+                            ovr().sketch_x_l2 == 1 ? 1 : 0);
 }
 
 // Tile shape (override sketch_tile).  Measured on c2 (1e5 x 2000,

@@ -64,13 +64,14 @@ def test_gaussian_entries(ctx):
     (2100, 2048, 1.2, 0.0, 2),      # 8 N-tiles: 8-CTA cluster, padded ld
     (1601, 1536, 1.1, 0.5, 0),      # 6 N-tiles: 2-CTA clusters, Tikhonov block, ragged K
 ])
-@pytest.mark.parametrize("kernel", [-1, 2])
-def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad, kernel):
-    """kernel -1: the planner's choice; 2: sketch_cg_kernel (DMMA warps generate G)."""
+@pytest.mark.parametrize("kernel,chunks", [(-1, -1), (2, -1), (-1, 4)])
+def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad, kernel, chunks):
+    """kernel -1: the planner's choice; 2: sketch_cg_kernel (DMMA warps generate G);
+    chunks 4: the device-resident A sketched in 4 stream-ordered row chunks."""
     g = torch.Generator().manual_seed(m * 7 + n)
     Xfull = torch.randn(m, n + ld_pad, generator=g, dtype=torch.float64)
     X = Xfull[:, :n]
-    with ctx.options(sketch_kernel=kernel):
+    with ctx.options(sketch_kernel=kernel, sketch_chunks=chunks):
         At = ctx.sketch(X.cuda() if ld_pad == 0 else Xfull.cuda()[:, :n], m, n, gamma, lam, seed=5981).cpu().numpy()
     p = orc_plan(m, n, gamma, lam)
     ref = orc_sketch(X.numpy(), p["s"], 5981, p["sigma_x"], p["sigma_i"])
@@ -315,7 +316,8 @@ def test_sketch_tiles_and_clusters(ctx, tile, maxcl, n):
 
 @pytest.mark.parametrize("opts", [dict(svd="gesvd"), dict(svd="polar"), dict(rowpass_keep=0), dict(rowpass_occ=1),
                                   dict(rowpass_occ=1, rowpass_keep=1), dict(sketch_kernel=1), dict(sketch_kernel=0),
-                                  dict(sketch_kernel=2),
+                                  dict(sketch_kernel=2), dict(sketch_chunks=3), dict(sketch_x_l2=1),
+                                  dict(rowpass_pf=0), dict(rowpass_pf=2),
                                   dict(sketch_nsplit=3), dict(graph_reuse=0)])
 def test_tuning_variants_match(ctx, opts):
     """Kernel variants selected by the plan overrides (lsrn_ctx_set_option) solve c1 to the
