@@ -139,3 +139,75 @@ def test_two_ranks_match_oracle(case):
     assert rel <= max(1e-9, 20 * kappa * U_), rel
     an = np.linalg.norm(Aop @ (x - orc["x"])) / np.linalg.norm(Aop @ orc["x"])
     assert an <= 1e-11, an
+
+
+def _worker_full(rank, world, port, name, solver, q):
+    """Full-size: rank p generates only its shard of the config (synth's block-seeded
+    recipe, bytes identical to the same rows of the whole matrix) and solves through
+    the library's sharded path with host-staged collectives."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1109_5981_b200 import dist as ldist
+        from synth.generate import CONFIGS, SKETCH_SEED, make_problem
+        torch.cuda.set_device(0)
+        cfg = CONFIGS[name]
+        L = max(cfg["m"], cfg["n"])
+        lo, hi = ldist.shard_bounds(L, world, rank)
+        p = make_problem(name, device="cuda", shard=(lo, hi))
+        ctx = ldist.host_context()
+        x, rep = ctx.solve(p.X, p.b, p.m, p.n, solver=solver, lo=lo, cnt=hi - lo, seed=SKETCH_SEED)
+        # normal equations on this shard: A_p^T (b_p - A_p x), summed over the ranks
+        g = p.X.T @ (p.b - p.X @ x)
+        nb = torch.tensor([float(torch.linalg.norm(p.b)) ** 2, float(torch.linalg.norm(p.X)) ** 2])
+        gt = g.cpu()
+        dist.all_reduce(gt)
+        dist.all_reduce(nb)
+        q.put((rank, "ok", float(torch.linalg.norm(gt)), nb.tolist(), rep, x[:8].cpu().numpy()))
+        ctx.close()
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc(), None, None, None, None))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("solver", ["cs"])
+def test_two_ranks_full_c5(solver):
+    """c5 at full size (1e6 x 1e4, 80 GB) split over two ranks of 500000 rows (40 GB each)
+    on the one GPU: the library's sharded sketch (global Philox index), the 1.6 GB sketch
+    allreduce, rank 0's SVD broadcast and the per-pass reductions.  Checks the pass count of
+    Alg. 3 at r = k, identical x on both ranks, and the normal equations
+    A^T (b - A x) = 0 to the iteration tolerance (Thm 4.5's bound, as tests/test_gpu_fullsize.py
+    checks for the one-rank solve)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()                 # earlier tests' cached blocks back to the device
+    free, total = torch.cuda.mem_get_info()
+    if free < 120e9:
+        pytest.skip("needs ~110 GB of device memory for two 40 GB shards and their workspaces")
+    import torch.multiprocessing as mp
+    from oracle import bounds
+    port = _free_port()
+    mpc = mp.get_context("spawn")
+    q = mpc.SimpleQueue()
+    procs = [mpc.Process(target=_worker_full, args=(r, 2, port, "c5", solver, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get() for _ in range(2)], key=lambda r: r[0])
+    for pr in procs:
+        pr.join(600)
+    for r in res:
+        assert r[1] == "ok", r[1]
+    s = 20000
+    sl, su = bounds.sigma_bounds(s, 10000, bounds.default_alpha(s))
+    for r in res:
+        assert r[4]["r"] == 10000 and r[4]["iters"] == bounds.cs_passes(sl, su, 1e-14) == 99
+    assert np.array_equal(res[0][5], res[1][5])               # x replicated bit for bit (same N on both)
+    gnorm, (b2, a2) = res[0][2], res[0][3]
+    assert gnorm <= 10 * 2e-14 * np.sqrt(a2) * np.sqrt(b2), (gnorm, a2, b2)
