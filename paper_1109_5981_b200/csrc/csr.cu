@@ -442,9 +442,19 @@ csr_sketch_slab_kernel(const int64_t* __restrict__ colptr, const int32_t* __rest
       for (int t = 0; t < CPW; ++t) {
         const int q1 = soff[t + 1];
         double a = acc[t];
+        int q = soff[t];
+        // two entries per trip (loads of both issued before the dependent FMAs; the
+        // accumulation order is unchanged)
 #pragma unroll 1
-        for (int q = soff[t]; q < q1; ++q) {
-          const double2 ev = ent[q];             // broadcast
+        for (; q + 1 < q1; q += 2) {
+          const double2 ev0 = ent[q], ev1 = ent[q + 1];   // broadcast
+          const double g0 = Gs[(int)__double_as_longlong(ev0.y) * IB + lane];
+          const double g1 = Gs[(int)__double_as_longlong(ev1.y) * IB + lane];
+          a = fma(g0, ev0.x, a);
+          a = fma(g1, ev1.x, a);
+        }
+        if (q < q1) {
+          const double2 ev = ent[q];
           a = fma(Gs[(int)__double_as_longlong(ev.y) * IB + lane], ev.x, a);
         }
         acc[t] = a;
