@@ -8,10 +8,12 @@ Recipe:
       b ~ N(0,1).                                          Stand-in for P:1079-1087.
   c3  dense 2000 x 2e5 (wide), A_ij ~ N(0,1) * 10^(-3 i / 1999) (row scales),
       b ~ N(0,1), lambda = 1e-3.                           Stand-in for P:1064-1077 + §5.
-  c4  CSR 2e6 x 2e4: per row 20 random columns among the first 19 950 (one
-      uniform draw in each of 20 equal strata, so distinct and sorted) plus the 50
-      dense columns 19 950..19 999; values N(0,1), dense-column values x 1e3,
+  c4  CSR 2e6 x 2e4: per row 20 distinct columns drawn uniformly without
+      replacement from the first 19 950 (C15: rejection of rows with a repeated
+      column, so every 20-subset is equally likely), sorted, plus the 50 dense
+      columns 19 950..19 999; values N(0,1), dense-column values x 1e3,
       b ~ N(0,1).                                          Stand-in for P:1115-1153.
+  t4  the same recipe with 21 random columns and no dense ones, as the CSR of A^T.
   c5  dense 1e6 x 1e4, A_ij ~ N(0,1) * 10^(-5 j / 9999) (column scales),
       b = A x0 + 1e-3 N(0,1).                              Stand-in for Table 3.
 Seeds: data seed = 1109 * 1000 + config number (C16); the sketch seed is 5981.
@@ -188,10 +190,6 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
         nd = min(cfg["dense_cols"], k - nr) if k > nr else 0   # columns of X (k = min(m, n))
         pool = k - nd
         nnz_row = nr + nd
-        # integer strata [floor(i pool / nr), floor((i+1) pool / nr)): one uniform draw in
-        # each, so the nr random columns of a row are distinct and sorted
-        edges = (torch.arange(nr + 1, device=device, dtype=torch.int64) * pool) // nr
-        lo_e, wid = edges[:-1], (edges[1:] - edges[:-1]).to(torch.float64)
         cols_d = torch.arange(pool, k, device=device, dtype=torch.int64)
         rows = hi - lo
         colind = torch.empty(rows, nnz_row, dtype=torch.int32, device=device)
@@ -200,9 +198,7 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
         for g in blocks:
             g0, g1 = g * BLOCK, min(L, (g + 1) * BLOCK)
             gen = _block_gen(seed, g, device)
-            u = torch.rand(g1 - g0, nr, generator=gen, **f64)
-            cr = lo_e + torch.minimum((u * wid).floor().to(torch.int64), (wid - 1).to(torch.int64))
-            # one draw per disjoint increasing stratum: distinct and sorted
+            cr = _distinct_sorted(gen, g1 - g0, nr, pool, f64)
             ci = torch.cat([cr, cols_d.expand(g1 - g0, nd)], dim=1).to(torch.int32)
             vv = torch.randn(g1 - g0, nnz_row, generator=gen, **f64)
             vv[:, nr:] *= cfg["dense_scale"]
@@ -218,6 +214,32 @@ def make_problem(name, device="cpu", m=None, n=None, seed=None, shard=None, keep
         return Problem(name, m, n, "csr", cfg["gamma"], cfg["lam"], b, rowptr=rowptr,
                        colind=colind.reshape(-1), val=val.reshape(-1), meta=meta)
     raise ValueError(f"unknown spectrum/kind for {name}")
+
+
+def _draw_sorted(gen, rows, nr, pool, f64):
+    u = torch.rand(rows, nr, generator=gen, **f64)
+    c = torch.minimum((u * pool).floor().to(torch.int64), torch.tensor(pool - 1, device=u.device))
+    return c.sort(dim=1).values
+
+
+def _distinct_sorted(gen, rows, nr, pool, f64):
+    """nr distinct columns per row, uniform over the nr-subsets of range(pool), sorted
+    (C15): nr uniform draws per row, and any row with a repeat is drawn again whole
+    (rejection keeps the subset distribution uniform)."""
+    if nr > pool:
+        raise ValueError(f"{nr} distinct columns out of {pool}")
+    if 4 * nr > pool:         # dense rows: the first nr of a random permutation instead
+        keys = torch.rand(rows, pool, generator=gen, **f64)
+        return keys.argsort(dim=1)[:, :nr].sort(dim=1).values
+    c = _draw_sorted(gen, rows, nr, pool, f64)
+    if nr < 2:
+        return c
+    bad = (c[:, 1:] == c[:, :-1]).any(dim=1).nonzero().squeeze(1)
+    while bad.numel():
+        d = _draw_sorted(gen, bad.numel(), nr, pool, f64)
+        c[bad] = d
+        bad = bad[(d[:, 1:] == d[:, :-1]).any(dim=1)]
+    return c
 
 
 def small(name, device="cpu"):
