@@ -86,7 +86,16 @@ enum {
    * A (the same pointers and values), its shard, gamma and seed are unchanged;
    * pointer / shard / gamma / seed / workspace mismatches return LSRN_EINVAL.
    * lambda may change: only the Tikhonov block depends on it. */
-  LSRN_REUSE_SKETCH = 4
+  LSRN_REUSE_SKETCH = 4,
+  /* precision = 1 (SURVEY §8(b) lsrn_opts.precision; reading C18(ii)):
+   * the iteration products A (N v) and N^T (A^T u) carry N v and A^T u as
+   * double-double pairs and accumulate every dot product and column sum with
+   * error-free transformations (TwoProd / TwoSum), removing the ~kappa(A) u
+   * cancellation floor of plain fp64 products; the Krylov recurrences stay
+   * fp64.  Dense A and nranks == 1 only (else LSRN_EUNSUPPORTED), like the
+   * oracle's long-double product mode.  Slower than the fp64 passes (two
+   * launches per pass, Y read twice, ~10x the arithmetic). */
+  LSRN_COMPENSATED = 8
 };
 
 typedef struct lsrn_ctx lsrn_ctx;
@@ -114,7 +123,8 @@ typedef struct {
   int32_t mode;          /* LSQR: LSRN_MODE_PREDICTABLE (Thm 4.5 count at alpha = 0, §8(c) C5)
                             or LSRN_MODE_ADAPTIVE (Paige-Saunders tests, capped) */
   int32_t max_iter;      /* adaptive cap; 0 = 2 x the Thm 4.5 count */
-  int32_t flags;         /* LSRN_HOST_IO, LSRN_SKETCH_ONLY (workspace query), LSRN_REUSE_SKETCH */
+  int32_t flags;         /* LSRN_HOST_IO, LSRN_SKETCH_ONLY (workspace query), LSRN_REUSE_SKETCH,
+                            LSRN_COMPENSATED */
   int32_t pad_;
 } lsrn_opts;
 

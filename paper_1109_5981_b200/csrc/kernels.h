@@ -118,6 +118,40 @@ struct ColReduceArgs {
 int colreduce_blocks(int64_t C);
 cudaError_t launch_colreduce(const ColReduceArgs& a, cudaStream_t st);
 
+// ---- compensated row pass (compensated.cu; precision = 1, C18(ii))
+struct ExtRowPassArgs {
+  const double* Y;
+  int64_t ld, R, C;
+  double sx;
+  double* z;
+  const double* t_hi;
+  const double* t_lo;
+  const double* coef;
+  double* acc;
+  const int* done;
+  double* part_s;        // [nblocks][C]
+  double* part_c;        // [nblocks][C]
+  double* npart;         // [nblocks]
+};
+struct ExtColReduceArgs {
+  const double* part_s;
+  const double* part_c;
+  const double* npart;
+  int nparts;
+  int64_t C;
+  double* zI;            // nullable
+  const double* t_hi;
+  const double* t_lo;
+  const double* coef;
+  double sI;
+  double* out_hi;        // C + 1 (out_hi[C] = ||z||^2)
+  double* out_lo;        // C + 1
+  const int* done;
+};
+int ext_rowpass_blocks(int64_t R, int nsm);
+cudaError_t launch_ext_rowpass(const ExtRowPassArgs& a, int nblocks, cudaStream_t st);
+cudaError_t launch_ext_colreduce(const ExtColReduceArgs& a, cudaStream_t st);
+
 // ---- Krylov scalar / vector steps (krylov.cu)
 struct LsqrState {
   double alpha, beta, su, sv, rhobar, phibar, anorm2, bnorm;

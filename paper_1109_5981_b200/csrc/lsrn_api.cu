@@ -945,11 +945,16 @@ struct IterWs {
   unsigned* counters;
   LsqrState* state;
   int ncoef;
+  // LSRN_COMPENSATED: low parts of the vectors that cross between the passes, a
+  // zero vector (the low part of b), and the compensated passes' block partials
+  double *comm_lo = nullptr, *tbuf_lo = nullptr, *xbuf_lo = nullptr, *zero_lo = nullptr;
+  double *epart_s = nullptr, *epart_c = nullptr, *enpart = nullptr;
+  int enb = 0;
 };
 
 enum Solver { SOLVER_LSQR = 0, SOLVER_CS = 1 };
 
-IterWs plan_iter(lsrn_ctx* c, const Dims& d, Arena& ar, int max_passes) {
+IterWs plan_iter(lsrn_ctx* c, const Dims& d, Arena& ar, int max_passes, bool compensated) {
   IterWs w{};
   const int64_t k = d.k;
   const int64_t Lz = d.Lz > 0 ? d.Lz : 1;
@@ -972,6 +977,16 @@ IterWs plan_iter(lsrn_ctx* c, const Dims& d, Arena& ar, int max_passes) {
   w.consts = ar.take<double>(16);
   w.counters = ar.take<unsigned>(4);
   w.state = ar.take<LsqrState>(1);
+  if (compensated) {
+    w.comm_lo = ar.take<double>((size_t)k + 1);
+    w.tbuf_lo = ar.take<double>((size_t)k + 1);
+    w.xbuf_lo = ar.take<double>((size_t)k + 1);
+    w.zero_lo = ar.take<double>((size_t)k + 1);
+    w.enb = 2 * (c->nsm > 0 ? c->nsm : 148);        // >= ext_rowpass_blocks of either pass
+    w.epart_s = ar.take<double>((size_t)w.enb * k);
+    w.epart_c = ar.take<double>((size_t)w.enb * k);
+    w.enpart = ar.take<double>((size_t)w.enb);
+  }
   return w;
 }
 
@@ -985,6 +1000,57 @@ struct Pass {
   RowPassPlan plong, pshort;
   const CsrWs* cw = nullptr;   // CSR A: rowdot + colgather instead of the dense row pass
   bool two_sync = false;       // LSRN_OPT_LSQR_SYNC = 1: reduce ||z||^2, then the vector (two collectives)
+  bool ext = false;            // LSRN_COMPENSATED: double-double vectors between the passes
+
+  // low part of a pass input / output (ext mode): the buffers that cross between passes
+  double* lo_of(const double* p) const {
+    if (p == w.comm) return w.comm_lo;
+    if (p == w.tbuf) return w.tbuf_lo;
+    if (p == w.xbuf) return w.xbuf_lo;
+    return w.zero_lo;                      // b (fp64 input)
+  }
+
+  // compensated row pass over Y (R x C): z <- c1 z + c2 sY Y t ; out = sY Y^T z (+ I block) ; ||z||^2
+  void pass_ext(const double* Y, int64_t ld, int64_t R, double sY, double* z, const double* t, const double* coef,
+                double* acc, const int* done, double* out, double* zI, double sI) {
+    cudaStream_t st = c->stream;
+    const int nb = R > 0 ? std::min(ext_rowpass_blocks(R, c->nsm), w.enb) : 0;
+    ExtRowPassArgs a{};
+    a.Y = Y;
+    a.ld = ld;
+    a.R = R;
+    a.C = d.k;
+    a.sx = sY;
+    a.z = z;
+    a.t_hi = t;
+    a.t_lo = lo_of(t);
+    a.coef = coef;
+    a.acc = acc;
+    a.done = done;
+    a.part_s = w.epart_s;
+    a.part_c = w.epart_c;
+    a.npart = w.enpart;
+    if (nb > 0) {
+      LSRN_CUDA(launch_ext_rowpass(a, nb, st));
+      c->launches++;
+    }
+    ExtColReduceArgs r{};
+    r.part_s = w.epart_s;
+    r.part_c = w.epart_c;
+    r.npart = w.enpart;
+    r.nparts = nb;
+    r.C = d.k;
+    r.zI = zI;
+    r.t_hi = t;
+    r.t_lo = lo_of(t);
+    r.coef = coef;
+    r.sI = sI;
+    r.out_hi = out;
+    r.out_lo = lo_of(out);
+    r.done = done;
+    LSRN_CUDA(launch_ext_colreduce(r, st));
+    c->launches++;
+  }
 
   void reduce_out(double* out) {
     if (two_sync) {
@@ -1086,6 +1152,10 @@ struct Pass {
 
   // long pass over X: z <- c1 z + c2 sX X t (+ I block), out = [P^T z ; ||z||^2]
   void long_pass(double* z, const double* t, const double* coef, double* acc, const int* done, double* out) {
+    if (ext) {
+      pass_ext(A->val, A->ld, d.cnt, d.sx, z, t, coef, acc, done, out, d.has_I ? z + d.cnt : nullptr, d.si);
+      return;
+    }
     if (cw != nullptr) {
       long_pass_csr(z, t, coef, acc, done, out);
       return;
@@ -1135,6 +1205,10 @@ struct Pass {
 
   // short pass over N^T: v <- c1 v + c2 N^T wv, out = [N v ; ||v||^2]
   void short_pass(double* v, const double* wv, const double* coef, double* acc, const int* done, double* out) {
+    if (ext) {
+      pass_ext(Nt, d.k, r, 1.0, v, wv, coef, acc, done, out, nullptr, 0.0);
+      return;
+    }
     cudaStream_t st = c->stream;
     RowPassArgs a{};
     a.Y = Nt;
@@ -1446,7 +1520,7 @@ size_t plan_all(lsrn_ctx* c, const lsrn_matrix* A, const lsrn_opts* o, Arena& ar
     P.vw = plan_svd(c, d, ar);
     // max passes: LSQR cap (2x the count for r = k) or CS passes with r = k; bounded by a generous margin
     const int max_passes = 4096;
-    P.iw = plan_iter(c, d, ar, max_passes);
+    P.iw = plan_iter(c, d, ar, max_passes, (o->flags & LSRN_COMPENSATED) != 0);
   }
   return ar.off;
 }
@@ -1562,6 +1636,9 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
                  "workspace too small: need " + std::to_string(need) + " bytes");
     LSRN_REQUIRE(!(o->mode == LSRN_MODE_ADAPTIVE && !d.tall && c->nranks > 1), LSRN_EUNSUPPORTED,
                  "adaptive LSQR on a sharded wide problem is not supported (use predictable mode)");
+    const bool ext = (o->flags & LSRN_COMPENSATED) != 0;
+    LSRN_REQUIRE(!ext || (A_in->kind == LSRN_DENSE && c->nranks == 1), LSRN_EUNSUPPORTED,
+                 "LSRN_COMPENSATED supports dense A on one rank");
     cudaStream_t st = c->stream;
     c->launches = 0;
     c->collectives = 0;
@@ -1620,6 +1697,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     // ---- iteration plans
     Pass P{c, d, &A, vw.Nt, r, iw, {}, {}};
     P.two_sync = solver == SOLVER_LSQR && c->lsqr_sync == 1;
+    P.ext = ext;
     const bool eager = host_collectives(c);   // host round trips cannot live in a graph
     if (PL.csr)
       P.cw = &PL.cw;
@@ -1675,6 +1753,10 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     LSRN_CUDA(launch_fill(iw.tbuf, 0.0, d.k + 1, st));
     LSRN_CUDA(launch_fill(iw.xbuf, 0.0, d.k + 1, st));
     c->launches += 9;
+    if (ext) {
+      for (double* q : {iw.comm_lo, iw.tbuf_lo, iw.xbuf_lo, iw.zero_lo}) LSRN_CUDA(launch_fill(q, 0.0, d.k + 1, st));
+      c->launches += 4;
+    }
     if (solver == SOLVER_LSQR) {
       LSRN_CUDA(launch_lsqr_init_state(iw.state, o->tol, o->mode == LSRN_MODE_ADAPTIVE ? 1 : 0, st));
       c->launches++;
@@ -1732,7 +1814,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
     ki((int64_t)c->pass_ev.size()), ki(PL.csr ? 1 : 0), ki(ovr().csr_rowdot), ki(P.two_sync ? 1 : 0);
     if (PL.csr) ki(PL.cw.nd), ki(PL.cw.ND), ki(PL.cw.ldd), ki(PL.cw.nnz_light);
     ki(d.tall ? 1 : 0), ki(d.m), ki(d.n), ki(d.L), ki(d.k), ki(d.s), ki(d.cnt), ki(d.lo), kd(d.sx), kd(d.si);
-    ki(d.has_I ? 1 : 0), ki(d.Lz);
+    ki(d.has_I ? 1 : 0), ki(d.Lz), ki(ext ? 1 : 0);
     kplan(P.plong), kplan(P.pshort);
     const bool graph_hit = !eager && c->gexec && c->graph_key == gk && c->graph_reuse;
     cudaGraph_t graph = nullptr;

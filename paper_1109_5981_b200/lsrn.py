@@ -20,6 +20,7 @@ MODE_PREDICTABLE, MODE_ADAPTIVE = 0, 1
 HOST_IO = 1
 SKETCH_ONLY = 2
 REUSE_SKETCH = 4
+COMPENSATED = 8            # precision = 1 (lsrn.h LSRN_COMPENSATED, C18(ii))
 STATUS = {0: "LSRN_OK", -1: "LSRN_EINVAL", -2: "LSRN_EDIM", -3: "LSRN_ENONFINITE", -4: "LSRN_ERANK0",
           -5: "LSRN_ESVD", -6: "LSRN_ENOMEM", -7: "LSRN_ECUDA", -8: "LSRN_ENCCL", -9: "LSRN_EUNSUPPORTED"}
 
@@ -336,10 +337,14 @@ class Context:
         return At
 
     def solve(self, X, b, m, n, solver="lsqr", gamma=2.0, lam=0.0, tol=1e-14, seed=5981, alpha=-1.0,
-              mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False, reuse_sketch=False):
-        """LSRN solve; X a long-index-major dense shard or a Csr row shard (device, or pinned host with host_io)."""
+              mode="predictable", max_iter=0, lo=0, cnt=None, x_out=None, host_io=False, reuse_sketch=False,
+              precision=0):
+        """LSRN solve; X a long-index-major dense shard or a Csr row shard (device, or pinned host with host_io).
+        precision: 0 fp64 products, 1 compensated products (LSRN_COMPENSATED; dense, one rank)."""
         if solver not in ("lsqr", "cs"):
             raise ValueError("solver must be 'lsqr' or 'cs'")
+        if precision not in (0, 1):
+            raise ValueError("precision must be 0 (fp64) or 1 (compensated)")
         _check_matrix_device(X, self.device, host_io)
         if host_io and not isinstance(X, Csr):
             if X.dtype != torch.float64:
@@ -361,7 +366,8 @@ class Context:
             _check_vec("x_out", x_out, xlen, self.device, host_io)
         opts = Opts(gamma=gamma, lambda_=lam, tol=tol, alpha=alpha, seed=seed,
                     mode=MODE_ADAPTIVE if mode == "adaptive" else MODE_PREDICTABLE, max_iter=max_iter,
-                    flags=(HOST_IO if host_io else 0) | (REUSE_SKETCH if reuse_sketch else 0))
+                    flags=(HOST_IO if host_io else 0) | (REUSE_SKETCH if reuse_sketch else 0)
+                    | (COMPENSATED if precision == 1 else 0))
         ws = self.workspace(self.workspace_size(mat, opts))
         rep = Report()
         fn = lib().lsrn_solve_lsqr if solver == "lsqr" else lib().lsrn_solve_cs
@@ -380,7 +386,8 @@ class Context:
         need = 0
         for lam in lambdas:
             o = Opts(gamma=kw.get("gamma", 2.0), lambda_=lam, tol=kw.get("tol", 1e-14), alpha=kw.get("alpha", -1.0),
-                     seed=kw.get("seed", 5981), mode=MODE_PREDICTABLE, max_iter=0, flags=0)
+                     seed=kw.get("seed", 5981), mode=MODE_PREDICTABLE, max_iter=0,
+                     flags=COMPENSATED if kw.get("precision", 0) == 1 else 0)
             need = max(need, self.workspace_size(mat, o))
         self.workspace(need)
         out = []

@@ -99,3 +99,14 @@ def test_options_table_matches_header():
     src = open(HEADER).read()
     hdr = {k.lower(): int(v) for k, v in re.findall(r"LSRN_OPT_([A-Z0-9_]+)\s*=\s*(\d+)", src)}
     assert hdr == lsrn.OPTIONS
+
+
+def test_flag_constants_match_header():
+    """The binding's lsrn_opts.flags bits and status codes equal include/lsrn.h's."""
+    from paper_1109_5981_b200 import lsrn
+    src = open(HEADER).read()
+    for name in ("HOST_IO", "SKETCH_ONLY", "REUSE_SKETCH", "COMPENSATED"):
+        v = re.search(rf"LSRN_{name}\s*=\s*(\d+)", src)
+        assert v is not None and int(v.group(1)) == getattr(lsrn, name), name
+    codes = {int(v): f"LSRN_{k}" for k, v in re.findall(r"LSRN_(E[A-Z0-9]+|OK)\s*=\s*(-?\d+)", src)}
+    assert codes == lsrn.STATUS
