@@ -854,7 +854,11 @@ csr_rowdot_all_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restr
   // updates (t4: 1.0 -> 0.70 ms per pass; the first version waited on rowptr ->
   // colind -> t per pair; four rows per step with the same pipelining: 1.37 ms; an
   // L2 prefetch of the next chunk's entries: 1.01 ms).  Rows of <= 32 entries keep (c, a) in registers for the w update;
-  // longer rows loop.
+  // longer rows loop.  Also rejected (round 2, t4): staging each warp's next 32-row chunk in
+  // shared memory with cp.async (8 KB in flight per warp, but 8 warps per SM: 0.84-1.30 ms)
+  // and lane-per-row dots without the shuffle tree (half the instructions, 0.88 ms): both
+  // leave the per-row w scatter (shared-memory read-modify-write chain, one row at a time)
+  // as the critical path, which the two-row pipelining here overlaps with the next loads.
   for (int64_t rc = r0; rc < r1; rc += 32) {
     const int nr = (int)min((int64_t)32, r1 - rc);
     const int64_t rp = lane < nr ? rowptr[rc + lane] - base : 0;

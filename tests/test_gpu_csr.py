@@ -230,3 +230,40 @@ def test_csr_solve_wide_k_uses_csc_gather(ctx, solver, m, nnz_row, dense, empty,
     assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
     rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
     assert rel <= 1e-9, rel
+
+
+def _ragged_csr(m, n, seed):
+    """Row lengths mixed: empty rows, rows of 3..45 entries, a 32-row chunk of 40-entry
+    rows and one 120-entry row (longer than a warp)."""
+    rng = np.random.default_rng(seed)
+    lens = rng.choice([0, 3, 7, 21, 45], size=m, p=[0.05, 0.4, 0.3, 0.2, 0.05])
+    lens[200:232] = 40
+    lens[300] = 120
+    rows, cols, vals = [], [], []
+    for i, L in enumerate(lens):
+        cs = rng.choice(n, size=min(int(L), n), replace=False)
+        rows += [i] * cs.size
+        cols += list(cs)
+        vals += list(rng.standard_normal(cs.size))
+    return sp.csr_matrix((vals, (rows, cols)), shape=(m, n))
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "cs"])
+@pytest.mark.parametrize("rowdot", [-1, 3])
+def test_csr_single_pass_staged_and_direct_chunks(ctx, solver, rowdot):
+    """k <= 2048 long pass on ragged rows (empty rows, rows longer than a warp, a chunk of
+    long rows): the single-pass kernel (default) and the two-kernel CSC-gather form
+    (LSRN_OPT_CSR_ROWDOT = 3) against the oracle."""
+    A = _ragged_csr(5000, 300, seed=8)
+    b = np.random.default_rng(9).standard_normal(A.shape[0])
+    with ctx.options(csr_rowdot=rowdot):
+        x, rep = ctx.solve(_gpu_csr(A), torch.from_numpy(b).cuda(), A.shape[0], A.shape[1], solver=solver)
+    orc = orc_solve(A, b, solver=solver)
+    assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
+    xg = x.cpu().numpy()
+    sv = np.linalg.svd(A.toarray(), compute_uv=False)
+    kappa = sv[0] / sv[sv > sv[0] * 1e-12][-1]
+    rel = np.linalg.norm(xg - orc["x"]) / np.linalg.norm(orc["x"])
+    assert rel <= max(1e-9, 20 * kappa * U), rel
+    an = np.linalg.norm(A @ (xg - orc["x"])) / np.linalg.norm(A @ orc["x"])
+    assert an <= 1e-11, an
