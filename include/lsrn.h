@@ -212,6 +212,10 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *   LSRN_OPT_SKETCH_X_L2    1: X tiles of the dense sketch loaded with an L2 evict_last policy
  *   LSRN_OPT_SKETCH_CHUNKS  dense sketch of a device-resident A: number of row chunks
  *                           launched in stream order (default: one per 4 GB of A, <= 16)
+ *   LSRN_OPT_SKETCH_G       dense sketch: -1 (default) each launch first writes its G tiles
+ *                           once into a workspace buffer of <= 8 GB and the DMMA kernel streams
+ *                           them; 0 G generated in registers by every CTA that needs it, never
+ *                           stored; N > 0 stored with an N-MB budget (same G values either way)
  *   LSRN_OPT_ROWPASS_*      row-pass plan fields; _PF: L2 prefetch distance
  *   LSRN_OPT_CSR_ROWDOT     CSR long pass: 0 heavy-dense + light-CSR, 8 rows per step;
  *                           1 warp per row over the full CSR; 2 as 0 with 2 rows per step;
@@ -232,6 +236,7 @@ enum {
   LSRN_OPT_SKETCH_NSPLIT = 103,
   LSRN_OPT_SKETCH_X_L2 = 104,
   LSRN_OPT_SKETCH_CHUNKS = 105,
+  LSRN_OPT_SKETCH_G = 106,
   LSRN_OPT_ROWPASS_KEEP = 110,
   LSRN_OPT_ROWPASS_OCC = 111,
   LSRN_OPT_ROWPASS_WIDE1 = 112,

@@ -19,6 +19,8 @@ struct Overrides {
   int sketch_nsplit = -1;     // split-K factor (>= 1)
   int sketch_x_l2 = -1;       // 1: X tiles loaded with an L2 evict_last policy
   int sketch_chunks = -1;     // device-resident A: row chunks launched one after the other (0/1 = one launch)
+  int sketch_g = -1;          // dense sketch G: -1 stored per launch (8 GB budget), 0 in-register (never
+                              // stored), N > 0 stored with an N-MB budget
   int rowpass_keep = -1;      // 0/1: re-read / register-kept row tile
   int rowpass_occ = -1;       // 1/2 CTAs per SM
   int rowpass_wide1 = -1;     // 0 disables the single 512-thread CTA plan for 8192 < k <= 10240
@@ -50,7 +52,12 @@ struct SketchDenseArgs {
   double* out;       // [nsplit][s][k]
   int64_t out_split_stride;
   int accumulate = 0;   // 1: out += partial (stream-ordered chunks of A, host-IO streaming)
+  double* G = nullptr;  // stored-G mode: buffer of sketch_g_bytes(s, rows) the launch fills with
+                        // this launch's G tiles first (rows_per_split a multiple of sketch_g_block_rows())
 };
+size_t sketch_g_bytes(int64_t s, int64_t rows);
+int64_t sketch_g_row_bytes(int64_t s);
+int64_t sketch_g_block_rows();
 size_t sketch_dense_smem();
 void sketch_tile_counts(int64_t s, int64_t k, int64_t* mtiles, int64_t* ntiles, int64_t* bk);
 cudaError_t launch_sketch_dense(const SketchDenseArgs& a, cudaStream_t st);   // picks v2 when supported

@@ -268,7 +268,31 @@ struct SketchWs {
   int nchunk = 0;
   int64_t chunk_r0[kMaxChunks + 1] = {};   // chunk i = rows [chunk_r0[i], chunk_r0[i+1])
   bool host_stream = false;                 // chunks wait on their H2D copy events
+  // stored G (ovr().sketch_g != 0): each launch covers <= g_rows rows (a multiple of 16)
+  // and first writes its G tiles into G (sketch_gen_g_kernel)
+  double* G = nullptr;
+  int64_t g_rows = 0;
 };
+
+// Stored-G plan: rows per sketch launch so that its G tiles fit the budget (0: the
+// in-register path).  Needs the 32 x 512 warp-specialized kernel's layout (even ld
+// and k; the kernel / tile overrides select the other kernels).
+int64_t stored_g_rows(const Dims& d, int64_t ld) {
+  if (ovr().sketch_g == 0 || d.cnt <= 0 || ld % 2 != 0 || d.k % 2 != 0) return 0;
+  if (ovr().sketch_kernel == 1 || ovr().sketch_kernel == 2 || ovr().sketch_tile == 0) return 0;
+  const double budget = ovr().sketch_g > 0 ? (double)ovr().sketch_g * 1048576.0 : 8.0e9;
+  const int64_t bk = sketch_g_block_rows();
+  const int64_t rows = (int64_t)(budget / (double)sketch_g_row_bytes(d.s)) / bk * bk;
+  return std::max(bk, rows);
+}
+
+// split-K of one sketch launch of `rows` rows (stored G: split boundaries on k-blocks)
+void launch_split(const lsrn_ctx* c, const Dims& d, int64_t rows, bool g, int* nsplit, int64_t* rps) {
+  *nsplit = choose_nsplit(d.s, d.k, rows, c->nsm);
+  int64_t r = (rows + *nsplit - 1) / *nsplit;
+  if (g) r = (r + 15) / 16 * 16;
+  *rps = r > 0 ? r : 16;
+}
 
 // Host-IO streaming: A is copied in chunks of >= 128 MB on a second stream and
 // each chunk is sketched as soon as it has landed, so the H2D copy of A
@@ -294,17 +318,31 @@ int stream_chunks(const Dims& d, int64_t ld, double first_mb, int64_t* r0) {
   return n;
 }
 
+// the largest split-K over the launches of chunks [chunk_r0] (stored G: sub-launches of <= g_rows)
+int max_nsplit(const lsrn_ctx* c, const Dims& d, const SketchWs& w) {
+  int ns = 1;
+  for (int i = 0; i < w.nchunk; ++i) {
+    const int64_t nr = w.chunk_r0[i + 1] - w.chunk_r0[i];
+    const int64_t step = w.g_rows > 0 ? w.g_rows : nr;
+    for (int64_t sub = 0; sub < nr; sub += step) ns = std::max(ns, choose_nsplit(d.s, d.k, std::min(step, nr - sub), c->nsm));
+  }
+  return ns;
+}
+
 SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_flag, bool host_stream = false,
                      int64_t ld = 0) {
   SketchWs w{};
+  w.g_rows = stored_g_rows(d, ld);
+  auto take_g = [&]() {
+    if (w.g_rows > 0) w.G = ar.take<double>(sketch_g_bytes(d.s, std::min(w.g_rows, d.cnt)) / sizeof(double));
+  };
   if (host_stream && d.cnt > 0) {
     w.nchunk = stream_chunks(d, ld, c->hostio_chunk_mb, w.chunk_r0);
     if (w.nchunk > 1) {
       w.host_stream = true;
-      w.nsplit = 1;
-      for (int i = 0; i < w.nchunk; ++i)
-        w.nsplit = std::max(w.nsplit, choose_nsplit(d.s, d.k, w.chunk_r0[i + 1] - w.chunk_r0[i], c->nsm));
+      w.nsplit = max_nsplit(c, d, w);
       w.part = ar.take<double>((size_t)w.nsplit * d.s * d.k);
+      take_g();
       return w;
     }
     w.nchunk = 0;
@@ -317,6 +355,8 @@ SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_fla
   const double a_bytes = 8.0 * (double)d.cnt * (double)ld;
   int nch = (int)std::ceil(a_bytes / 4.0e9);
   if (ovr().sketch_chunks >= 0) nch = ovr().sketch_chunks;
+  if (w.g_rows > 0 && w.g_rows < d.cnt)       // stored G: at least one launch per budget of G tiles
+    nch = std::max(nch, (int)((d.cnt + w.g_rows - 1) / w.g_rows));
   nch = std::min(nch, kMaxChunks);
   if (d.cnt > 0 && nch > 1 && d.cnt >= 16 * (int64_t)nch) {
     int64_t per = (d.cnt + nch - 1) / nch;
@@ -325,18 +365,19 @@ SketchWs plan_sketch(lsrn_ctx* c, const Dims& d, Arena& ar, bool need_finish_fla
     for (int64_t row = 0; row < d.cnt && w.nchunk < kMaxChunks; row += per) w.chunk_r0[w.nchunk++] = row;
     w.chunk_r0[w.nchunk] = d.cnt;
     if (w.nchunk > 1) {
-      w.nsplit = 1;
-      for (int i = 0; i < w.nchunk; ++i)
-        w.nsplit = std::max(w.nsplit, choose_nsplit(d.s, d.k, w.chunk_r0[i + 1] - w.chunk_r0[i], c->nsm));
+      w.nsplit = max_nsplit(c, d, w);
       w.part = ar.take<double>((size_t)w.nsplit * d.s * d.k);
+      take_g();
       return w;
     }
     w.nchunk = 0;
   }
+  w.g_rows = (w.g_rows > 0 && w.g_rows >= d.cnt) ? w.g_rows : 0;   // one launch (or none: cnt < 16 chunks)
   w.nsplit = choose_nsplit(d.s, d.k, d.cnt, c->nsm);
   int64_t rps = (d.cnt + w.nsplit - 1) / w.nsplit;
   rps = (rps + 15) / 16 * 16;
   w.rows_per_split = rps > 0 ? rps : 16;
+  take_g();
   const bool direct = (w.nsplit == 1);
   (void)need_finish_flag;
   w.part = direct ? nullptr : ar.take<double>((size_t)w.nsplit * d.s * d.k);
@@ -546,24 +587,28 @@ void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed,
     LSRN_CUDA(launch_fill(w.part, 0.0, (int64_t)w.nsplit * d.s * d.k, st));
     c->launches++;
     for (int i = 0; i < w.nchunk; ++i) {
-      const int64_t r0 = w.chunk_r0[i];
-      const int64_t nr = w.chunk_r0[i + 1] - r0;
+      const int64_t c0 = w.chunk_r0[i];
+      const int64_t cn = w.chunk_r0[i + 1] - c0;
       if (w.host_stream) LSRN_CUDA(cudaStreamWaitEvent(st, c->chunk_ev[i], 0));
-      SketchDenseArgs a{};
-      a.X = A->val + r0 * A->ld;
-      a.ld = A->ld;
-      a.rows = nr;
-      a.k = d.k;
-      a.lo = d.lo + r0;
-      a.s = d.s;
-      a.seed = seed;
-      a.nsplit = choose_nsplit(d.s, d.k, nr, c->nsm);      // <= w.nsplit
-      a.rows_per_split = (nr + a.nsplit - 1) / a.nsplit;
-      a.out = w.part;
-      a.out_split_stride = d.s * d.k;
-      a.accumulate = 1;       // chunks are stream-ordered: fixed summation order
-      LSRN_CUDA(launch_sketch_dense(a, st));
-      c->launches++;
+      const int64_t step = w.G ? w.g_rows : cn;            // stored G: <= g_rows rows per launch
+      for (int64_t sub = 0; sub < cn; sub += step) {
+        const int64_t r0 = c0 + sub, nr = std::min(step, cn - sub);
+        SketchDenseArgs a{};
+        a.X = A->val + r0 * A->ld;
+        a.ld = A->ld;
+        a.rows = nr;
+        a.k = d.k;
+        a.lo = d.lo + r0;
+        a.s = d.s;
+        a.seed = seed;
+        launch_split(c, d, nr, w.G != nullptr, &a.nsplit, &a.rows_per_split);   // nsplit <= w.nsplit
+        a.out = w.part;
+        a.out_split_stride = d.s * d.k;
+        a.accumulate = 1;     // launches are stream-ordered: fixed summation order
+        a.G = w.G;
+        LSRN_CUDA(launch_sketch_dense(a, st));
+        c->launches += w.G ? 2 : 1;
+      }
     }
     LSRN_CUDA(launch_sketch_finish(w.part, w.nsplit, d.s * d.k, d.s, d.k, 1.0, 0.0, d.L, seed, At, st, c->nsm));
     c->launches++;
@@ -582,8 +627,9 @@ void run_sketch(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, uint64_t seed,
     a.nsplit = w.nsplit;
     a.out = w.part ? w.part : At;
     a.out_split_stride = d.s * d.k;
+    a.G = w.G;
     LSRN_CUDA(launch_sketch_dense(a, st));
-    c->launches++;
+    c->launches += w.G ? 2 : 1;
   } else if (!w.part) {
     LSRN_CUDA(launch_fill(At, 0.0, d.s * d.k, st));
     c->launches++;
@@ -1368,6 +1414,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_SKETCH_MAXCL: if (!in(-1, 4)) return bad(); o.sketch_maxcl = (int)value; break;
     case LSRN_OPT_SKETCH_X_L2: if (!in(-1, 1)) return bad(); o.sketch_x_l2 = (int)value; break;
     case LSRN_OPT_SKETCH_CHUNKS: if (!in(-1, 16)) return bad(); o.sketch_chunks = (int)value; break;
+    case LSRN_OPT_SKETCH_G: if (!in(-1, 1 << 20)) return bad(); o.sketch_g = (int)value; break;
     case LSRN_OPT_SKETCH_NSPLIT: if (!in(-1, 64) || value == 0) return bad(); o.sketch_nsplit = (int)value; break;
     case LSRN_OPT_ROWPASS_KEEP: if (!in(-1, 1)) return bad(); o.rowpass_keep = (int)value; break;
     case LSRN_OPT_ROWPASS_OCC: if (!in(-1, 2) || value == 0) return bad(); o.rowpass_occ = (int)value; break;

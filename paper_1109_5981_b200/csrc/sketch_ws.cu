@@ -112,7 +112,7 @@ template <class C, int CL>
 __global__ void __launch_bounds__(ws::THREADS, 1)
 sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t k, int64_t lo, int64_t s,
                  uint64_t seed, int64_t rows_per_split, double* __restrict__ out, int64_t out_split_stride,
-                 int accumulate, int x_evict_last) {
+                 int accumulate, int x_evict_last, const double* __restrict__ Gmem, int64_t g_nkb) {
   using namespace ws;
   constexpr int BM = C::BM, BN = C::BN, BK = C::BK, NSX = C::NSX, NSG = C::NSG;
   constexpr int A_LD = C::A_LD, G_LD = C::G_LD, X_STAGE = C::X_STAGE, G_STAGE = C::G_STAGE;
@@ -141,7 +141,8 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
       mbar_init(&xempty[i], NCONS_WARPS);
     }
     for (int i = 0; i < NSG; ++i) {
-      mbar_init(&gfull[i], NPW);                        // one per local producer warp (+ tx of remote rows)
+      // one per local producer warp (+ tx of remote rows); stored G: the one bulk copy
+      mbar_init(&gfull[i], Gmem != nullptr ? 1 : NPW);
       mbar_init(&gempty[i], NCONS_WARPS * CL);          // one per consumer warp of each CTA of the cluster
     }
     mbar_fence_init();
@@ -159,6 +160,38 @@ sketch_ws_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t
     // free, generate its PPT pairs per lane (independent chains, interleaved),
     // store, push its rows to the other CTAs of the cluster, arrive on gfull.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    if (Gmem != nullptr) {
+      // stored G (sketch_gen_g_kernel wrote this chunk's tiles, padded like the G
+      // stage): lane 0 of warp 0 streams the X rows and the G tile of every k-block;
+      // the other producer warps have nothing to do
+      if (CL == 1 && warp == 0 && lane == 0) {
+        const int64_t ncols = min((int64_t)BN, k - n0);
+        const unsigned seg_bytes = (unsigned)(ncols * 8);
+        const uint64_t xpol = x_evict_last ? l2_policy_evict_last() : 0ull;
+        const double* gsrc = Gmem + ((m0 / BM) * g_nkb + r_begin / BK) * (int64_t)G_STAGE;
+        for (int kb = 0; kb < nk; ++kb) {
+          const int sx = kb % NSX, sg = kb % NSG;
+          const unsigned px = (unsigned)(((kb / NSX) & 1) ^ 1), pg = (unsigned)(((kb / NSG) & 1) ^ 1);
+          const int64_t rbase = r_begin + (int64_t)kb * BK;
+          const int nrow = (int)min((int64_t)BK, r_end - rbase);
+          if (kb >= NSX) mbar_wait(&xempty[sx], px);
+          double* dst = Xs + sx * X_STAGE;
+          if (nrow < BK)          // ragged K tail: zero the missing rows (the G tile is zero there too)
+            for (int e = 0; e < (BK - nrow) * A_LD; ++e) dst[nrow * A_LD + e] = 0.0;
+          mbar_arrive_expect_tx(&xfull[sx], seg_bytes * (unsigned)nrow);
+          for (int rr = 0; rr < nrow; ++rr) {
+            if (x_evict_last)
+              bulk_g2s_hint(dst + rr * A_LD, X + (rbase + rr) * ld + n0, seg_bytes, &xfull[sx], xpol);
+            else
+              bulk_g2s(dst + rr * A_LD, X + (rbase + rr) * ld + n0, seg_bytes, &xfull[sx]);
+          }
+          if (kb >= NSG) mbar_wait(&gempty[sg], pg);
+          mbar_arrive_expect_tx(&gfull[sg], (unsigned)(G_STAGE * sizeof(double)));
+          bulk_g2s(Gs + sg * G_STAGE, gsrc + (int64_t)kb * G_STAGE, (unsigned)(G_STAGE * sizeof(double)), &gfull[sg]);
+        }
+      }
+      return;
+    }
     constexpr int ROWS_W = SLICE_ROWS / NPW;            // G rows per producer warp (even)
     static_assert(ROWS_W >= 2 && ROWS_W % 2 == 0, "each producer warp needs whole row pairs");
     constexpr int PAIRS_W = (ROWS_W / 2) * BK;
@@ -491,7 +524,8 @@ static cudaError_t launch_ws_t(const SketchDenseArgs& a, cudaStream_t st) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, sketch_ws_kernel<C, CL>, a.X, a.ld, a.rows, a.k, a.lo, a.s, a.seed,
                             a.rows_per_split, a.out, a.out_split_stride, a.accumulate,
-                            ovr().sketch_x_l2 == 1 ? 1 : 0);
+                            ovr().sketch_x_l2 == 1 ? 1 : 0, CL == 1 ? a.G : nullptr,
+                            (a.rows + C::BK - 1) / C::BK);
 }
 
 // Tile shape (override sketch_tile).  Measured on c2 (1e5 x 2000,
@@ -538,7 +572,62 @@ static cudaError_t launch_ws_tile(const SketchDenseArgs& a, cudaStream_t st) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Stored G (the default, LSRN_OPT_SKETCH_G): the G tiles of one launch's rows are
+// generated ONCE by sketch_gen_g_kernel into a bounded workspace buffer, laid out
+// tile by tile exactly as the producer ring stage (BM rows x G_LD, padded), and
+// sketch_ws_kernel streams them with one 5 KB bulk copy per k-block instead of
+// regenerating them in every N-tile CTA.  In-register generation (never stored,
+// SURVEY a1) costs k / BN regenerations of each normal (c5: 20) and its FP64
+// Box-Muller steps share the pipe with the DMMAs; storing costs s * rows * 10 B of
+// HBM writes and one tile read per CTA k-block (from L2 or DRAM).  Measurements:
+// DESIGN.md §6 K2.
+__global__ void __launch_bounds__(256)
+sketch_gen_g_kernel(double* __restrict__ G, int64_t ntm, int64_t nkb, int64_t rows, int64_t jbase, uint64_t seed) {
+  using C = Tile1;
+  __shared__ double bmT[bm::TAB_SIZE];
+  for (int i = threadIdx.x; i < bm::TAB_SIZE; i += blockDim.x) bmT[i] = bm::kTable[i];
+  __syncthreads();
+  const uint2 key = philox_key(seed);
+  constexpr int PAIRS = (C::BM / 2) * C::BK;       // pairs per tile
+  const int64_t total = ntm * nkb * PAIRS;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = p / PAIRS;
+    const int w = (int)(p % PAIRS), qp = w / C::BK, kk = w % C::BK;
+    const int64_t mt = tile / nkb, kb = tile % nkb;
+    const int64_t r = kb * C::BK + kk;
+    double z0 = 0.0, z1 = 0.0;
+    if (r < rows) gaussian_pair(key, (uint64_t)(mt * (C::BM / 2) + qp), (uint64_t)(jbase + r), bmT, z0, z1);
+    double* t = G + tile * C::G_STAGE;
+    t[(2 * qp) * C::G_LD + kk] = z0;
+    t[(2 * qp + 1) * C::G_LD + kk] = z1;
+  }
+}
+
+int64_t sketch_g_row_bytes(int64_t s) {
+  return ((s + Tile1::BM - 1) / Tile1::BM) * (int64_t)Tile1::G_STAGE * 8 / Tile1::BK;
+}
+int64_t sketch_g_block_rows() { return Tile1::BK; }
+size_t sketch_g_bytes(int64_t s, int64_t rows) {
+  const int64_t ntm = (s + Tile1::BM - 1) / Tile1::BM, nkb = (rows + Tile1::BK - 1) / Tile1::BK;
+  return (size_t)ntm * (size_t)nkb * Tile1::G_STAGE * sizeof(double);
+}
+
+static cudaError_t launch_gen_g(const SketchDenseArgs& a, cudaStream_t st) {
+  const int64_t ntm = (a.s + Tile1::BM - 1) / Tile1::BM, nkb = (a.rows + Tile1::BK - 1) / Tile1::BK;
+  const int64_t pairs = ntm * nkb * (Tile1::BM / 2) * Tile1::BK;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((pairs + 255) / 256, 148 * 16));
+  sketch_gen_g_kernel<<<blocks, 256, 0, st>>>(a.G, ntm, nkb, a.rows, a.lo, a.seed);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sketch_ws(const SketchDenseArgs& a, cudaStream_t st) {
+  if (a.G != nullptr) {       // stored G: 32 x 512 tile, no cluster
+    if (a.nsplit > 1 && a.rows_per_split % Tile1::BK != 0) return cudaErrorInvalidValue;
+    cudaError_t e = launch_gen_g(a, st);
+    if (e != cudaSuccess) return e;
+    return launch_ws_t<Tile1, 1>(a, st);
+  }
   if (ovr().sketch_kernel == 2) return launch_cg(a, st);
   return sketch_ws_tile() == 0 ? launch_ws_tile<Tile0>(a, st) : launch_ws_tile<Tile1>(a, st);
 }

@@ -33,7 +33,7 @@ EXPORTS = ["lsrn_last_error", "lsrn_version", "lsrn_nccl_unique_id", "lsrn_ctx_c
 # lsrn_ctx_set_option keys (include/lsrn.h)
 OPTIONS = {"profiling": 1, "svd": 2, "graph_reuse": 3, "hostio_chunk_mb": 4, "lsqr_sync": 5, "bcast_n": 6,
            "sketch_kernel": 100, "sketch_tile": 101, "sketch_maxcl": 102, "sketch_nsplit": 103, "sketch_x_l2": 104,
-           "sketch_chunks": 105,
+           "sketch_chunks": 105, "sketch_g": 106,
            "rowpass_keep": 110, "rowpass_occ": 111, "rowpass_wide1": 112, "rowpass_wide2": 113,
            "rowpass_asyncx": 114, "rowpass_nt": 115, "rowpass_tr": 116, "rowpass_budget_kb": 117,
            "rowpass_wide_slice": 118, "rowpass_pf": 119, "csr_rowdot": 120, "csr_sketch": 121}

@@ -64,14 +64,17 @@ def test_gaussian_entries(ctx):
     (2100, 2048, 1.2, 0.0, 2),      # 8 N-tiles: 8-CTA cluster, padded ld
     (1601, 1536, 1.1, 0.5, 0),      # 6 N-tiles: 2-CTA clusters, Tikhonov block, ragged K
 ])
-@pytest.mark.parametrize("kernel,chunks", [(-1, -1), (2, -1), (-1, 4)])
-def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad, kernel, chunks):
+@pytest.mark.parametrize("kernel,chunks,gmode", [(-1, -1, -1), (-1, -1, 0), (2, -1, -1), (-1, 4, -1), (-1, 4, 0),
+                                             (-1, -1, 1)])
+def test_sketch_tall_small(ctx, m, n, gamma, lam, ld_pad, kernel, chunks, gmode):
     """kernel -1: the planner's choice; 2: sketch_cg_kernel (DMMA warps generate G);
-    chunks 4: the device-resident A sketched in 4 stream-ordered row chunks."""
+    chunks 4: the device-resident A sketched in 4 stream-ordered row chunks;
+    gmode -1: G tiles generated once per launch into the workspace and streamed (default),
+    0: G generated in registers by every CTA, 1: a 1 MB G budget (many launches)."""
     g = torch.Generator().manual_seed(m * 7 + n)
     Xfull = torch.randn(m, n + ld_pad, generator=g, dtype=torch.float64)
     X = Xfull[:, :n]
-    with ctx.options(sketch_kernel=kernel, sketch_chunks=chunks):
+    with ctx.options(sketch_kernel=kernel, sketch_chunks=chunks, sketch_g=gmode):
         At = ctx.sketch(X.cuda() if ld_pad == 0 else Xfull.cuda()[:, :n], m, n, gamma, lam, seed=5981).cpu().numpy()
     p = orc_plan(m, n, gamma, lam)
     ref = orc_sketch(X.numpy(), p["s"], 5981, p["sigma_x"], p["sigma_i"])
