@@ -2,7 +2,7 @@
 """LSRN hot-path benchmark (driver contract).
 
 One step = one full LSRN solve of the configured workload on device-resident
-inputs: Gaussian sketch (K1+K2, DMMA) -> [NCCL allreduce] -> SVD (cuSOLVER,
+inputs: Gaussian sketch (K1 G tiles + K2 DMMA) -> [NCCL allreduce] -> SVD (cuSOLVER,
 outside the hot path, reported separately) -> N -> fused LSQR (or CS)
 iterations (K5/K6/K8, one CUDA graph) -> x.
 
@@ -389,10 +389,11 @@ def main():
                        "algorithmic": f"2*s*nnz = {sketch_flops:.4g} flop per sketch (+ s*cnt normals, not counted)",
                        "peak_source": DFMA_PEAK_NOTE, "share_of_step": sketch_share}
     else:
-        roof_sketch = {"kernel": "sketch_ws_kernel (K1+K2, DMMA, warp-specialized)", "bound": "tensor",
+        roof_sketch = {"kernel": "sketch_gen_g_kernel + sketch_ws_kernel (K1 once per launch into stored G "
+                                 "tiles, K2 DMMA warp-specialized; the sketch stage)", "bound": "tensor",
                        "achieved": sketch_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                        "frac": sketch_tf / FP64_PEAK_TFLOPS, "traffic": None,
-                       "algorithmic": f"2*s*k*L = {sketch_flops:.4g} flop per launch",
+                       "algorithmic": f"2*s*k*L = {sketch_flops:.4g} flop per sketch stage (all its launches)",
                        "peak_source": FP64_PEAK_NOTE, "share_of_step": sketch_share}
     roof_lp = {"kernel": "csr_rowdot + csr_colgather (K6-CSR)" if csr else "rowpass_bulk_kernel long pass (K6)",
                "bound": "hbm", "achieved": lp_gbs, "peak": hbm_peak,
