@@ -221,8 +221,10 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *                           1 warp per row over the full CSR; 2 as 0 with 2 rows per step;
  *                           3 the two-kernel form (row dots, then A^T u gathered from the
  *                           CSC copy) also for k <= 2048
- *   LSRN_OPT_CSR_SKETCH     CSR sketch light part: 0 column-stationary (per nonzero),
- *                           1 generate-once row-stationary slab */
+ *   LSRN_OPT_CSR_SKETCH     CSR sketch: 0 column-stationary light part, G regenerated per
+ *                           nonzero; 1 generate-once row-stationary slab;
+ *                           2 (default) G generated once per chunk of rows (<= 8 GB, or the
+ *                           LSRN_OPT_SKETCH_G budget) and read by the heavy and light kernels */
 enum {
   LSRN_OPT_PROFILING = 1,
   LSRN_OPT_SVD = 2,

@@ -483,10 +483,124 @@ csr_sketch_slab_kernel(const int64_t* __restrict__ colptr, const int32_t* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// Stored-G CSR sketch (csr_sketch = 2, the default when the slab does not pay: c4).
+// The per-nonzero kernel above evaluates G[:, j] once per light nonzero of row j
+// (c4: 20 x s L = 1.6e12 normals, 7.3 s).  Here the rows of the shard are taken in
+// chunks whose G block (s x rows, <= 8 GB) is generated ONCE (csr_gen_g_kernel,
+// G[j][i] with i contiguous), and the heavy and light kernels read it instead of
+// regenerating it: the heavy part streams it row by row, the light part gathers
+// G[j, i-block] per nonzero (2 KB coalesced per 256 sketch rows) and accumulates
+// into the transposed partial Pt[c][i] (coalesced read-modify-write, one per chunk;
+// fixed chunk order: deterministic).  Memory for FLOPs: ~8 B of G traffic per
+// (nonzero, sketch row) instead of a Box-Muller pair per two.
+__global__ void __launch_bounds__(256)
+csr_gen_g_kernel(double* __restrict__ G, int64_t s2, int64_t rows, int64_t jbase, uint64_t seed) {
+  __shared__ double bmT[bm::TAB_SIZE];
+  bm_load_table(bmT);
+  __syncthreads();
+  const uint2 key = philox_key(seed);
+  const int64_t hp = s2 / 2, total = rows * hp;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t jl = p / hp, q = p % hp;
+    double z0, z1;
+    gaussian_pair(key, (uint64_t)q, (uint64_t)(jbase + jl), bmT, z0, z1);
+    *reinterpret_cast<double2*>(G + jl * s2 + 2 * q) = make_double2(z0, z1);
+  }
+}
+
+// Heavy part from stored G: part[split][i][h] (+)= sum_{j in split} G[j][i] D[j][h].
+// The JT rows' G values are loaded before their FMAs (JT loads in flight per thread:
+// one at a time left the kernel latency-bound at 0.33 TB/s, 2 s on c4).
+template <int ND>
+__global__ void __launch_bounds__(THR)
+csr_sketch_heavy_g_kernel(const double* __restrict__ D, int ldd, int nd, int64_t rows, const double* __restrict__ G,
+                          int64_t s2, int64_t s, int64_t rows_per_split, double* __restrict__ part, int accumulate) {
+  constexpr int JT = 16;
+  __shared__ __align__(16) double Ds[JT][ND];
+  const int64_t i = (int64_t)blockIdx.x * THR + threadIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t j1 = min(rows, j0 + rows_per_split);
+  double acc[ND];
+#pragma unroll
+  for (int h = 0; h < ND; ++h) acc[h] = 0.0;
+  for (int64_t jb = j0; jb < j1; jb += JT) {
+    const int nj = (int)min((int64_t)JT, j1 - jb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < JT * ND; e += THR) {
+      const int r = e / ND, h = e % ND;
+      Ds[r][h] = (r < nj && h < nd) ? D[(jb + r) * ldd + h] : 0.0;
+    }
+    __syncthreads();
+    if (i < s) {
+      double z[JT];
+#pragma unroll
+      for (int r = 0; r < JT; ++r) z[r] = r < nj ? G[(jb + r) * s2 + i] : 0.0;
+#pragma unroll
+      for (int r = 0; r < JT; ++r)          // Ds rows past nj are zero
+#pragma unroll
+        for (int h = 0; h < ND; h += 2) {
+          const double2 d = *reinterpret_cast<const double2*>(&Ds[r][h]);
+          acc[h] = fma(z[r], d.x, acc[h]);
+          acc[h + 1] = fma(z[r], d.y, acc[h + 1]);
+        }
+    }
+  }
+  if (i < s) {
+    double* o = part + ((int64_t)blockIdx.y * s + i) * ND;
+#pragma unroll
+    for (int h = 0; h < ND; ++h) o[h] = accumulate ? o[h] + acc[h] : acc[h];
+  }
+}
+
+// Light part from stored G, chunk J (rows [row0, row0 + rows) of the shard):
+// Pt[c][i] (+)= sum over the light entries (j, a) of column c in the chunk of a G[j - row0][i].
+__global__ void __launch_bounds__(THR)
+csr_sketch_light_g_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                          const double* __restrict__ cval, const int* __restrict__ colmap,
+                          const int32_t* __restrict__ cp, int64_t J, int64_t k, int64_t s, int64_t s2,
+                          const double* __restrict__ G, int64_t row0, int cols_per_cta, double* __restrict__ Pt,
+                          int accumulate) {
+  constexpr int NT = 256;
+  __shared__ int32_t js[NT];
+  __shared__ double as[NT];
+  // column groups fastest: the CTAs resident together share one sketch-row block, so
+  // its slice of the chunk's G rows (2 KB each) stays in L2 for the ~20 nonzeros of a row
+  const int64_t i = (int64_t)blockIdx.y * THR + threadIdx.x;
+  const int64_t cb = (int64_t)blockIdx.x * cols_per_cta;
+  for (int64_t c = cb; c < min(k, cb + cols_per_cta); ++c) {
+    if (colmap[c] >= 0) continue;
+    const int64_t e0 = colptr[c] + cp[J * k + c], e1 = colptr[c] + cp[(J + 1) * k + c];
+    double acc = 0.0;
+    for (int64_t eb = e0; eb < e1; eb += NT) {
+      const int ne = (int)min((int64_t)NT, e1 - eb);
+      __syncthreads();
+      if (threadIdx.x < ne) {
+        js[threadIdx.x] = (int32_t)(rowidx[eb + threadIdx.x] - row0);
+        as[threadIdx.x] = cval[eb + threadIdx.x];
+      }
+      __syncthreads();
+      if (i < s) {
+        int e = 0;
+        for (; e + 4 <= ne; e += 4) {          // four gathers in flight
+          const double g0 = G[(int64_t)js[e] * s2 + i], g1 = G[(int64_t)js[e + 1] * s2 + i];
+          const double g2 = G[(int64_t)js[e + 2] * s2 + i], g3 = G[(int64_t)js[e + 3] * s2 + i];
+          acc = fma(g0, as[e], acc);
+          acc = fma(g1, as[e + 1], acc);
+          acc = fma(g2, as[e + 2], acc);
+          acc = fma(g3, as[e + 3], acc);
+        }
+        for (; e < ne; ++e) acc = fma(G[(int64_t)js[e] * s2 + i], as[e], acc);
+      }
+    }
+    if (i < s) Pt[c * s + i] = accumulate ? Pt[c * s + i] + acc : acc;
+  }
+}
+
 // cp[J][c] = number of CSC entries of light column c with row < J * CJ, J = 0..nchunks
 // (warp per column; rows within a CSC column are ascending).  Heavy columns: 0.
 __global__ void csr_chunkptr_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
-                                    const int* __restrict__ colmap, int64_t k, int64_t nchunks,
+                                    const int* __restrict__ colmap, int64_t k, int64_t nchunks, int64_t chunk_rows,
                                     int32_t* __restrict__ cp) {
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -495,8 +609,8 @@ __global__ void csr_chunkptr_kernel(const int64_t* __restrict__ colptr, const in
   const int64_t n = e1 - e0;
   for (int64_t t = lane; t <= n; t += 32) {
     // chunks J in (chunk(t - 1), chunk(t)] start at entry t (chunk(-1) = -1, chunk(n) = nchunks)
-    const int64_t hi = t < n ? rowidx[e0 + t] / slab::CJ : nchunks;
-    const int64_t lo_ = t > 0 ? rowidx[e0 + t - 1] / slab::CJ : -1;
+    const int64_t hi = t < n ? rowidx[e0 + t] / chunk_rows : nchunks;
+    const int64_t lo_ = t > 0 ? rowidx[e0 + t - 1] / chunk_rows : -1;
     for (int64_t J = lo_ + 1; J <= hi; ++J) cp[J * k + c] = (int32_t)t;
   }
 }
@@ -1095,9 +1209,58 @@ int64_t csr_slab_tile_cols() { return slab::CW; }
 int64_t csr_slab_row_blocks(int64_t s) { return (s + slab::IB - 1) / slab::IB; }
 
 cudaError_t launch_csr_chunkptr(const int64_t* colptr, const int32_t* rowidx, const int* colmap, int64_t k,
-                                int64_t nchunks, int32_t* cp, cudaStream_t st) {
+                                int64_t nchunks, int32_t* cp, cudaStream_t st, int64_t chunk_rows) {
   if (k <= 0) return cudaSuccess;
-  csr_chunkptr_kernel<<<(unsigned)((k * 32 + 255) / 256), 256, 0, st>>>(colptr, rowidx, colmap, k, nchunks, cp);
+  if (chunk_rows <= 0) chunk_rows = slab::CJ;
+  csr_chunkptr_kernel<<<(unsigned)((k * 32 + 255) / 256), 256, 0, st>>>(colptr, rowidx, colmap, k, nchunks,
+                                                                       chunk_rows, cp);
+  return cudaGetLastError();
+}
+
+template <int ND>
+static void heavy_g_t(const CsrSketchGArgs& a, const double* G, int64_t rows, int64_t rps, int nsplit, int acc,
+                      cudaStream_t st) {
+  dim3 grid((unsigned)((a.s + THR - 1) / THR), (unsigned)nsplit);
+  csr_sketch_heavy_g_kernel<ND><<<grid, THR, 0, st>>>(a.D + 0, a.ldd, a.nd, rows, G, a.s2, a.s, rps, a.part, acc);
+}
+
+int64_t csr_g_s2(int64_t s) { return (s + 1) / 2 * 2; }
+
+cudaError_t launch_csr_sketch_g(const CsrSketchGArgs& a, cudaStream_t st, int nsm) {
+  const int64_t nch = (a.rows + a.g_rows - 1) / a.g_rows;
+  const unsigned row_blocks = (unsigned)((a.s + THR - 1) / THR);
+  cudaError_t e = launch_csr_chunkptr(a.colptr, a.rowidx, a.colmap, a.k, nch, a.cp, st, a.g_rows);
+  if (e != cudaSuccess) return e;
+  for (int64_t J = 0; J < nch; ++J) {
+    const int64_t r0 = J * a.g_rows, nr = std::min(a.g_rows, a.rows - r0);
+    const int64_t pairs = nr * (a.s2 / 2);
+    csr_gen_g_kernel<<<grid_cap(pairs, 256, (int64_t)nsm * 16), 256, 0, st>>>(a.G, a.s2, nr, a.lo + r0, a.seed);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (a.nd > 0) {
+      const int64_t rps = (nr + a.nsplit - 1) / a.nsplit;
+      const double* D = a.D + r0 * a.ldd;
+      CsrSketchGArgs b = a;
+      b.D = D;
+      switch (a.ND) {
+        case 16: heavy_g_t<16>(b, a.G, nr, rps, a.nsplit, J > 0, st); break;
+        case 32: heavy_g_t<32>(b, a.G, nr, rps, a.nsplit, J > 0, st); break;
+        default: heavy_g_t<64>(b, a.G, nr, rps, a.nsplit, J > 0, st); break;
+      }
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    const int cpc = 16;      // a chunk holds ~g_rows nnz / k entries per column (c4: ~25)
+    dim3 g2((unsigned)((a.k + cpc - 1) / cpc), row_blocks);
+    csr_sketch_light_g_kernel<<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, J, a.k, a.s, a.s2, a.G,
+                                                  r0, cpc, a.Pt, J > 0);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (a.nd > 0) {
+    csr_heavy_finish_kernel<<<grid_cap(a.s * a.nd, 256, (int64_t)nsm * 16), 256, 0, st>>>(
+        a.part, a.nsplit, a.s, a.nd, a.ND, a.heavy_cols, a.k, a.At);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  dim3 g3((unsigned)((a.s + 31) / 32), (unsigned)((a.k + 31) / 32));
+  csr_slab_finish_kernel<<<g3, dim3(32, 8), 0, st>>>(a.Pt, 1, a.s, a.k, a.colmap, a.At);
   return cudaGetLastError();
 }
 

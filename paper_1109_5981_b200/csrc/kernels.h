@@ -33,7 +33,7 @@ struct Overrides {
   int rowpass_pf = -1;        // L2 prefetch distance (tiles) of the bulk row pass, 0 = off
   int csr_rowdot = -1;        // 0 heavy-dense + light-CSR 8 rows/step, 1 warp per row (full CSR), 2 hl 2 rows/step,
                               // 3 the two-kernel form (row dots + CSC gather) also for k <= 2048
-  int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch
+  int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch, 2 stored G
 };
 const Overrides& ovr();
 struct OverrideScope {
@@ -244,7 +244,27 @@ int64_t csr_slab_chunk_rows();
 int64_t csr_slab_tile_cols();
 int64_t csr_slab_row_blocks(int64_t s);
 cudaError_t launch_csr_chunkptr(const int64_t* colptr, const int32_t* rowidx, const int* colmap, int64_t k,
-                                int64_t nchunks, int32_t* cp, cudaStream_t st);
+                                int64_t nchunks, int32_t* cp, cudaStream_t st, int64_t chunk_rows = 0);
+// Stored-G CSR sketch (csr.cu): per chunk of g_rows shard rows, G (g_rows x s2, i contiguous)
+// is generated once and read by the heavy and light kernels; Pt: [k][s] light partial.
+struct CsrSketchGArgs {
+  const double* D;
+  int64_t rows, lo, s, s2, k, g_rows;
+  uint64_t seed;
+  int nd, ND, nsplit, ldd;
+  double* part;            // [nsplit][s][ND] heavy partials
+  const int* heavy_cols;
+  const int* colmap;
+  const int64_t* colptr;
+  const int32_t* rowidx;
+  const double* cval;
+  int32_t* cp;             // [nchunks + 1][k] chunk pointers (filled here)
+  double* G;               // [g_rows][s2]
+  double* Pt;              // [k][s]
+  double* At;
+};
+int64_t csr_g_s2(int64_t s);
+cudaError_t launch_csr_sketch_g(const CsrSketchGArgs& a, cudaStream_t st, int nsm);
 cudaError_t launch_csr_sketch_slab(const CsrSlabArgs& a, cudaStream_t st);
 cudaError_t launch_sketch_add_gblock(double* At, int64_t s, int64_t k, int64_t L, double si, uint64_t seed,
                                      cudaStream_t st, int nsm);

@@ -401,6 +401,12 @@ struct CsrWs {
   int64_t slab_nchunks = 0;
   int32_t* cp = nullptr;
   double* slab_part = nullptr;
+  // stored-G sketch (launch_csr_sketch_g): G rows per chunk, G block, chunk pointers, light partial
+  bool gstore = false;
+  int64_t g_rows = 0;
+  double* G = nullptr;
+  int32_t* cpg = nullptr;
+  double* Pt = nullptr;
   int32_t* lcol;
   double* lval;
   int nsplit;
@@ -441,16 +447,30 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
   const size_t wp_heavy = (size_t)csr_rowdot_blocks(c->nsm) * kMaxHeavy;
   const size_t wp_all = d.k <= csr_rowdot_all_max_k() ? (size_t)csr_rowdot_all_blocks(c->nsm, d.k) * d.k : 0;
   w.wpart = ar.take<double>(std::max(wp_heavy, wp_all));
-  // Light sketch: the generate-once slab kernel generates each G[i, j] once per
-  // 512-column tile, the per-nonzero kernel once per light nonzero of row j; the
-  // slab kernel is chosen when the tiles are fewer than half the nonzeros per row
-  // (t4: 2 tiles vs 21 nonzeros; c4: 40 tiles vs 70) -- override csr_sketch.
-  const int64_t tiles = (d.k + csr_slab_tile_cols() - 1) / csr_slab_tile_cols();
-  const double nnz_row = d.cnt > 0 ? (double)A->nnz / (double)d.cnt : 0.0;
-  w.slab = d.cnt > 0 && A->nnz > 0 &&
-           (ovr().csr_sketch == 1 || (ovr().csr_sketch != 0 && 2.0 * (double)tiles <= nnz_row));
+  // Sketch of the CSR shard: by default the stored-G kernels (G generated once per chunk
+  // of rows, <= 8 GB, and read by the heavy and light kernels): c4 7.33 -> 4.37 s, t4
+  // 267 ms (slab) -> 207 ms (profiles/r02_csr_sketch_modes.jsonl).  Overrides (csr_sketch):
+  // 0 the per-nonzero kernel regenerating G[:, j] per light nonzero, 1 the generate-once
+  // slab kernel (each G[i, j] once per 512-column tile).
+  w.slab = d.cnt > 0 && A->nnz > 0 && ovr().csr_sketch == 1;
+  w.gstore = d.cnt > 0 && A->nnz > 0 && (ovr().csr_sketch == 2 || ovr().csr_sketch == -1);
+  if (w.gstore) {
+    // the stored-G heavy kernel holds ~1 CTA per SM (64 accumulators + 16 staged G values
+    // per thread): split-K for ~16 nearly full waves
+    w.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(16, d.cnt / 256));
+    w.rows_per_split = std::max<int64_t>(1, (d.cnt + w.nsplit - 1) / w.nsplit);
+    w.part = ar.take<double>((size_t)w.nsplit * d.s * kMaxHeavy);
+    const int64_t s2 = csr_g_s2(d.s);
+    const double budget = ovr().sketch_g > 0 ? (double)ovr().sketch_g * 1048576.0 : 8.0e9;   // as the dense G
+    w.g_rows = std::max<int64_t>(1, std::min<int64_t>(d.cnt, (int64_t)(budget / (8.0 * (double)s2))));
+    const int64_t nchg = (d.cnt + w.g_rows - 1) / w.g_rows;
+    w.G = ar.take<double>((size_t)w.g_rows * s2);
+    w.cpg = ar.take<int32_t>((size_t)(nchg + 1) * d.k);
+    w.Pt = ar.take<double>((size_t)d.k * d.s);
+  }
   if (w.slab) {
     w.slab_nchunks = (d.cnt + csr_slab_chunk_rows() - 1) / csr_slab_chunk_rows();
+    const int64_t tiles = (d.k + csr_slab_tile_cols() - 1) / csr_slab_tile_cols();
     const int64_t ctas = csr_slab_row_blocks(d.s) * tiles;
     int64_t ns = (3 * (int64_t)c->nsm + ctas - 1) / ctas;
     ns = std::max<int64_t>(1, std::min<int64_t>({ns, 16, w.slab_nchunks}));
@@ -537,6 +557,35 @@ void csr_prepare(lsrn_ctx* c, const lsrn_matrix* A, const Dims& d, CsrWs& w) {
 
 // Raw sketch S0 = G[:, lo:lo+cnt] X_shard (no scaling, no Tikhonov block) of a CSR shard.
 void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double* At) {
+  if (w.gstore) {
+    CsrSketchGArgs g{};
+    g.D = w.D;
+    g.rows = d.cnt;
+    g.lo = d.lo;
+    g.s = d.s;
+    g.s2 = csr_g_s2(d.s);
+    g.k = d.k;
+    g.g_rows = w.g_rows;
+    g.seed = seed;
+    g.nd = w.nd;
+    g.ND = w.ND;
+    g.nsplit = w.nsplit;
+    g.ldd = w.ldd;
+    g.part = w.part;
+    g.heavy_cols = w.heavy_cols;
+    g.colmap = w.colmap;
+    g.colptr = w.colptr;
+    g.rowidx = w.rowidx;
+    g.cval = w.cval;
+    g.cp = w.cpg;
+    g.G = w.G;
+    g.Pt = w.Pt;
+    g.At = At;
+    LSRN_CUDA(launch_csr_sketch_g(g, c->stream, c->nsm));
+    const int64_t nchg = (d.cnt + w.g_rows - 1) / w.g_rows;
+    c->launches += 1 + (int)nchg * (2 + (w.nd > 0 ? 1 : 0)) + (w.nd > 0 ? 1 : 0) + 1;
+    return;
+  }
   CsrSketchArgs a{};
   a.D = w.D;
   a.rows = d.cnt;
@@ -1427,7 +1476,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_ROWPASS_WIDE_SLICE: if (!(value == -1 || in(512, 1 << 20))) return bad(); o.rowpass_wide_slice = (int)value; break;
     case LSRN_OPT_ROWPASS_PF: if (!in(-1, 8)) return bad(); o.rowpass_pf = (int)value; break;
     case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 3)) return bad(); o.csr_rowdot = (int)value; break;
-    case LSRN_OPT_CSR_SKETCH: if (!in(-1, 1)) return bad(); o.csr_sketch = (int)value; break;
+    case LSRN_OPT_CSR_SKETCH: if (!in(-1, 2)) return bad(); o.csr_sketch = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
   }
   return LSRN_OK;

@@ -70,12 +70,14 @@ def _relfro(a, b):
     (2597, 1300, 9, 0, 0.0, 3),      # 3 column tiles of the slab kernel, ragged last chunk and tile
     (1100, 530, 4, 40, 0.25, 0),     # 2 tiles, heavy + light, Tikhonov block
 ])
-@pytest.mark.parametrize("light", [0, 1])
-def test_csr_sketch_vs_oracle(ctx, m, n, nnz_row, dense_cols, lam, empty, light):
+@pytest.mark.parametrize("light,gmb", [(0, -1), (1, -1), (2, -1), (2, 1)])
+def test_csr_sketch_vs_oracle(ctx, m, n, nnz_row, dense_cols, lam, empty, light, gmb):
     """light = 0: per-nonzero light sketch (G[:, j] regenerated per nonzero); light = 1:
-    the generate-once slab kernel (each G[i, j] once per 512-column tile)."""
+    the generate-once slab kernel (each G[i, j] once per 512-column tile); light = 2: G
+    generated once per chunk of rows and read by the heavy and light kernels (gmb = 1: a
+    1 MB G budget, so several chunks)."""
     A = _random_csr(m, n, nnz_row, dense_cols, 1e3, empty, seed=m + n)
-    with ctx.options(csr_sketch=light):
+    with ctx.options(csr_sketch=light, sketch_g=gmb):
         At = ctx.sketch(_gpu_csr(A), m, n, 2.0, lam, seed=5981).cpu().numpy()
     p = orc_plan(m, n, 2.0, lam)
     ref = orc_sketch(A, p["s"], 5981, p["sigma_x"], p["sigma_i"])
@@ -90,11 +92,11 @@ def test_csr_sketch_equals_dense_sketch(ctx):
     assert _relfro(a1, a2) <= 1e-13
 
 
-@pytest.mark.parametrize("light", [0, 1])
-def test_csr_sketch_shards_sum_to_full(ctx, light):
+@pytest.mark.parametrize("light,gmb", [(0, -1), (1, -1), (2, -1), (2, 1)])
+def test_csr_sketch_shards_sum_to_full(ctx, light, gmb):
     m, n = 3100, 70
     A = _random_csr(m, n, 4, 5, 100.0, 0, seed=2)
-    with ctx.options(csr_sketch=light):
+    with ctx.options(csr_sketch=light, sketch_g=gmb):
         full = ctx.sketch(_gpu_csr(A), m, n).cpu().numpy()
         acc = np.zeros_like(full)
         for lo, hi in [(0, 999), (999, 1000), (1000, 3100)]:
