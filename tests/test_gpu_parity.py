@@ -253,15 +253,17 @@ def test_host_io_matches_device(ctx):
 
 
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
-def test_host_io_streamed(ctx, solver):
+@pytest.mark.parametrize("gmb", [-1, 1])
+def test_host_io_streamed(ctx, solver, gmb):
     """LSRN_HOST_IO with A streamed in chunks (each sketched as soon as its copy lands):
     same solution as the device-resident call up to the split-K summation order of the
-    sketch.  A 2 MB first chunk cuts the 19.2 MB A into 10 chunks."""
+    sketch.  A 2 MB first chunk cuts the 19.2 MB A into 10 chunks; gmb = 1: a 1 MB budget
+    of stored G tiles splits every chunk into several sketch launches."""
     g = torch.Generator().manual_seed(5)
     m, n = 40000, 60
     X = torch.randn(m, n, generator=g, dtype=torch.float64)
     b = torch.randn(m, generator=g, dtype=torch.float64)
-    with ctx.options(hostio_chunk_mb=2):
+    with ctx.options(hostio_chunk_mb=2, sketch_g=gmb):
         xd, rd = ctx.solve(X.cuda(), b.cuda(), m, n, solver=solver)
         xh, rh = ctx.solve(X.pin_memory(), b.pin_memory(), m, n, solver=solver, host_io=True)
     xs = np.linalg.lstsq(X.numpy(), b.numpy(), rcond=None)[0]
