@@ -135,8 +135,8 @@ typedef struct {
   double sigma_L, sigma_U, alpha;   /* Thm 4.4 bounds used */
   double t_sketch, t_allreduce, t_svd, t_iter, t_total;  /* seconds (CUDA events) */
   double rnorm_est;      /* LSQR phibar estimate of ||Abar y - bbar|| (0 for CS) */
-  int32_t svd_used;      /* SVD method that produced N: LSRN_SVD_JW / _GESVD / _POLAR (a rejected
-                            polar result redone with gesvd reports LSRN_SVD_GESVD) */
+  int32_t svd_used;      /* method that produced N: LSRN_SVD_QR (N = R^{-1}) / _JW / _GESVD / _POLAR
+                            (a rejected polar result redone with gesvd reports LSRN_SVD_GESVD) */
   int32_t collectives;   /* collective calls issued by this rank during the solve (sketch
                             allreduce, non-finite flag, sigma / N broadcasts, per-pass reductions);
                             0 with one rank and no communicator */
@@ -173,11 +173,17 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
 /* Context options (lsrn_ctx_set_option).  Values are validated (LSRN_EINVAL on
  * an unknown option or value).  The product options:
  *   LSRN_OPT_PROFILING      0/1, as lsrn_ctx_set_profiling.
- *   LSRN_OPT_SVD            how the SVD of the s x k sketch is computed (Alg. 1/2
- *                           step 4; outside the hot path).  Every method
- *                           is a true SVD (no Gram matrix):
- *                           LSRN_SVD_AUTO (default): Jordan-Wielandt eigenproblem of R
- *                             for k <= 16384, else LSRN_SVD_POLAR;
+ *   LSRN_OPT_SVD            how N is obtained from the s x k sketch (Alg. 1/2 steps 4-5,
+ *                           P:489-495; outside the hot path).  Every SVD method is a
+ *                           true SVD (no Gram matrix):
+ *                           LSRN_SVD_AUTO (default) = LSRN_SVD_QR, falling back to the
+ *                             Jordan-Wielandt eigenproblem of R for k <= 4095 and to
+ *                             LSRN_SVD_POLAR above;
+ *                           LSRN_SVD_QR: geqrf, then N = R^{-1} (trtri) when R is
+ *                             certified full rank under the rank rule (kappa_F(R) <
+ *                             1e-2 / (max(s, k) 2^-52); C23): the same
+ *                             preconditioned singular values as V Sigma^{-1}; otherwise
+ *                             the SVD as for AUTO;
  *                           LSRN_SVD_JW: geqrf, then syevdx on [[0, R^T], [R, 0]]
  *                             (k <= 16384, cuSOLVER's symmetric-eigensolver limit);
  *                           LSRN_SVD_GESVD: geqrf, then gesvd of R;
@@ -252,7 +258,7 @@ enum {
   LSRN_OPT_CSR_ROWDOT = 120,
   LSRN_OPT_CSR_SKETCH = 121
 };
-enum { LSRN_SVD_AUTO = 0, LSRN_SVD_JW = 1, LSRN_SVD_GESVD = 2, LSRN_SVD_POLAR = 3 };
+enum { LSRN_SVD_AUTO = 0, LSRN_SVD_JW = 1, LSRN_SVD_GESVD = 2, LSRN_SVD_POLAR = 3, LSRN_SVD_QR = 4 };
 lsrn_status lsrn_ctx_set_option(lsrn_ctx* ctx, int option, int64_t value);
 
 /* Host-staged collectives for nranks > 1 without NCCL (any host transport: MPI,

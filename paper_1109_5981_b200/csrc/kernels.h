@@ -338,6 +338,9 @@ cudaError_t launch_form_nt(const double* VT, const double* S, int64_t k, int64_t
 
 // V column-major k x k (gesvdp): Nt[c][j] = V[j + c k] / S[c]
 cudaError_t launch_form_nt_v(const double* V, const double* S, int64_t k, int64_t r, double* Nt, cudaStream_t st);
+// out[0] = ||A||^2, out[1] = ||B||^2 over n entries (fixed order); part: sumsq2_part_size() doubles
+cudaError_t launch_sumsq2(const double* A, const double* B, int64_t n, double* part, double* out, cudaStream_t st);
+int sumsq2_part_size();
 // flag[0] <- 1.0 if any of p[0..n) is not finite (never cleared here)
 cudaError_t launch_check_finite(const double* p, int64_t n, double* flag, cudaStream_t st);
 

@@ -127,6 +127,8 @@ struct lsrn_ctx {
   std::vector<int64_t> graph_key;
   int graph_launches = 0, graph_pass_ev = 0;
   int svd_polar_fallbacks = 0;        // polar SVD results rejected (redone with gesvd)
+  int svd_qr_fallbacks = 0;           // QR routes not certified full rank (SVD computed instead)
+  double qr_kappa_f = 0.0;            // kappa_F(R) of the last certified QR route
   int svd_used = 0;                   // method that produced N in the last solve
   int collectives = 0;                // collective calls of the current call (reported)
   int graph_collectives = 0;          // ... inside the cached iteration graph
@@ -845,6 +847,8 @@ struct SvdWs {
   int* info;
   int method;                            // LSRN_SVD_JW / _GESVD / _POLAR (polar may fall back)
   bool fallback_jw;                      // a rejected polar result is redone with JW (else gesvd)
+  bool try_qr;                           // N = R^{-1} when R is certified full rank (C23), else `method`
+  double* red;                           // sumsq2 partials + the two norms
 };
 
 // 64-bit cuSOLVER API: the c4 shape (s x k = 4e4 x 2e4) needs workspaces beyond
@@ -856,7 +860,9 @@ SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   // auto: the polar route from k = 4096 up (c5, k = 1e4: 2.5 s against 4.4 s for the
   // Jordan-Wielandt eigenproblem, profiles/r02_svd_c5.jsonl), falling back to JW (or
   // gesvd above its limit) when the polar result is rejected; JW below (c2: 80 ms)
-  if (w.method == LSRN_SVD_AUTO) w.method = (k >= kPolarMinK || 2 * k > kMaxJW) ? LSRN_SVD_POLAR : LSRN_SVD_JW;
+  w.try_qr = w.method == LSRN_SVD_AUTO || w.method == LSRN_SVD_QR;
+  if (w.method == LSRN_SVD_AUTO || w.method == LSRN_SVD_QR)
+    w.method = (k >= kPolarMinK || 2 * k > kMaxJW) ? LSRN_SVD_POLAR : LSRN_SVD_JW;
   w.fallback_jw = (w.method == LSRN_SVD_POLAR) && (2 * k <= kMaxJW);
   LSRN_REQUIRE(!(w.method == LSRN_SVD_JW && 2 * k > kMaxJW), LSRN_EUNSUPPORTED,
                "LSRN_SVD_JW needs min(m, n) <= 16384 (cuSOLVER symmetric eigensolver limit)");
@@ -882,8 +888,12 @@ SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
                                                nullptr, k, CUDA_R_64F, nullptr, CUDA_R_64F, nullptr, k, CUDA_R_64F,
                                                nullptr, k, CUDA_R_64F, &d3, &h3));
   }
-  w.work_bytes = std::max({d1, d2, d3});
-  w.host_bytes = std::max({h1, h2, h3});
+  size_t d5 = 0, h5 = 0;
+  if (w.try_qr)
+    LSRN_SOLVER(cusolverDnXtrtri_bufferSize(c->solver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, k, CUDA_R_64F,
+                                            nullptr, k, &d5, &h5));
+  w.work_bytes = std::max({d1, d2, d3, d5});
+  w.host_bytes = std::max({h1, h2, h3, h5});
   w.W1 = ar.take<double>((size_t)d.s * k);
   w.tau = ar.take<double>((size_t)k);
   const int nblk = (w.method == LSRN_SVD_JW || w.fallback_jw) ? 4 : (w.method == LSRN_SVD_POLAR ? 3 : 2);
@@ -894,6 +904,7 @@ SvdWs plan_svd(lsrn_ctx* c, const Dims& d, Arena& ar) {
   w.work = ar.take<char>(w.work_bytes + 16);
   w.Nt = ar.take<double>((size_t)k * k);
   w.info = ar.take<int>(4);
+  w.red = ar.take<double>((size_t)sumsq2_part_size() + 2);
   return w;
 }
 
@@ -928,6 +939,38 @@ int64_t svd_local(lsrn_ctx* c, const Dims& d, const double* At, const SvdWs& w, 
                      std::to_string(info[1]) + ", values " + std::to_string(meig));
   };
   double* R = w.JW;                          // gesvd / polar: R (k x k) first
+  if (w.try_qr) {
+    // Reading C23: N = R^{-1} (Ã = Q R) preconditions exactly as N = V Sigma^{-1}:
+    // R^{-1} = V Sigma^{-1} U_R^T, so A R^{-1} = (A V Sigma^{-1}) U_R^T has the same
+    // singular values (Lemma 4.2 / Thm 4.4) and LSQR / CS the same iterates up
+    // to that rotation of y.  Used only when R is certified full rank under the rank rule
+    // C4: kappa_F(R) = ||R||_F ||R^{-1}||_F >= kappa_2(R), required below
+    // 1e-2 / (max(s, k) 2^-52); otherwise (rank-deficient or nearly so) the SVD route.
+    double* Ri = w.JW + (size_t)k * k;
+    LSRN_CUDA(launch_extract_r(w.W1, d.s, k, R, st));
+    LSRN_CUDA(launch_extract_r(w.W1, d.s, k, Ri, st));
+    c->launches += 2;
+    LSRN_SOLVER(cusolverDnXtrtri(c->solver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, k, CUDA_R_64F, Ri, k, w.work,
+                                 w.work_bytes, c->host_ws.data(), w.host_bytes, w.info + 1));
+    LSRN_CUDA(launch_sumsq2(R, Ri, k * k, w.red, w.red + sumsq2_part_size(), st));
+    c->launches += 2;
+    double nrm[2] = {0.0, 0.0};
+    LSRN_CUDA(cudaMemcpyAsync(nrm, w.red + sumsq2_part_size(), sizeof(nrm), cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaMemcpyAsync(info, w.info, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+    LSRN_CUDA(cudaStreamSynchronize(st));
+    LSRN_REQUIRE(info[0] == 0, LSRN_ESVD, "cuSOLVER geqrf info = " + std::to_string(info[0]));
+    const double kf = std::sqrt(nrm[0]) * std::sqrt(nrm[1]);
+    const double tau = (double)std::max(d.s, k) * std::ldexp(1.0, -52);
+    if (info[1] == 0 && std::isfinite(kf) && nrm[0] > 0.0 && kf * tau < 1e-2) {
+      // Nt row-major r x k = N column-major: R^{-1} (column-major, zero below the diagonal)
+      LSRN_CUDA(cudaMemcpyAsync(w.Nt, Ri, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+      c->svd_used = LSRN_SVD_QR;
+      c->qr_kappa_f = kf;
+      S_host.assign((size_t)k, 1.0);         // certified: r = k under C4 (sigma are not computed)
+      return k;
+    }
+    c->svd_qr_fallbacks++;
+  }
   auto gesvd = [&]() {
     double* VT = w.JW + (size_t)k * k;
     LSRN_CUDA(launch_extract_r(w.W1, d.s, k, R, st));
@@ -1453,7 +1496,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
   Overrides& o = c->ovr;
   switch (option) {
     case LSRN_OPT_PROFILING: if (!in(0, 1)) return bad(); c->profile = value != 0; break;
-    case LSRN_OPT_SVD: if (!in(LSRN_SVD_AUTO, LSRN_SVD_POLAR)) return bad(); c->svd_method = (int)value; break;
+    case LSRN_OPT_SVD: if (!in(LSRN_SVD_AUTO, LSRN_SVD_QR)) return bad(); c->svd_method = (int)value; break;
     case LSRN_OPT_GRAPH_REUSE: if (!in(0, 1)) return bad(); c->graph_reuse = value != 0; break;
     case LSRN_OPT_HOSTIO_CHUNK_MB: if (!in(1, 1 << 20)) return bad(); c->hostio_chunk_mb = (double)value; break;
     case LSRN_OPT_LSQR_SYNC: if (!in(0, 1)) return bad(); c->lsqr_sync = (int)value; break;

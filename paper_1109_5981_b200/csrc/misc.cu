@@ -160,6 +160,55 @@ cudaError_t launch_form_nt_v(const double* V, const double* S, int64_t k, int64_
   return cudaGetLastError();
 }
 
+// out[0] = sum A[i]^2, out[1] = sum B[i]^2 (i < n), in a fixed order: per-block partials
+// (grid-stride, fixed tree) then one block over the partials.  part: 2 * SUMSQ_BLOCKS doubles.
+constexpr int SUMSQ_BLOCKS = 296;
+__global__ void sumsq2_part_kernel(const double* __restrict__ A, const double* __restrict__ B, int64_t n,
+                                   double* __restrict__ part) {
+  __shared__ double sh[2][8];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    a = fma(A[i], A[i], a);
+    b = fma(B[i], B[i], b);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = a;
+    sh[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      x += sh[0][w];
+      y += sh[1][w];
+    }
+    part[2 * blockIdx.x] = x;
+    part[2 * blockIdx.x + 1] = y;
+  }
+}
+__global__ void sumsq2_final_kernel(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      x += part[2 * b];
+      y += part[2 * b + 1];
+    }
+    out[0] = x;
+    out[1] = y;
+  }
+}
+
+cudaError_t launch_sumsq2(const double* A, const double* B, int64_t n, double* part, double* out, cudaStream_t st) {
+  sumsq2_part_kernel<<<SUMSQ_BLOCKS, 256, 0, st>>>(A, B, n, part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  sumsq2_final_kernel<<<1, 32, 0, st>>>(part, SUMSQ_BLOCKS, out);
+  return cudaGetLastError();
+}
+int sumsq2_part_size() { return 2 * SUMSQ_BLOCKS; }
+
 // flag[0] = 1.0 if any p[i] (i < n) is NaN or +-Inf (flag is only ever set, never
 // cleared, so several arrays can be checked into one flag).
 __global__ void check_finite_kernel(const double* __restrict__ p, int64_t n, double* flag) {

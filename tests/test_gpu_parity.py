@@ -172,22 +172,31 @@ def test_single_column_or_row(ctx, shape):
         assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-12 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
-@pytest.mark.parametrize("method", ["gesvd", "polar"])
+SVD_USED = {  # (method, config) -> lsrn_report.svd_used (1 JW, 2 gesvd, 3 polar, 4 N = R^-1)
+    ("gesvd", "c2"): 2, ("gesvd", "c3"): 2, ("polar", "c2"): 1, ("polar", "c3"): 3,
+    ("jw", "c2"): 1, ("jw", "c3"): 1, ("qr", "c2"): 1, ("qr", "c3"): 4, ("auto", "c2"): 1, ("auto", "c3"): 4,
+    ("auto", "c5"): 4, ("jw", "c5"): 1, ("qr", "c5"): 4,
+}
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+@pytest.mark.parametrize("method", ["gesvd", "polar", "jw", "qr", "auto"])
 def test_svd_methods_small(ctx, name, method):
-    """The SVD methods of the large-k configs, forced at small size: polar (gesvdp of R,
-    the default from k = 4096, accepted only for clearly full-rank R) and gesvd of R (the
-    fallback above the Jordan-Wielandt limit, k > 16384): same rank, counts and solution
-    as the oracle (rank-deficient c2 -- where the polar result must be rejected and
-    redone -- and Tikhonov c3)."""
+    """Every way of forming N, forced at small size: polar (gesvdp of R, accepted only for
+    clearly full-rank R), gesvd of R, the Jordan-Wielandt eigenproblem, and the QR route
+    (N = R^{-1} when R is certified full rank, reading C23; the default): same rank, counts
+    and solution as the oracle's SVD-based N (rank-deficient c2 -- where the polar and QR
+    routes must give way to the SVD -- Tikhonov c3, graded c5)."""
+    if (method, name) not in SVD_USED:
+        pytest.skip("covered by the other configs")
     p = small(name)
     A = p.dense_A().numpy()
     b = p.b.numpy()
     with ctx.options(svd=method):
         x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs", lam=p.lam)
-    # c2's sketch has rank 1800 < k: the polar result is rejected and redone with the
-    # Jordan-Wielandt eigensolver (k <= 16384)
-    assert rep["svd_used"] == (2 if method == "gesvd" else (1 if name == "c2" else 3))
+    # c2's sketch has rank 1800 < k: the polar result is rejected, and R is not certified,
+    # so both are redone with the Jordan-Wielandt eigensolver (k <= 16384)
+    assert rep["svd_used"] == SVD_USED[(method, name)]
     orc = orc_solve(A, b, solver="cs", lam=p.lam)
     assert rep["r"] == orc["r"] and rep["iters"] == orc["iters"]
     sv = np.linalg.svd(A, compute_uv=False)
