@@ -230,7 +230,8 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *   LSRN_OPT_CSR_SKETCH     CSR sketch: 0 column-stationary light part, G regenerated per
  *                           nonzero; 1 generate-once row-stationary slab;
  *                           2 (default) G generated once per chunk of rows (<= 8 GB, or the
- *                           LSRN_OPT_SKETCH_G budget) and read by the heavy and light kernels */
+ *                           LSRN_OPT_SKETCH_G budget) and read by the heavy and light kernels
+ *   LSRN_OPT_CSR_HEAVY_FMA  stored-G heavy block: 1 = FP64-FMA kernel instead of the DMMA GEMM */
 enum {
   LSRN_OPT_PROFILING = 1,
   LSRN_OPT_SVD = 2,
@@ -256,7 +257,8 @@ enum {
   LSRN_OPT_ROWPASS_WIDE_SLICE = 118,
   LSRN_OPT_ROWPASS_PF = 119,
   LSRN_OPT_CSR_ROWDOT = 120,
-  LSRN_OPT_CSR_SKETCH = 121
+  LSRN_OPT_CSR_SKETCH = 121,
+  LSRN_OPT_CSR_HEAVY_FMA = 123
 };
 enum { LSRN_SVD_AUTO = 0, LSRN_SVD_JW = 1, LSRN_SVD_GESVD = 2, LSRN_SVD_POLAR = 3, LSRN_SVD_QR = 4 };
 lsrn_status lsrn_ctx_set_option(lsrn_ctx* ctx, int option, int64_t value);

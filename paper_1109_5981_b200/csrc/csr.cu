@@ -553,6 +553,82 @@ csr_sketch_heavy_g_kernel(const double* __restrict__ D, int ldd, int nd, int64_t
   }
 }
 
+// Heavy part from stored G on the FP64 tensor cores: part[split] (s x ND) (+)= G^T D over
+// the split's rows, a GEMM with M = s, N = ND, K = rows.  CTA = 64 sketch rows x ND, 4
+// warps of 16 x ND (DMMA.8x8x4 fragments), K in steps of 16 rows with both operand
+// tiles (G rows are contiguous in i, D rows in h) double-buffered by cp.async.
+constexpr int HM_M = 64, HM_K = 16, HM_THREADS = 128;
+template <int ND>
+__global__ void __launch_bounds__(HM_THREADS)
+csr_sketch_heavy_mma_kernel(const double* __restrict__ D, int ldd, int nd, int64_t rows, const double* __restrict__ G,
+                            int64_t s2, int64_t s, int64_t rows_per_split, double* __restrict__ part, int accumulate) {
+  constexpr int LDG = HM_M + 4, LDD = ND + 4, NJ = ND / 8;
+  __shared__ __align__(16) double Gs[2][HM_K][LDG];
+  __shared__ __align__(16) double Ds[2][HM_K][LDD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * HM_M;
+  const int64_t j0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t j1 = min(rows, j0 + rows_per_split);
+  const int nk = j1 > j0 ? (int)((j1 - j0 + HM_K - 1) / HM_K) : 0;
+  const int64_t mvalid = min((int64_t)HM_M, s - i0);           // sketch rows of this tile
+  auto issue = [&](int kb, int b) {
+    const int64_t jb = j0 + (int64_t)kb * HM_K;
+    // G: HM_K rows x HM_M doubles (16-byte pieces; rows / sketch rows past the end read nothing, zero-filled)
+    for (int e = tid; e < HM_K * HM_M / 2; e += HM_THREADS) {
+      const int kk = e / (HM_M / 2), m2 = 2 * (e % (HM_M / 2));
+      const bool ok = jb + kk < j1 && m2 < mvalid;
+      const int nb = ok ? (m2 + 1 < mvalid ? 16 : 8) : 0;
+      cp_async16(&Gs[b][kk][m2], ok ? G + (jb + kk) * s2 + i0 + m2 : G, nb);
+    }
+    for (int e = tid; e < HM_K * ND / 2; e += HM_THREADS) {
+      const int kk = e / (ND / 2), h2 = 2 * (e % (ND / 2));
+      const bool ok = jb + kk < j1 && h2 < nd;
+      const int nb = ok ? (h2 + 1 < nd ? 16 : 8) : 0;
+      cp_async16(&Ds[b][kk][h2], ok ? D + (jb + kk) * ldd + h2 : D, nb);
+    }
+  };
+  double acc[2][NJ][2];
+#pragma unroll
+  for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+    for (int fj = 0; fj < NJ; ++fj) acc[fi][fj][0] = acc[fi][fj][1] = 0.0;
+  if (nk > 0) issue(0, 0);
+  cp_async_commit();
+  for (int kb = 0; kb < nk; ++kb) {
+    const int b = kb & 1;
+    if (kb + 1 < nk) issue(kb + 1, b ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < HM_K / 4; ++ks) {
+      const int k = ks * 4 + (lane & 3);
+      double a[2], bf[NJ];
+#pragma unroll
+      for (int fi = 0; fi < 2; ++fi) a[fi] = Gs[b][k][warp * 16 + fi * 8 + (lane >> 2)];
+#pragma unroll
+      for (int fj = 0; fj < NJ; ++fj) bf[fj] = Ds[b][k][fj * 8 + (lane >> 2)];
+#pragma unroll
+      for (int fi = 0; fi < 2; ++fi)
+#pragma unroll
+        for (int fj = 0; fj < NJ; ++fj) dmma884(acc[fi][fj], a[fi], bf[fj]);
+    }
+    __syncthreads();                      // buffer b is refilled two steps later
+  }
+#pragma unroll
+  for (int fi = 0; fi < 2; ++fi) {
+    const int64_t i = i0 + warp * 16 + fi * 8 + (lane >> 2);
+    if (i >= s) continue;
+    double* o = part + ((int64_t)blockIdx.y * s + i) * ND;
+#pragma unroll
+    for (int fj = 0; fj < NJ; ++fj) {
+      const int h = fj * 8 + 2 * (lane & 3);
+      o[h] = accumulate ? o[h] + acc[fi][fj][0] : acc[fi][fj][0];
+      o[h + 1] = accumulate ? o[h + 1] + acc[fi][fj][1] : acc[fi][fj][1];
+    }
+  }
+}
+
 // Light part from stored G, chunk J (rows [row0, row0 + rows) of the shard):
 // Pt[c][i] (+)= sum over the light entries (j, a) of column c in the chunk of a G[j - row0][i].
 __global__ void __launch_bounds__(THR)
@@ -1220,8 +1296,13 @@ cudaError_t launch_csr_chunkptr(const int64_t* colptr, const int32_t* rowidx, co
 template <int ND>
 static void heavy_g_t(const CsrSketchGArgs& a, const double* G, int64_t rows, int64_t rps, int nsplit, int acc,
                       cudaStream_t st) {
-  dim3 grid((unsigned)((a.s + THR - 1) / THR), (unsigned)nsplit);
-  csr_sketch_heavy_g_kernel<ND><<<grid, THR, 0, st>>>(a.D + 0, a.ldd, a.nd, rows, G, a.s2, a.s, rps, a.part, acc);
+  if (ovr().csr_heavy_fma == 1) {          // the FP64-FMA kernel (reference for the DMMA one)
+    dim3 grid((unsigned)((a.s + THR - 1) / THR), (unsigned)nsplit);
+    csr_sketch_heavy_g_kernel<ND><<<grid, THR, 0, st>>>(a.D + 0, a.ldd, a.nd, rows, G, a.s2, a.s, rps, a.part, acc);
+    return;
+  }
+  dim3 grid((unsigned)((a.s + HM_M - 1) / HM_M), (unsigned)nsplit);
+  csr_sketch_heavy_mma_kernel<ND><<<grid, HM_THREADS, 0, st>>>(a.D, a.ldd, a.nd, rows, G, a.s2, a.s, rps, a.part, acc);
 }
 
 int64_t csr_g_s2(int64_t s) { return (s + 1) / 2 * 2; }

@@ -34,6 +34,7 @@ struct Overrides {
   int csr_rowdot = -1;        // 0 heavy-dense + light-CSR 8 rows/step, 1 warp per row (full CSR), 2 hl 2 rows/step,
                               // 3 the two-kernel form (row dots + CSC gather) also for k <= 2048
   int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch, 2 stored G
+  int csr_heavy_fma = -1;     // stored-G heavy block: 1 = FP64-FMA kernel instead of DMMA
 };
 const Overrides& ovr();
 struct OverrideScope {

@@ -1520,6 +1520,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_ROWPASS_PF: if (!in(-1, 8)) return bad(); o.rowpass_pf = (int)value; break;
     case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 3)) return bad(); o.csr_rowdot = (int)value; break;
     case LSRN_OPT_CSR_SKETCH: if (!in(-1, 2)) return bad(); o.csr_sketch = (int)value; break;
+    case LSRN_OPT_CSR_HEAVY_FMA: if (!in(-1, 1)) return bad(); o.csr_heavy_fma = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
   }
   return LSRN_OK;

@@ -70,14 +70,14 @@ def _relfro(a, b):
     (2597, 1300, 9, 0, 0.0, 3),      # 3 column tiles of the slab kernel, ragged last chunk and tile
     (1100, 530, 4, 40, 0.25, 0),     # 2 tiles, heavy + light, Tikhonov block
 ])
-@pytest.mark.parametrize("light,gmb", [(0, -1), (1, -1), (2, -1), (2, 1)])
-def test_csr_sketch_vs_oracle(ctx, m, n, nnz_row, dense_cols, lam, empty, light, gmb):
+@pytest.mark.parametrize("light,gmb,hfma", [(0, -1, -1), (1, -1, -1), (2, -1, -1), (2, 1, -1), (2, -1, 1)])
+def test_csr_sketch_vs_oracle(ctx, m, n, nnz_row, dense_cols, lam, empty, light, gmb, hfma):
     """light = 0: per-nonzero light sketch (G[:, j] regenerated per nonzero); light = 1:
     the generate-once slab kernel (each G[i, j] once per 512-column tile); light = 2: G
     generated once per chunk of rows and read by the heavy and light kernels (gmb = 1: a
-    1 MB G budget, so several chunks)."""
+    1 MB G budget, so several chunks; hfma = 1: the FP64-FMA heavy kernel instead of DMMA)."""
     A = _random_csr(m, n, nnz_row, dense_cols, 1e3, empty, seed=m + n)
-    with ctx.options(csr_sketch=light, sketch_g=gmb):
+    with ctx.options(csr_sketch=light, sketch_g=gmb, csr_heavy_fma=hfma):
         At = ctx.sketch(_gpu_csr(A), m, n, 2.0, lam, seed=5981).cpu().numpy()
     p = orc_plan(m, n, 2.0, lam)
     ref = orc_sketch(A, p["s"], 5981, p["sigma_x"], p["sigma_i"])

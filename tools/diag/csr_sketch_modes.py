@@ -16,6 +16,9 @@ modes = [int(a) for a in sys.argv[2:]] or [0, 2]
 p = make_problem(cfg, device="cuda")
 X = lsrn.Csr(p.rowptr, p.colind, p.val)
 ctx = lsrn.Context()
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _opts import apply_env_options  # noqa: E402
+apply_env_options(ctx)               # LSRN_OPT_* of the environment (e.g. LSRN_OPT_CSR_HEAVY_FMA)
 ref = None
 for mode in modes:
     ctx.set_option("csr_sketch", mode)
