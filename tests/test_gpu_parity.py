@@ -438,3 +438,21 @@ def test_lambda_path_reuses_the_sketch(ctx, solver, shape):
         assert np.linalg.norm(x.cpu().numpy() - ref) <= 1e-9 * np.linalg.norm(ref)
     with pytest.raises(LsrnError, match="EINVAL"):        # a different seed has no cached sketch
         ctx.solve(X, bd, m, n, solver=solver, lam=0.5, seed=1, reuse_sketch=True)
+
+
+@pytest.mark.parametrize("log_range,expect", [(6.0, 4), (11.0, 1)])
+def test_qr_route_certificate(ctx, log_range, expect):
+    """Reading C23's certificate: a full-rank sketch with kappa = 1e6 takes N = R^-1
+    (svd_used 4); one with kappa = 1e11 -- still full rank under the rank rule C4
+    (threshold 8.9e-14 sigma_1 at s = 400) but not under the certificate kappa_F(R) <
+    1e-2 / (max(s, k) 2^-52) = 1.1e11 (kappa_F ~ 2-3 kappa here) -- gets the
+    Jordan-Wielandt SVD (svd_used 1).  Both: r = k, the oracle's counts, and x in the
+    A-norm form (compensated products, so that kappa = 1e11 does not set the floor)."""
+    p = make_problem("c1", m=3000, n=200, log_range=log_range)
+    A, b = p.X.numpy(), p.b.numpy()
+    x, rep = ctx.solve(p.X.cuda(), p.b.cuda(), p.m, p.n, solver="cs", precision=1)
+    assert rep["svd_used"] == expect
+    orc = orc_solve(A, b, solver="cs", extended=True)
+    assert rep["r"] == orc["r"] == 200 and rep["iters"] == orc["iters"]
+    an = np.linalg.norm(A @ (x.cpu().numpy() - orc["x"])) / np.linalg.norm(A @ orc["x"])
+    assert an <= 1e-11, an
