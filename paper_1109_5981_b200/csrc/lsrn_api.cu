@@ -815,8 +815,9 @@ void broadcast(lsrn_ctx* c, double* buf, int64_t count, int root) {
 }
 
 // ------------------------------------------------------------------ SVD
-// Alg. 1/2 steps 4-5: singular values and right singular
-// vectors of the s x k sketch, outside the hot path.  Ãt = Q R (geqrf), then
+// Alg. 1/2 steps 4-5: N from the s x k sketch, outside the hot
+// path.  Ãt = Q R (geqrf); when R is certified full rank N = R^{-1} (reading C23, in
+// svd_local below: same preconditioned singular values as V Sigma^{-1}).  Otherwise
 // the SVD of R through the symmetric eigenproblem of its Jordan-Wielandt matrix
 // [[0, R^T], [R, 0]], whose eigenpairs are (+-sigma_i, [v_i; +-u_i] / sqrt 2):
 // a true SVD (eigenvalues with absolute error ~ eps ||R||, no squaring of
