@@ -1123,6 +1123,199 @@ csr_rowdot_all_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restr
   }
 }
 
+// Dots of G rows, one value per lane on entry (lane's share of row j in d[j]),
+// reduced by a transposing butterfly: at offset 16 a lane keeps one half of its G
+// values and sends the other half, at 8 a quarter, ... (G - 1 + 5 - log2 G
+// shuffles instead of 5 G).  On exit d[0] of lane l is the sum of row l >> (5 - log2 G).
+template <int G>
+LSRN_DEV double transpose_reduce(double (&d)[G], int lane) {
+  int off = 16;
+#pragma unroll
+  for (int n = G; n > 1; n >>= 1, off >>= 1) {
+    const int half = n >> 1;
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = hi ? d[i] : d[i + half];
+      const double keep = hi ? d[i + half] : d[i];
+      d[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (; off > 0; off >>= 1) d[0] += __shfl_xor_sync(0xffffffffu, d[0], off);
+  return d[0];
+}
+
+// The single-pass long pass of csr_rowdot_all_kernel with a deeper load pipeline.
+// That kernel keeps one pair of rows (~0.5 KB on t4) in flight per warp, so 24 warps
+// per SM hold ~12 KB and the pass is DRAM-latency bound (1.57 TB/s on t4).  Here a
+// warp walks its rows in chunks of G * NB rows, each chunk in NB groups of G rows;
+// the first 32 entries of every row of a group (colind, val) are loaded into a ring
+// of NB register buffers NB - 1 groups ahead of the group being reduced, the row
+// pointers / u / acc of a chunk two chunks ahead.  A group is reduced in one
+// transposing butterfly (transpose_reduce), then its rows update the warp's shared
+// copy of w one row at a time in row order (rows may share columns), exactly as in
+// csr_rowdot_all_kernel.  Deterministic (fixed lane order, reduction tree and row
+// order); rows longer than 32 entries take the remainder from global memory.
+template <int G, int NB, int MINB, bool TS>
+__global__ void __launch_bounds__(THR, MINB)
+csr_rowdot_all_pipe_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                           const double* __restrict__ val, int64_t rows, int64_t k, const double* __restrict__ t,
+                           const double* __restrict__ coef, double sx, double* __restrict__ u,
+                           double* __restrict__ acc, double* __restrict__ npart, double* __restrict__ wpart,
+                           const int* __restrict__ done) {
+  constexpr int CHUNK = G * NB;
+  static_assert(CHUNK <= 32 && (G & (G - 1)) == 0 && G <= 32, "chunk of at most 32 rows, G a power of two");
+  constexpr int SH = (G == 1) ? 5 : (G == 2) ? 4 : (G == 4) ? 3 : (G == 8) ? 2 : (G == 16) ? 1 : 0;
+  extern __shared__ double wsh[];            // [THR / 32][k] (+ t[k] when TS)
+  __shared__ double sh[THR / 32];
+  if (done != nullptr && *done != 0) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* wd = wsh + (int64_t)wib * k;
+  for (int64_t c = lane; c < k; c += 32) wd[c] = 0.0;
+  // TS: t gathered from shared memory.  A row's ~21 random t[c] hit ~18 distinct 128-byte
+  // lines, i.e. ~18 L1 wavefronts per gather, against ~3-4 bank-conflict wavefronts from
+  // shared memory; the L1 / shared-memory data path is the pass's bottleneck on t4.
+  const double* tg = t;
+  if (TS) {
+    double* ts = wsh + (int64_t)(THR / 32) * k;
+    for (int64_t c = threadIdx.x; c < k; c += THR) ts[c] = t[c];
+    __syncthreads();
+    tg = ts;
+  } else {
+    __syncwarp();
+  }
+  const int64_t warp = ((int64_t)blockIdx.x * THR + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * THR) >> 5;
+  const double c1 = coef[0], c2 = coef[1] * sx;
+  const bool has_acc = acc != nullptr;
+  const double ca = has_acc ? coef[2] : 0.0;
+  const int64_t base = rowptr[0];
+  const int64_t per = (rows + nwarps - 1) / nwarps;
+  const int64_t r0 = min(rows, warp * per), r1 = min(rows, r0 + per);
+  const int64_t nchunks = (r1 - r0 + CHUNK - 1) / CHUNK;
+
+  // chunk descriptor: cb = the chunk's first entry (relative to the shard), lane l <
+  // CHUNK holds rp = row pointer of row l of the chunk minus cb (clamped to the chunk
+  // end; a chunk has at most 32 k entries since the columns of a row are distinct),
+  // lane CHUNK (or 0 when CHUNK = 32: end) the end; lng = some row > 32 entries
+  struct Chunk {
+    int64_t cb;
+    int rp, end;
+    bool lng;
+    double uo, ao;
+  };
+  auto load_chunk = [&](int64_t ci, Chunk& C) {
+    C.cb = 0;
+    C.rp = 0;
+    C.end = 0;
+    C.uo = 0.0;
+    C.ao = 0.0;
+    C.lng = false;
+    if (ci < nchunks) {
+      const int64_t rc = r0 + ci * CHUNK;
+      const int nr = (int)min((int64_t)CHUNK, r1 - rc);
+      const int64_t p = rowptr[rc + min(lane, nr)] - base;
+      const int64_t pe = rowptr[rc + nr] - base;
+      C.cb = __shfl_sync(0xffffffffu, p, 0);
+      C.rp = (int)(p - C.cb);
+      C.end = (int)(pe - C.cb);
+      if (lane < nr) {
+        C.uo = u[rc + lane];
+        if (has_acc) C.ao = acc[rc + lane];
+      }
+    }
+  };
+  auto rptr = [&](const Chunk& C, int i) -> int {   // i in [0, CHUNK]
+    const int v = __shfl_sync(0xffffffffu, C.rp, i & 31);
+    return i < CHUNK ? v : C.end;
+  };
+  struct Buf {
+    int c[G];          // column, -1 where the lane holds no entry of row j
+    double a[G];
+  };
+  auto load_group = [&](const Chunk& C, int q, Buf& B) {
+    const int32_t* ci_ = colind + C.cb;
+    const double* va_ = val + C.cb;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int e0 = rptr(C, q * G + j), e1 = rptr(C, q * G + j + 1);
+      B.c[j] = -1;
+      B.a[j] = 0.0;
+      if (e0 + lane < e1) {
+        B.c[j] = ci_[e0 + lane];
+        B.a[j] = ldg_stream1(va_ + e0 + lane);
+      }
+    }
+  };
+  double nrm = 0.0;
+  auto reduce_group = [&](const Chunk& C, int64_t ci, int q, const Buf& B, bool lng) {
+    double d[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) d[j] = (B.c[j] >= 0) ? B.a[j] * tg[B.c[j]] : 0.0;
+    if (lng) {                                                 // rows of more than 32 entries
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int64_t e0 = C.cb + rptr(C, q * G + j), e1 = C.cb + rptr(C, q * G + j + 1);
+        for (int64_t e = e0 + 32 + lane; e < e1; e += 32) d[j] = fma(val[e], tg[colind[e]], d[j]);
+      }
+    }
+    const double dot = transpose_reduce<G>(d, lane);
+    const int R = lane >> SH;                                  // this lane's row of the group
+    const int rin = q * G + R;                                 // row within the chunk
+    const int64_t row = r0 + ci * CHUNK + rin;
+    const double un = fma(c1, __shfl_sync(0xffffffffu, C.uo, rin), c2 * dot);
+    const double ao = __shfl_sync(0xffffffffu, C.ao, rin);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const double uj = __shfl_sync(0xffffffffu, un, j << SH);
+      if (B.c[j] >= 0) wd[B.c[j]] = fma(B.a[j], uj, wd[B.c[j]]);
+      if (lng) {
+        const int64_t e0 = C.cb + rptr(C, q * G + j), e1 = C.cb + rptr(C, q * G + j + 1);
+        for (int64_t e = e0 + 32 + lane; e < e1; e += 32) wd[colind[e]] = fma(val[e], uj, wd[colind[e]]);
+      }
+      __syncwarp();                                            // the next row may share columns
+    }
+    if ((lane & ((1 << SH) - 1)) == 0 && row < r1) {
+      u[row] = un;
+      if (has_acc) acc[row] = fma(ca, un, ao);
+      nrm = fma(un, un, nrm);
+    }
+  };
+
+  Chunk C0, C1, C2;
+  Buf B[NB];
+  load_chunk(0, C0);
+  load_chunk(1, C1);
+#pragma unroll
+  for (int q = 0; q < NB - 1; ++q) load_group(C0, q, B[q]);
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    load_chunk(ci + 2, C2);
+    // rows of more than 32 entries in this chunk (warp-uniform)
+    const int nxt = rptr(C0, min(lane + 1, CHUNK));            // every lane shuffles
+    const bool lng = __any_sync(0xffffffffu, lane < CHUNK && nxt - C0.rp > 32);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      // group q + NB - 1 of this chunk, or group q - 1 of the next, into the buffer freed last
+      if (q == 0)
+        load_group(C0, NB - 1, B[NB - 1]);
+      else
+        load_group(C1, q - 1, B[q - 1]);
+      reduce_group(C0, ci, q, B[q], lng);
+    }
+    C0 = C1;
+    C1 = C2;
+  }
+  const double b = block_sum(nrm, sh);     // contains __syncthreads: every warp's wd complete
+  if (threadIdx.x == 0) npart[blockIdx.x] = b;
+  for (int64_t c = threadIdx.x; c < k; c += THR) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < THR / 32; ++w) v += wsh[(int64_t)w * k + c];
+    wpart[(int64_t)blockIdx.x * k + c] = sx * v;
+  }
+}
+
 // w_c = sum_{(j,a) in col c} a u_j (light columns: warp per column, lanes stride
 // the CSC column; heavy columns: the row pass's block partials);
 // Tikhonov block and ||u||^2 as in colreduce_kernel: out = [w ; ||u||^2 + ||zI||^2].
@@ -1189,18 +1382,57 @@ int csr_rowdot_hl_blocks(int nsm, int ND) {
   return nsm * std::min(per_sm, 8);
 }
 int64_t csr_rowdot_all_max_k() { return 2048; }      // 8 warps x k doubles of shared memory (128 KB)
-// CTAs of 8 warps, as many per SM as the per-warp w copies (8 k doubles) allow
-int csr_rowdot_all_blocks(int nsm, int64_t k) {
-  const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (200 * 1024) / (64 * k)));
+// Variants of the single pass (csr_rowdot option): 0 csr_rowdot_all_kernel (one pair of
+// rows in flight per warp), 4.. the pipelined kernel with (G, NB) below.
+namespace {
+struct AllVariant {
+  int G, NB, minb;
+};
+constexpr AllVariant kAllVariants[] = {{8, 4, 1}, {4, 4, 2}, {8, 2, 2}, {4, 8, 1}, {4, 2, 3}, {2, 4, 3},
+                                       {8, 2, 2}, {4, 4, 2}, {4, 2, 3}, {8, 4, 1}};
+constexpr int kMaxVariant = 13;
+bool all_ts(int v) { return v >= 10; }     // t staged in shared memory
+const void* all_kernel(int v) {
+  switch (v) {
+    case 4: return (const void*)csr_rowdot_all_pipe_kernel<8, 4, 1, false>;
+    case 5: return (const void*)csr_rowdot_all_pipe_kernel<4, 4, 2, false>;
+    case 6: return (const void*)csr_rowdot_all_pipe_kernel<8, 2, 2, false>;
+    case 7: return (const void*)csr_rowdot_all_pipe_kernel<4, 8, 1, false>;
+    case 8: return (const void*)csr_rowdot_all_pipe_kernel<4, 2, 3, false>;
+    case 9: return (const void*)csr_rowdot_all_pipe_kernel<2, 4, 3, false>;
+    case 10: return (const void*)csr_rowdot_all_pipe_kernel<8, 2, 2, true>;
+    case 11: return (const void*)csr_rowdot_all_pipe_kernel<4, 4, 2, true>;
+    case 12: return (const void*)csr_rowdot_all_pipe_kernel<4, 2, 3, true>;
+    case 13: return (const void*)csr_rowdot_all_pipe_kernel<8, 4, 1, true>;
+    default: return (const void*)csr_rowdot_all_kernel;
+  }
+}
+}  // namespace
+int csr_rowdot_all_default_variant() { return 10; }
+// CTAs of 8 warps, as many per SM as the per-warp w copies (8 k doubles) and the
+// variant's registers allow
+int csr_rowdot_all_blocks(int nsm, int64_t k, int variant) {
+  const int64_t per_cta = 8 * k * (THR / 32 + (all_ts(variant) ? 1 : 0));
+  int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / per_cta));
+  if (variant >= 4 && variant <= kMaxVariant) per_sm = std::min<int64_t>(per_sm, kAllVariants[variant - 4].minb);
   return (int)(nsm * per_sm);
 }
+int csr_rowdot_all_blocks_max(int nsm, int64_t k) {
+  int b = 0;
+  for (int v = 0; v <= kMaxVariant; ++v) b = std::max(b, csr_rowdot_all_blocks(nsm, k, v));
+  return b;
+}
 
-cudaError_t launch_csr_rowdot_all(const CsrRowdotArgs& a, int64_t k, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (size_t)(THR / 32) * (size_t)k;
-  cudaError_t e = cudaFuncSetAttribute(csr_rowdot_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t launch_csr_rowdot_all(const CsrRowdotArgs& a, int64_t k, int variant, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)(THR / 32 + (all_ts(variant) ? 1 : 0)) * (size_t)k;
+  const void* fn = all_kernel(variant);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  csr_rowdot_all_kernel<<<(unsigned)a.nblocks, THR, smem, st>>>(a.rowptr, a.colind, a.val, a.rows, k, a.t, a.coef,
-                                                                 a.sx, a.u, a.acc, a.npart, a.wpart, a.done);
+  void* args[] = {(void*)&a.rowptr, (void*)&a.colind, (void*)&a.val, (void*)&a.rows, (void*)&k, (void*)&a.t,
+                  (void*)&a.coef, (void*)&a.sx, (void*)&a.u, (void*)&a.acc, (void*)&a.npart, (void*)&a.wpart,
+                  (void*)&a.done};
+  e = cudaLaunchKernel(fn, dim3((unsigned)a.nblocks), dim3(THR), args, smem, st);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 int csr_colgather_blocks(int64_t k) { return (int)((k * 32 + THR - 1) / THR); }

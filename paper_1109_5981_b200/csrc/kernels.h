@@ -35,6 +35,7 @@ struct Overrides {
                               // 3 the two-kernel form (row dots + CSC gather) also for k <= 2048
   int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch, 2 stored G
   int csr_heavy_fma = -1;     // stored-G heavy block: 1 = FP64-FMA kernel instead of DMMA
+  int csr_all = -1;           // k <= 2048 single-pass kernel: 0 one pair of rows in flight, 4..7 pipelined
 };
 const Overrides& ovr();
 struct OverrideScope {
@@ -297,8 +298,10 @@ cudaError_t launch_csr_rowdot(const CsrRowdotArgs& a, cudaStream_t st);
 cudaError_t launch_csr_rowdot_hl(const CsrRowdotArgs& a, cudaStream_t st);
 // single-pass variant for k <= csr_rowdot_all_max_k(): wpart[nblocks][k], then colreduce
 int64_t csr_rowdot_all_max_k();
-int csr_rowdot_all_blocks(int nsm, int64_t k);
-cudaError_t launch_csr_rowdot_all(const CsrRowdotArgs& a, int64_t k, cudaStream_t st);
+int csr_rowdot_all_default_variant();
+int csr_rowdot_all_blocks(int nsm, int64_t k, int variant);
+int csr_rowdot_all_blocks_max(int nsm, int64_t k);   // over every variant (workspace)
+cudaError_t launch_csr_rowdot_all(const CsrRowdotArgs& a, int64_t k, int variant, cudaStream_t st);
 
 struct CsrGatherArgs {
   const int64_t* colptr;

@@ -445,9 +445,9 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
   w.nsplit = nsplit;
   w.rows_per_split = std::max<int64_t>(1, (d.cnt + nsplit - 1) / nsplit);
   w.part = ar.take<double>((size_t)nsplit * d.s * kMaxHeavy);
-  w.npart = ar.take<double>((size_t)std::max(csr_rowdot_blocks(c->nsm), csr_rowdot_all_blocks(c->nsm, d.k)));
+  w.npart = ar.take<double>((size_t)std::max(csr_rowdot_blocks(c->nsm), csr_rowdot_all_blocks_max(c->nsm, d.k)));
   const size_t wp_heavy = (size_t)csr_rowdot_blocks(c->nsm) * kMaxHeavy;
-  const size_t wp_all = d.k <= csr_rowdot_all_max_k() ? (size_t)csr_rowdot_all_blocks(c->nsm, d.k) * d.k : 0;
+  const size_t wp_all = d.k <= csr_rowdot_all_max_k() ? (size_t)csr_rowdot_all_blocks_max(c->nsm, d.k) * d.k : 0;
   w.wpart = ar.take<double>(std::max(wp_heavy, wp_all));
   // Sketch of the CSR shard: by default the stored-G kernels (G generated once per chunk
   // of rows, <= 8 GB, and read by the heavy and light kernels): c4 7.33 -> 4.37 s, t4
@@ -1223,8 +1223,9 @@ struct Pass {
     a.ND = cw->ND;
     if (d.k <= csr_rowdot_all_max_k() && ovr().csr_rowdot != 3) {
       // single pass: w for every column accumulated in shared memory, then the fixed-order block sum
-      a.nblocks = csr_rowdot_all_blocks(c->nsm, d.k);
-      LSRN_CUDA(launch_csr_rowdot_all(a, d.k, st));
+      const int var = ovr().csr_all >= 0 ? ovr().csr_all : csr_rowdot_all_default_variant();
+      a.nblocks = csr_rowdot_all_blocks(c->nsm, d.k, var);
+      LSRN_CUDA(launch_csr_rowdot_all(a, d.k, var, st));
       ColReduceArgs r{};
       r.wpart = cw->wpart;
       r.npart = cw->npart;
@@ -1522,6 +1523,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 3)) return bad(); o.csr_rowdot = (int)value; break;
     case LSRN_OPT_CSR_SKETCH: if (!in(-1, 2)) return bad(); o.csr_sketch = (int)value; break;
     case LSRN_OPT_CSR_HEAVY_FMA: if (!in(-1, 1)) return bad(); o.csr_heavy_fma = (int)value; break;
+    case LSRN_OPT_CSR_ALL: if (!in(-1, 13) || value == 1 || value == 2 || value == 3) return bad(); o.csr_all = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
   }
   return LSRN_OK;
@@ -1952,7 +1954,7 @@ lsrn_status solve_impl(lsrn_ctx* c, const lsrn_matrix* A_in, const double* b_in,
                             (const void*)PL.cw.lcol, (const void*)PL.cw.lval})
         kp(q);
     ki(A.ld), ki(A.nnz), ki(r), ki(iters_graph), ki(passes), ki(solver), ki(o->mode), ki(c->profile ? 1 : 0);
-    ki((int64_t)c->pass_ev.size()), ki(PL.csr ? 1 : 0), ki(ovr().csr_rowdot), ki(P.two_sync ? 1 : 0);
+    ki((int64_t)c->pass_ev.size()), ki(PL.csr ? 1 : 0), ki(ovr().csr_rowdot), ki(ovr().csr_all), ki(P.two_sync ? 1 : 0);
     if (PL.csr) ki(PL.cw.nd), ki(PL.cw.ND), ki(PL.cw.ldd), ki(PL.cw.nnz_light);
     ki(d.tall ? 1 : 0), ki(d.m), ki(d.n), ki(d.L), ki(d.k), ki(d.s), ki(d.cnt), ki(d.lo), kd(d.sx), kd(d.si);
     ki(d.has_I ? 1 : 0), ki(d.Lz), ki(ext ? 1 : 0);

@@ -251,14 +251,15 @@ def _ragged_csr(m, n, seed):
 
 
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
-@pytest.mark.parametrize("rowdot", [-1, 3])
-def test_csr_single_pass_staged_and_direct_chunks(ctx, solver, rowdot):
+@pytest.mark.parametrize("rowdot,variant", [(-1, -1), (3, -1), (-1, 0)] + [(-1, v) for v in range(4, 14)])
+def test_csr_single_pass_staged_and_direct_chunks(ctx, solver, rowdot, variant):
     """k <= 2048 long pass on ragged rows (empty rows, rows longer than a warp, a chunk of
-    long rows): the single-pass kernel (default) and the two-kernel CSC-gather form
-    (LSRN_OPT_CSR_ROWDOT = 3) against the oracle."""
+    long rows): the single-pass kernels (LSRN_OPT_CSR_ALL: 0 one pair of rows in flight,
+    4-7 the pipelined groups) and the two-kernel CSC-gather form (LSRN_OPT_CSR_ROWDOT = 3)
+    against the oracle."""
     A = _ragged_csr(5000, 300, seed=8)
     b = np.random.default_rng(9).standard_normal(A.shape[0])
-    with ctx.options(csr_rowdot=rowdot):
+    with ctx.options(csr_rowdot=rowdot, csr_all=variant):
         x, rep = ctx.solve(_gpu_csr(A), torch.from_numpy(b).cuda(), A.shape[0], A.shape[1], solver=solver)
     orc = orc_solve(A, b, solver=solver)
     assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
@@ -269,3 +270,21 @@ def test_csr_single_pass_staged_and_direct_chunks(ctx, solver, rowdot):
     assert rel <= max(1e-9, 20 * kappa * U), rel
     an = np.linalg.norm(A @ (xg - orc["x"])) / np.linalg.norm(A @ orc["x"])
     assert an <= 1e-11, an
+
+
+@pytest.mark.parametrize("variant", [0] + list(range(4, 14)))
+@pytest.mark.parametrize("lam", [0.0, 0.05])
+def test_csr_single_pass_variants_wide_ragged(ctx, variant, lam):
+    """Wide ragged CSR (X = A^T with empty, short and > 32-entry rows; CS keeps the
+    acc_j += ca u_j update of the wide form in the same pass) for every single-pass
+    variant: iteration count, rank and x against the oracle."""
+    AT = _ragged_csr(4100, 260, seed=17)
+    A = AT.T.tocsr()
+    m, n = AT.shape[1], AT.shape[0]
+    b = np.random.default_rng(3).standard_normal(m)
+    with ctx.options(csr_all=variant):
+        x, rep = ctx.solve(_gpu_csr(AT), torch.from_numpy(b).cuda(), m, n, solver="cs", lam=lam)
+    orc = orc_solve(A, b, solver="cs", lam=lam)
+    assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
+    rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
+    assert rel <= 1e-9, rel

@@ -1,0 +1,42 @@
+"""CSR single-pass long pass (k <= 2048) per LSRN_OPT_CSR_ALL variant on a full config
+(default t4): average long-pass time (library CUDA events), algorithmic bytes, GB/s,
+and x of each variant against the first one.  argv: config [variants...]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.getcwd())
+import torch  # noqa: E402
+
+from paper_1109_5981_b200 import lsrn  # noqa: E402
+from synth.generate import make_problem  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "t4"
+variants = sys.argv[2:] or ["0", "4", "5", "6", "7"]   # "r3": the two-kernel form (csr_rowdot = 3)
+p = make_problem(cfg, device="cuda")
+X = lsrn.Csr(p.rowptr, p.colind, p.val)
+ctx = lsrn.Context()
+ctx.set_profiling(True)
+xs = {}
+for v in variants:
+    if v.startswith("r"):
+        ctx.set_option("csr_all", -1)
+        ctx.set_option("csr_rowdot", int(v[1:]))
+    else:
+        ctx.set_option("csr_rowdot", -1)
+        ctx.set_option("csr_all", int(v))
+    best = None
+    for _ in range(3):
+        x, rep = ctx.solve(X, p.b, p.m, p.n, solver="cs")
+        torch.cuda.synchronize()
+        st = ctx.stats()
+        if best is None or st["long_pass_ms"] < best[0]:
+            best = (st["long_pass_ms"], st["long_pass_bytes"], rep["t_iter"], rep["iters"])
+    xs[v] = x.clone()
+    lp, by, ti, it = best
+    print(json.dumps({"cfg": cfg, "csr_all": v, "long_pass_ms": lp, "bytes": by, "gbs": by / lp / 1e6,
+                      "t_iter": ti, "iters": it}), flush=True)
+ks = list(xs)
+for v in ks[1:]:
+    print(json.dumps({"x_reldiff": [ks[0], v],
+                      "value": float(torch.linalg.norm(xs[v] - xs[ks[0]]) / torch.linalg.norm(xs[ks[0]]))}))
