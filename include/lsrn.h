@@ -235,11 +235,7 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *   LSRN_OPT_CSR_ALL        CSR single pass (k <= 2048): 0 one pair of rows in flight per warp;
  *                           4-9 load pipelines of (rows per group G, groups NB; NB - 1 in
  *                           flight) = (8,4) (4,4) (8,2) (4,8) (4,2) (2,4); 10-13 the same with
- *                           t staged in shared memory: (8,2) (default) (4,4) (4,2) (8,4)
- *   LSRN_OPT_CSR_GEN_OVERLAP stored-G CSR sketch: 0 = generate every chunk's G on the
- *                           context stream with one G block; default: two blocks, chunk
- *                           J + 1 generated on an internal stream while chunk J is read,
- *                           by 2 (N > 0: N) generator CTAs per SM */
+ *                           t staged in shared memory: (8,2) (default) (4,4) (4,2) (8,4) */
 enum {
   LSRN_OPT_PROFILING = 1,
   LSRN_OPT_SVD = 2,
@@ -267,8 +263,7 @@ enum {
   LSRN_OPT_CSR_ROWDOT = 120,
   LSRN_OPT_CSR_SKETCH = 121,
   LSRN_OPT_CSR_HEAVY_FMA = 123,
-  LSRN_OPT_CSR_ALL = 124,
-  LSRN_OPT_CSR_GEN_OVERLAP = 125
+  LSRN_OPT_CSR_ALL = 124
 };
 enum { LSRN_SVD_AUTO = 0, LSRN_SVD_JW = 1, LSRN_SVD_GESVD = 2, LSRN_SVD_POLAR = 3, LSRN_SVD_QR = 4 };
 lsrn_status lsrn_ctx_set_option(lsrn_ctx* ctx, int option, int64_t value);

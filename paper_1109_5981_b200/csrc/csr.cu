@@ -1544,58 +1544,28 @@ cudaError_t launch_csr_sketch_g(const CsrSketchGArgs& a, cudaStream_t st, int ns
   const unsigned row_blocks = (unsigned)((a.s + THR - 1) / THR);
   cudaError_t e = launch_csr_chunkptr(a.colptr, a.rowidx, a.colmap, a.k, nch, a.cp, st, a.g_rows);
   if (e != cudaSuccess) return e;
-  // Overlap (G2 set): the generator (Philox + Box-Muller, FP64/ALU-bound) of chunk J + 1
-  // runs on gen_st into the other buffer while chunk J's heavy (DMMA) and light
-  // (L2-gather-bound) kernels run on st; a buffer is regenerated only after the light
-  // kernel that last read it (ev free), and read only after its generation (ev ready).
-  const bool ov = a.G2 != nullptr && a.gen_st != nullptr && nch > 1;
-  cudaStream_t gs = ov ? a.gen_st : st;
-  if (ov) {
-    if ((e = cudaEventRecord(a.ev[0], st)) != cudaSuccess) return e;          // fork: after the chunk pointers
-    if ((e = cudaStreamWaitEvent(gs, a.ev[0], 0)) != cudaSuccess) return e;
-  }
-  auto gen = [&](int64_t J) -> cudaError_t {
-    const int64_t r0 = J * a.g_rows, nr = std::min(a.g_rows, a.rows - r0);
-    const int64_t pairs = nr * (a.s2 / 2);
-    double* Gb = (ov && (J & 1)) ? a.G2 : a.G;
-    cudaError_t e2;
-    if (ov && J >= 2 && (e2 = cudaStreamWaitEvent(gs, a.ev[3 + (J & 1)], 0)) != cudaSuccess) return e2;
-    // overlapped: a few CTAs per SM, so that the generator runs beside the chunk's
-    // heavy / light kernels instead of taking every SM first (a full grid of 16 per SM
-    // was dispatched ahead of them and the two serialised: t4 207 -> 201 ms only)
-    const int64_t cap = (int64_t)nsm * (ov ? a.gen_ctas_per_sm : 16);
-    csr_gen_g_kernel<<<grid_cap(pairs, 256, cap), 256, 0, gs>>>(Gb, a.s2, nr, a.lo + r0, a.seed);
-    if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
-    if (ov && (e2 = cudaEventRecord(a.ev[1 + (J & 1)], gs)) != cudaSuccess) return e2;
-    return cudaSuccess;
-  };
-  if ((e = gen(0)) != cudaSuccess) return e;
   for (int64_t J = 0; J < nch; ++J) {
     const int64_t r0 = J * a.g_rows, nr = std::min(a.g_rows, a.rows - r0);
-    const double* Gb = (ov && (J & 1)) ? a.G2 : a.G;
-    if (ov) {
-      if (J + 1 < nch && (e = gen(J + 1)) != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(st, a.ev[1 + (J & 1)], 0)) != cudaSuccess) return e;
-    }
+    const int64_t pairs = nr * (a.s2 / 2);
+    csr_gen_g_kernel<<<grid_cap(pairs, 256, (int64_t)nsm * 16), 256, 0, st>>>(a.G, a.s2, nr, a.lo + r0, a.seed);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (a.nd > 0) {
       const int64_t rps = (nr + a.nsplit - 1) / a.nsplit;
       const double* D = a.D + r0 * a.ldd;
       CsrSketchGArgs b = a;
       b.D = D;
       switch (a.ND) {
-        case 16: heavy_g_t<16>(b, Gb, nr, rps, a.nsplit, J > 0, st); break;
-        case 32: heavy_g_t<32>(b, Gb, nr, rps, a.nsplit, J > 0, st); break;
-        default: heavy_g_t<64>(b, Gb, nr, rps, a.nsplit, J > 0, st); break;
+        case 16: heavy_g_t<16>(b, a.G, nr, rps, a.nsplit, J > 0, st); break;
+        case 32: heavy_g_t<32>(b, a.G, nr, rps, a.nsplit, J > 0, st); break;
+        default: heavy_g_t<64>(b, a.G, nr, rps, a.nsplit, J > 0, st); break;
       }
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     const int cpc = 16;      // a chunk holds ~g_rows nnz / k entries per column (c4: ~25)
     dim3 g2((unsigned)((a.k + cpc - 1) / cpc), row_blocks);
-    csr_sketch_light_g_kernel<<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, J, a.k, a.s, a.s2, Gb,
+    csr_sketch_light_g_kernel<<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, J, a.k, a.s, a.s2, a.G,
                                                   r0, cpc, a.Pt, J > 0);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (ov && (e = cudaEventRecord(a.ev[3 + (J & 1)], st)) != cudaSuccess) return e;
-    if (!ov && J + 1 < nch && (e = gen(J + 1)) != cudaSuccess) return e;
   }
   if (a.nd > 0) {
     csr_heavy_finish_kernel<<<grid_cap(a.s * a.nd, 256, (int64_t)nsm * 16), 256, 0, st>>>(

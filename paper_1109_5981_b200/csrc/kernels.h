@@ -35,9 +35,7 @@ struct Overrides {
                               // 3 the two-kernel form (row dots + CSC gather) also for k <= 2048
   int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch, 2 stored G
   int csr_heavy_fma = -1;     // stored-G heavy block: 1 = FP64-FMA kernel instead of DMMA
-  int csr_all = -1;           // k <= 2048 single-pass kernel: 0 one pair of rows in flight, 4..13 pipelined
-  int csr_gen_overlap = -1;   // stored-G CSR sketch: 0 = generate each chunk's G on the main stream (no second
-                              // buffer); N > 0 = overlapped with N generator CTAs per SM (default 2)
+  int csr_all = -1;           // k <= 2048 single-pass kernel: 0 one pair of rows in flight, 4..7 pipelined
 };
 const Overrides& ovr();
 struct OverrideScope {
@@ -266,13 +264,6 @@ struct CsrSketchGArgs {
   double* G;               // [g_rows][s2]
   double* Pt;              // [k][s]
   double* At;
-  // overlapped generation (csr_sketch_g_overlap): G of chunk J + 1 generated into the
-  // second buffer G2 on gen_st while chunk J is consumed on the main stream; ev:
-  // fork, ready[2], free[2].  G2 == nullptr: one buffer, everything on the main stream.
-  double* G2;
-  cudaStream_t gen_st;
-  cudaEvent_t ev[5];
-  int gen_ctas_per_sm;     // generator grid when overlapped
 };
 int64_t csr_g_s2(int64_t s);
 cudaError_t launch_csr_sketch_g(const CsrSketchGArgs& a, cudaStream_t st, int nsm);

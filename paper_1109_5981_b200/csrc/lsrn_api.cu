@@ -114,9 +114,6 @@ struct lsrn_ctx {
   // host-IO streaming of A: copy stream + per-chunk events
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t chunk_ev[16] = {};
-  // stored-G CSR sketch: generator stream + fork / ready[2] / free[2] events
-  cudaStream_t gen_stream = nullptr;
-  cudaEvent_t gen_ev[5] = {};
   cudaEvent_t io_ev = nullptr;
   // raw sketch cache (λ-path reuse): key of the sketch held in the workspace
   bool sketch_cached = false;
@@ -410,7 +407,6 @@ struct CsrWs {
   bool gstore = false;
   int64_t g_rows = 0;
   double* G = nullptr;
-  double* G2 = nullptr;                // second G block: generation of chunk J + 1 overlaps chunk J
   int32_t* cpg = nullptr;
   double* Pt = nullptr;
   int32_t* lcol;
@@ -471,8 +467,6 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
     w.g_rows = std::max<int64_t>(1, std::min<int64_t>(d.cnt, (int64_t)(budget / (8.0 * (double)s2))));
     const int64_t nchg = (d.cnt + w.g_rows - 1) / w.g_rows;
     w.G = ar.take<double>((size_t)w.g_rows * s2);
-    // second block for the overlapped generation (profiles/r02_csr_gen_overlap.jsonl)
-    if (nchg > 1 && ovr().csr_gen_overlap != 0) w.G2 = ar.take<double>((size_t)w.g_rows * s2);
     w.cpg = ar.take<int32_t>((size_t)(nchg + 1) * d.k);
     w.Pt = ar.take<double>((size_t)d.k * d.s);
   }
@@ -589,10 +583,6 @@ void run_sketch_csr(lsrn_ctx* c, const Dims& d, uint64_t seed, CsrWs& w, double*
     g.G = w.G;
     g.Pt = w.Pt;
     g.At = At;
-    g.G2 = w.G2;
-    g.gen_st = c->gen_stream;
-    g.gen_ctas_per_sm = ovr().csr_gen_overlap > 0 ? ovr().csr_gen_overlap : 2;
-    for (int i = 0; i < 5; ++i) g.ev[i] = c->gen_ev[i];
     LSRN_CUDA(launch_csr_sketch_g(g, c->stream, c->nsm));
     const int64_t nchg = (d.cnt + w.g_rows - 1) / w.g_rows;
     c->launches += 1 + (int)nchg * (2 + (w.nd > 0 ? 1 : 0)) + (w.nd > 0 ? 1 : 0) + 1;
@@ -1443,8 +1433,6 @@ lsrn_status lsrn_ctx_create(lsrn_ctx** out, void* stream, int nranks, int rank, 
     LSRN_SOLVER(cusolverDnCreateParams(&c->params));
     for (auto& e : c->ev) LSRN_CUDA(cudaEventCreate(&e));
     LSRN_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    LSRN_CUDA(cudaStreamCreateWithFlags(&c->gen_stream, cudaStreamNonBlocking));
-    for (auto& e : c->gen_ev) LSRN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->chunk_ev) LSRN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     LSRN_CUDA(cudaEventCreateWithFlags(&c->io_ev, cudaEventDisableTiming));
     // nranks = 1 with an id: a one-rank communicator, so that the NCCL path (the
@@ -1480,9 +1468,6 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->io_ev) cudaEventDestroy(c->io_ev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-  for (auto& e : c->gen_ev)
-    if (e) cudaEventDestroy(e);
-  if (c->gen_stream) cudaStreamDestroy(c->gen_stream);
   for (auto& e : c->join_ev)
     if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) {
@@ -1538,7 +1523,6 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 3)) return bad(); o.csr_rowdot = (int)value; break;
     case LSRN_OPT_CSR_SKETCH: if (!in(-1, 2)) return bad(); o.csr_sketch = (int)value; break;
     case LSRN_OPT_CSR_HEAVY_FMA: if (!in(-1, 1)) return bad(); o.csr_heavy_fma = (int)value; break;
-    case LSRN_OPT_CSR_GEN_OVERLAP: if (!in(-1, 16)) return bad(); o.csr_gen_overlap = (int)value; break;
     case LSRN_OPT_CSR_ALL: if (!in(-1, 13) || value == 1 || value == 2 || value == 3) return bad(); o.csr_all = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
   }

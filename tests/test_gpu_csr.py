@@ -288,22 +288,3 @@ def test_csr_single_pass_variants_wide_ragged(ctx, variant, lam):
     assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
     rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
     assert rel <= 1e-9, rel
-
-
-@pytest.mark.parametrize("dense_cols", [0, 7])
-def test_csr_stored_g_overlap_is_bitwise_serial(ctx, dense_cols):
-    """Stored-G CSR sketch with a 1 MB G budget (many chunks): the overlapped generation
-    (chunk J + 1's G on the internal stream into the second block, the default) gives the
-    sketch of the serial one-block schedule (LSRN_OPT_CSR_GEN_OVERLAP = 0) bit for bit --
-    the same kernels read the same G values in the same chunk order -- and matches the
-    oracle."""
-    A = _random_csr(3000, 150, 5, dense_cols, 3.0, 4, seed=41)
-    X = _gpu_csr(A)
-    with ctx.options(sketch_g=1):
-        a1 = ctx.sketch(X, 3000, 150).cpu().numpy()
-        with ctx.options(csr_gen_overlap=0):
-            a0 = ctx.sketch(X, 3000, 150).cpu().numpy()
-    assert np.array_equal(a0, a1)
-    p = orc_plan(3000, 150, 2.0, 0.0)
-    ref = orc_sketch(A, p["s"], 5981, p["sigma_x"], p["sigma_i"])
-    assert _relfro(a1, ref) <= 1e-12
