@@ -235,7 +235,9 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *   LSRN_OPT_CSR_ALL        CSR single pass (k <= 2048): 0 one pair of rows in flight per warp;
  *                           4-9 load pipelines of (rows per group G, groups NB; NB - 1 in
  *                           flight) = (8,4) (4,4) (8,2) (4,8) (4,2) (2,4); 10-13 the same with
- *                           t staged in shared memory: (8,2) (default) (4,4) (4,2) (8,4) */
+ *                           t staged in shared memory: (8,2) (default) (4,4) (4,2) (8,4)
+ *   LSRN_OPT_CSR_LIGHT      stored-G light sketch kernel: 10 * (columns per CTA, 1-64) +
+ *                           (gathers in flight per thread: 2, 4 or 8) */
 enum {
   LSRN_OPT_PROFILING = 1,
   LSRN_OPT_SVD = 2,
@@ -263,7 +265,8 @@ enum {
   LSRN_OPT_CSR_ROWDOT = 120,
   LSRN_OPT_CSR_SKETCH = 121,
   LSRN_OPT_CSR_HEAVY_FMA = 123,
-  LSRN_OPT_CSR_ALL = 124
+  LSRN_OPT_CSR_ALL = 124,
+  LSRN_OPT_CSR_LIGHT = 126
 };
 enum { LSRN_SVD_AUTO = 0, LSRN_SVD_JW = 1, LSRN_SVD_GESVD = 2, LSRN_SVD_POLAR = 3, LSRN_SVD_QR = 4 };
 lsrn_status lsrn_ctx_set_option(lsrn_ctx* ctx, int option, int64_t value);

@@ -631,6 +631,7 @@ csr_sketch_heavy_mma_kernel(const double* __restrict__ D, int ldd, int nd, int64
 
 // Light part from stored G, chunk J (rows [row0, row0 + rows) of the shard):
 // Pt[c][i] (+)= sum over the light entries (j, a) of column c in the chunk of a G[j - row0][i].
+template <int UNR>
 __global__ void __launch_bounds__(THR)
 csr_sketch_light_g_kernel(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
                           const double* __restrict__ cval, const int* __restrict__ colmap,
@@ -658,13 +659,12 @@ csr_sketch_light_g_kernel(const int64_t* __restrict__ colptr, const int32_t* __r
       __syncthreads();
       if (i < s) {
         int e = 0;
-        for (; e + 4 <= ne; e += 4) {          // four gathers in flight
-          const double g0 = G[(int64_t)js[e] * s2 + i], g1 = G[(int64_t)js[e + 1] * s2 + i];
-          const double g2 = G[(int64_t)js[e + 2] * s2 + i], g3 = G[(int64_t)js[e + 3] * s2 + i];
-          acc = fma(g0, as[e], acc);
-          acc = fma(g1, as[e + 1], acc);
-          acc = fma(g2, as[e + 2], acc);
-          acc = fma(g3, as[e + 3], acc);
+        for (; e + UNR <= ne; e += UNR) {      // UNR gathers in flight
+          double g[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) g[u] = G[(int64_t)js[e + u] * s2 + i];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) acc = fma(g[u], as[e + u], acc);
         }
         for (; e < ne; ++e) acc = fma(G[(int64_t)js[e] * s2 + i], as[e], acc);
       }
@@ -1561,10 +1561,23 @@ cudaError_t launch_csr_sketch_g(const CsrSketchGArgs& a, cudaStream_t st, int ns
       }
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    const int cpc = 16;      // a chunk holds ~g_rows nnz / k entries per column (c4: ~25)
+    // columns per CTA and gathers in flight per thread (csr_light: 10 * cpc + unroll).
+    // Round 1 used 16 columns and 4 gathers: t4's grid of 64 x 8 CTAs held 27 warps per SM
+    // and the gathers were latency-bound (ncu: 22 cycles per issued instruction, L2 41 %
+    // busy).  One column per CTA for k <= 2048 (t4: 8192 CTAs), four above (c4), eight
+    // gathers in flight: t4 207 -> 147 ms, c4 1.98 -> 1.82 s (profiles/r02_csr_light*.jsonl).
+    const int cpc = ovr().csr_light > 0 ? ovr().csr_light / 10 : (a.k <= 2048 ? 1 : 4);
+    const int unr = ovr().csr_light > 0 ? ovr().csr_light % 10 : 8;
     dim3 g2((unsigned)((a.k + cpc - 1) / cpc), row_blocks);
-    csr_sketch_light_g_kernel<<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, J, a.k, a.s, a.s2, a.G,
-                                                  r0, cpc, a.Pt, J > 0);
+    if (unr == 8)
+      csr_sketch_light_g_kernel<8><<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, J, a.k, a.s, a.s2,
+                                                       a.G, r0, cpc, a.Pt, J > 0);
+    else if (unr == 2)
+      csr_sketch_light_g_kernel<2><<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, J, a.k, a.s, a.s2,
+                                                       a.G, r0, cpc, a.Pt, J > 0);
+    else
+      csr_sketch_light_g_kernel<4><<<g2, THR, 0, st>>>(a.colptr, a.rowidx, a.cval, a.colmap, a.cp, J, a.k, a.s, a.s2,
+                                                       a.G, r0, cpc, a.Pt, J > 0);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (a.nd > 0) {

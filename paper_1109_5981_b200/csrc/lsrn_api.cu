@@ -463,7 +463,21 @@ CsrWs plan_csr(lsrn_ctx* c, const Dims& d, const lsrn_matrix* A, Arena& ar) {
     w.rows_per_split = std::max<int64_t>(1, (d.cnt + w.nsplit - 1) / w.nsplit);
     w.part = ar.take<double>((size_t)w.nsplit * d.s * kMaxHeavy);
     const int64_t s2 = csr_g_s2(d.s);
-    const double budget = ovr().sketch_g > 0 ? (double)ovr().sketch_g * 1048576.0 : 8.0e9;   // as the dense G
+    // G rows per chunk.  Default: as few rows as keep ~256 nonzeros per column and chunk
+    // (the light kernel's staging batch; estimated as nnz / k), but a G block of at least
+    // 256 MB and at most 8 GB (as the dense G).  Small blocks stay L2-resident between
+    // generation and the light gathers: t4 (82000 nonzeros per column) -> 256 MB, 245
+    // chunks: 147 -> 123 ms; c4 (7000 per column) keeps 8 GB, smaller blocks are slower
+    // there (launches, short heavy GEMMs: 2 GB 2.78 s vs 1.82 s; profiles/r02_csr_light2_*.jsonl).
+    double budget = 8.0e9;
+    if (ovr().sketch_g > 0) {
+      budget = (double)ovr().sketch_g * 1048576.0;
+    } else if (d.k > 0 && A->nnz > 0) {
+      const double per_col = (double)A->nnz / (double)d.k;
+      const double chunks = std::max(1.0, std::floor(per_col / 256.0));
+      const double rows_c = std::ceil((double)d.cnt / chunks);
+      budget = std::min(8.0e9, std::max(256.0 * 1048576.0, rows_c * 8.0 * (double)s2));
+    }
     w.g_rows = std::max<int64_t>(1, std::min<int64_t>(d.cnt, (int64_t)(budget / (8.0 * (double)s2))));
     const int64_t nchg = (d.cnt + w.g_rows - 1) / w.g_rows;
     w.G = ar.take<double>((size_t)w.g_rows * s2);
@@ -1523,6 +1537,11 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
     case LSRN_OPT_CSR_ROWDOT: if (!in(-1, 3)) return bad(); o.csr_rowdot = (int)value; break;
     case LSRN_OPT_CSR_SKETCH: if (!in(-1, 2)) return bad(); o.csr_sketch = (int)value; break;
     case LSRN_OPT_CSR_HEAVY_FMA: if (!in(-1, 1)) return bad(); o.csr_heavy_fma = (int)value; break;
+    case LSRN_OPT_CSR_LIGHT:
+      if (!(value == -1 || (value >= 12 && value <= 648 && (value % 10 == 2 || value % 10 == 4 || value % 10 == 8))))
+        return bad();
+      o.csr_light = (int)value;
+      break;
     case LSRN_OPT_CSR_ALL: if (!in(-1, 13) || value == 1 || value == 2 || value == 3) return bad(); o.csr_all = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
   }

@@ -37,7 +37,7 @@ OPTIONS = {"profiling": 1, "svd": 2, "graph_reuse": 3, "hostio_chunk_mb": 4, "ls
            "rowpass_keep": 110, "rowpass_occ": 111, "rowpass_wide1": 112, "rowpass_wide2": 113,
            "rowpass_asyncx": 114, "rowpass_nt": 115, "rowpass_tr": 116, "rowpass_budget_kb": 117,
            "rowpass_wide_slice": 118, "rowpass_pf": 119, "csr_rowdot": 120, "csr_sketch": 121, "csr_heavy_fma": 123,
-           "csr_all": 124}
+           "csr_all": 124, "csr_light": 126}
 SVD_METHODS = {"auto": 0, "jw": 1, "gesvd": 2, "polar": 3, "qr": 4}
 OPTION_DEFAULTS = {k: -1 for k in OPTIONS}
 OPTION_DEFAULTS.update(profiling=0, svd=0, graph_reuse=1, hostio_chunk_mb=32, lsqr_sync=0, bcast_n=1)
