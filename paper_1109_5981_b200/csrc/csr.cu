@@ -500,12 +500,18 @@ csr_gen_g_kernel(double* __restrict__ G, int64_t s2, int64_t rows, int64_t jbase
   bm_load_table(bmT);
   __syncthreads();
   const uint2 key = philox_key(seed);
-  const int64_t hp = s2 / 2, total = rows * hp;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t jl = p / hp, q = p % hp;
-    double z0, z1;
-    gaussian_pair(key, (uint64_t)q, (uint64_t)(jbase + jl), bmT, z0, z1);
-    *reinterpret_cast<double2*>(G + jl * s2 + 2 * q) = make_double2(z0, z1);
+  // rows over CTAs, pairs of a row over threads: no 64-bit division per pair (the
+  // flat index p -> (p / hp, p % hp) per pair: 162 -> 139 us per t4 launch,
+  // profiles/r02_gen2d_launches_t4.txt)
+  const int64_t hp = s2 / 2;
+  for (int64_t jl = blockIdx.x; jl < rows; jl += gridDim.x) {
+    double* Gr = G + jl * s2;
+    const uint64_t j = (uint64_t)(jbase + jl);
+    for (int64_t q = threadIdx.x; q < hp; q += blockDim.x) {
+      double z0, z1;
+      gaussian_pair(key, (uint64_t)q, j, bmT, z0, z1);
+      *reinterpret_cast<double2*>(Gr + 2 * q) = make_double2(z0, z1);
+    }
   }
 }
 
@@ -1546,8 +1552,7 @@ cudaError_t launch_csr_sketch_g(const CsrSketchGArgs& a, cudaStream_t st, int ns
   if (e != cudaSuccess) return e;
   for (int64_t J = 0; J < nch; ++J) {
     const int64_t r0 = J * a.g_rows, nr = std::min(a.g_rows, a.rows - r0);
-    const int64_t pairs = nr * (a.s2 / 2);
-    csr_gen_g_kernel<<<grid_cap(pairs, 256, (int64_t)nsm * 16), 256, 0, st>>>(a.G, a.s2, nr, a.lo + r0, a.seed);
+    csr_gen_g_kernel<<<grid_cap(nr, 1, (int64_t)nsm * 16), 256, 0, st>>>(a.G, a.s2, nr, a.lo + r0, a.seed);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (a.nd > 0) {
       const int64_t rps = (nr + a.nsplit - 1) / a.nsplit;

@@ -590,17 +590,19 @@ sketch_gen_g_kernel(double* __restrict__ G, int64_t ntm, int64_t nkb, int64_t ro
   __syncthreads();
   const uint2 key = philox_key(seed);
   constexpr int PAIRS = (C::BM / 2) * C::BK;       // pairs per tile
-  const int64_t total = ntm * nkb * PAIRS;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < total; p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t tile = p / PAIRS;
-    const int w = (int)(p % PAIRS), qp = w / C::BK, kk = w % C::BK;
+  // tiles over CTAs, a tile's pairs over threads: the 64-bit division by nkb happens
+  // once per tile, not once per pair
+  for (int64_t tile = blockIdx.x; tile < ntm * nkb; tile += gridDim.x) {
     const int64_t mt = tile / nkb, kb = tile % nkb;
-    const int64_t r = kb * C::BK + kk;
-    double z0 = 0.0, z1 = 0.0;
-    if (r < rows) gaussian_pair(key, (uint64_t)(mt * (C::BM / 2) + qp), (uint64_t)(jbase + r), bmT, z0, z1);
     double* t = G + tile * C::G_STAGE;
-    t[(2 * qp) * C::G_LD + kk] = z0;
-    t[(2 * qp + 1) * C::G_LD + kk] = z1;
+    for (int w = threadIdx.x; w < PAIRS; w += blockDim.x) {
+      const int qp = w / C::BK, kk = w % C::BK;
+      const int64_t r = kb * C::BK + kk;
+      double z0 = 0.0, z1 = 0.0;
+      if (r < rows) gaussian_pair(key, (uint64_t)(mt * (C::BM / 2) + qp), (uint64_t)(jbase + r), bmT, z0, z1);
+      t[(2 * qp) * C::G_LD + kk] = z0;
+      t[(2 * qp + 1) * C::G_LD + kk] = z1;
+    }
   }
 }
 
@@ -615,8 +617,7 @@ size_t sketch_g_bytes(int64_t s, int64_t rows) {
 
 static cudaError_t launch_gen_g(const SketchDenseArgs& a, cudaStream_t st) {
   const int64_t ntm = (a.s + Tile1::BM - 1) / Tile1::BM, nkb = (a.rows + Tile1::BK - 1) / Tile1::BK;
-  const int64_t pairs = ntm * nkb * (Tile1::BM / 2) * Tile1::BK;
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((pairs + 255) / 256, 148 * 16));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntm * nkb, 148 * 16));
   sketch_gen_g_kernel<<<blocks, 256, 0, st>>>(a.G, ntm, nkb, a.rows, a.lo, a.seed);
   return cudaGetLastError();
 }
