@@ -383,7 +383,10 @@ def main():
     sketch_share = (sk_ms / 1e3) / (ms / 1e3)
     lp_share = (lp_ms / 1e3) * max(iters + 1, 1) / (ms / 1e3)
     if csr:
-        roof_sketch = {"kernel": "csr_sketch_heavy/light (K4, FP64 FMA + in-kernel RNG)", "bound": "alu",
+        roof_sketch = {"kernel": "csr_gen_g_kernel + csr_sketch_heavy_mma_kernel + csr_sketch_light_g_kernel (K4 "
+                                 "stored G per chunk; the light gathers are bound by L2-to-SM traffic, 8 B of G "
+                                 "per (nonzero, sketch row), not by FP64 issue: DESIGN.md §6 K4 round 2c)",
+                       "bound": "alu",
                        "achieved": sketch_tf, "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                        "frac": sketch_tf / DFMA_PEAK_TFLOPS, "traffic": None,
                        "algorithmic": f"2*s*nnz = {sketch_flops:.4g} flop per sketch (+ s*cnt normals, not counted)",
