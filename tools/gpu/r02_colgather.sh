@@ -1,4 +1,5 @@
 # c4 long pass: CSC-gather entries in flight (csr_colgather), parity tests, ncu of the two kernels
+# (the csr_colgather / csr_hl_minb options were an uncommitted experiment, removed after this measurement)
 mkdir -p gpurun_out/cg
 timeout 600 python -m pytest tests/test_gpu_csr.py -x -q -p no:cacheprovider -k "wide_k or c4" > gpurun_out/cg/tests.log 2>&1
 tail -1 gpurun_out/cg/tests.log

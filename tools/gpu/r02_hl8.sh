@@ -1,4 +1,5 @@
 # c4 long pass: row-pass occupancy (csr_hl_minb) x CSC gather depth
+# (the csr_colgather / csr_hl_minb options were an uncommitted experiment, removed after this measurement)
 mkdir -p gpurun_out/cg
 timeout 600 python -m pytest tests/test_gpu_csr.py -x -q -p no:cacheprovider -k "wide_k or c4" > gpurun_out/cg/tests2.log 2>&1
 tail -1 gpurun_out/cg/tests2.log
