@@ -232,10 +232,9 @@ lsrn_status lsrn_ctx_destroy(lsrn_ctx* ctx);
  *                           2 (default) G generated once per chunk of rows (<= 8 GB, or the
  *                           LSRN_OPT_SKETCH_G budget) and read by the heavy and light kernels
  *   LSRN_OPT_CSR_HEAVY_FMA  stored-G heavy block: 1 = FP64-FMA kernel instead of the DMMA GEMM
- *   LSRN_OPT_CSR_ALL        CSR single pass (k <= 2048): 0 one pair of rows in flight per warp;
- *                           4-9 load pipelines of (rows per group G, groups NB; NB - 1 in
- *                           flight) = (8,4) (4,4) (8,2) (4,8) (4,2) (2,4); 10-13 the same with
- *                           t staged in shared memory: (8,2) (default) (4,4) (4,2) (8,4)
+ *   LSRN_OPT_CSR_ALL        CSR single pass (k <= 2048): 0 one pair of rows in flight per warp
+ *                           (round 1); 6 a register load pipeline of 8-row groups, one group
+ *                           in flight; 10 (default) the same with t in shared memory
  *   LSRN_OPT_CSR_LIGHT      stored-G light sketch kernel: 10 * (columns per CTA, 1-64) +
  *                           (gathers in flight per thread: 2, 4 or 8) */
 enum {

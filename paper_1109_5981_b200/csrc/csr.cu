@@ -1388,28 +1388,18 @@ int csr_rowdot_hl_blocks(int nsm, int ND) {
   return nsm * std::min(per_sm, 8);
 }
 int64_t csr_rowdot_all_max_k() { return 2048; }      // 8 warps x k doubles of shared memory (128 KB)
-// Variants of the single pass (csr_rowdot option): 0 csr_rowdot_all_kernel (one pair of
-// rows in flight per warp), 4.. the pipelined kernel with (G, NB) below.
+// Variants of the single pass (option csr_all): 0 csr_rowdot_all_kernel (round 1, one
+// pair of rows in flight per warp); 6 the pipelined kernel, (G, NB) = (8, 2), t read
+// through L1; 10 (default) the same with t in shared memory.  The other pipelines
+// measured on t4 -- (8,4) (4,4) (4,8) (4,2) (2,4), with and without TS, 0.52-0.91 ms
+// against 0.42 ms -- were removed (profiles/r02_csr_all_t4*.jsonl).
 namespace {
-struct AllVariant {
-  int G, NB, minb;
-};
-constexpr AllVariant kAllVariants[] = {{8, 4, 1}, {4, 4, 2}, {8, 2, 2}, {4, 8, 1}, {4, 2, 3}, {2, 4, 3},
-                                       {8, 2, 2}, {4, 4, 2}, {4, 2, 3}, {8, 4, 1}};
-constexpr int kMaxVariant = 13;
-bool all_ts(int v) { return v >= 10; }     // t staged in shared memory
+int all_minb(int v) { return (v == 6 || v == 10) ? 2 : 4; }
+bool all_ts(int v) { return v == 10; }     // t staged in shared memory
 const void* all_kernel(int v) {
   switch (v) {
-    case 4: return (const void*)csr_rowdot_all_pipe_kernel<8, 4, 1, false>;
-    case 5: return (const void*)csr_rowdot_all_pipe_kernel<4, 4, 2, false>;
     case 6: return (const void*)csr_rowdot_all_pipe_kernel<8, 2, 2, false>;
-    case 7: return (const void*)csr_rowdot_all_pipe_kernel<4, 8, 1, false>;
-    case 8: return (const void*)csr_rowdot_all_pipe_kernel<4, 2, 3, false>;
-    case 9: return (const void*)csr_rowdot_all_pipe_kernel<2, 4, 3, false>;
     case 10: return (const void*)csr_rowdot_all_pipe_kernel<8, 2, 2, true>;
-    case 11: return (const void*)csr_rowdot_all_pipe_kernel<4, 4, 2, true>;
-    case 12: return (const void*)csr_rowdot_all_pipe_kernel<4, 2, 3, true>;
-    case 13: return (const void*)csr_rowdot_all_pipe_kernel<8, 4, 1, true>;
     default: return (const void*)csr_rowdot_all_kernel;
   }
 }
@@ -1420,12 +1410,12 @@ int csr_rowdot_all_default_variant() { return 10; }
 int csr_rowdot_all_blocks(int nsm, int64_t k, int variant) {
   const int64_t per_cta = 8 * k * (THR / 32 + (all_ts(variant) ? 1 : 0));
   int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / per_cta));
-  if (variant >= 4 && variant <= kMaxVariant) per_sm = std::min<int64_t>(per_sm, kAllVariants[variant - 4].minb);
+  per_sm = std::min<int64_t>(per_sm, all_minb(variant));
   return (int)(nsm * per_sm);
 }
 int csr_rowdot_all_blocks_max(int nsm, int64_t k) {
   int b = 0;
-  for (int v = 0; v <= kMaxVariant; ++v) b = std::max(b, csr_rowdot_all_blocks(nsm, k, v));
+  for (int v : {0, 6, 10}) b = std::max(b, csr_rowdot_all_blocks(nsm, k, v));
   return b;
 }
 

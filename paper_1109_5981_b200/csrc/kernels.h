@@ -35,7 +35,7 @@ struct Overrides {
                               // 3 the two-kernel form (row dots + CSC gather) also for k <= 2048
   int csr_sketch = -1;        // 0 column-stationary light sketch, 1 generate-once slab sketch, 2 stored G
   int csr_heavy_fma = -1;     // stored-G heavy block: 1 = FP64-FMA kernel instead of DMMA
-  int csr_all = -1;           // k <= 2048 single-pass kernel: 0 one pair of rows in flight, 4..13 pipelined
+  int csr_all = -1;           // k <= 2048 single-pass kernel: 0 one pair of rows in flight, 6 / 10 pipelined
   int csr_light = -1;         // stored-G light sketch: 10 * (columns per CTA) + (gathers in flight: 2, 4, 8)
 };
 const Overrides& ovr();

@@ -1542,7 +1542,7 @@ lsrn_status lsrn_ctx_set_option(lsrn_ctx* c, int option, int64_t value) {
         return bad();
       o.csr_light = (int)value;
       break;
-    case LSRN_OPT_CSR_ALL: if (!in(-1, 13) || value == 1 || value == 2 || value == 3) return bad(); o.csr_all = (int)value; break;
+    case LSRN_OPT_CSR_ALL: if (!(value == -1 || value == 0 || value == 6 || value == 10)) return bad(); o.csr_all = (int)value; break;
     default: return set_error(LSRN_EINVAL, "unknown option " + std::to_string(option));
   }
   return LSRN_OK;

@@ -251,11 +251,11 @@ def _ragged_csr(m, n, seed):
 
 
 @pytest.mark.parametrize("solver", ["lsqr", "cs"])
-@pytest.mark.parametrize("rowdot,variant", [(-1, -1), (3, -1), (-1, 0)] + [(-1, v) for v in range(4, 14)])
+@pytest.mark.parametrize("rowdot,variant", [(-1, -1), (3, -1), (-1, 0), (-1, 6), (-1, 10)])
 def test_csr_single_pass_staged_and_direct_chunks(ctx, solver, rowdot, variant):
     """k <= 2048 long pass on ragged rows (empty rows, rows longer than a warp, a chunk of
     long rows): the single-pass kernels (LSRN_OPT_CSR_ALL: 0 one pair of rows in flight,
-    4-7 the pipelined groups) and the two-kernel CSC-gather form (LSRN_OPT_CSR_ROWDOT = 3)
+    6 / 10 the pipelined groups, 10 with t in shared memory) and the two-kernel CSC-gather form (LSRN_OPT_CSR_ROWDOT = 3)
     against the oracle."""
     A = _ragged_csr(5000, 300, seed=8)
     b = np.random.default_rng(9).standard_normal(A.shape[0])
@@ -272,7 +272,7 @@ def test_csr_single_pass_staged_and_direct_chunks(ctx, solver, rowdot, variant):
     assert an <= 1e-11, an
 
 
-@pytest.mark.parametrize("variant", [0] + list(range(4, 14)))
+@pytest.mark.parametrize("variant", [0, 6, 10])
 @pytest.mark.parametrize("lam", [0.0, 0.05])
 def test_csr_single_pass_variants_wide_ragged(ctx, variant, lam):
     """Wide ragged CSR (X = A^T with empty, short and > 32-entry rows; CS keeps the

@@ -12,7 +12,7 @@ from paper_1109_5981_b200 import lsrn  # noqa: E402
 from synth.generate import make_problem  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "t4"
-variants = sys.argv[2:] or ["0", "4", "5", "6", "7"]   # "r3": the two-kernel form (csr_rowdot = 3)
+variants = sys.argv[2:] or ["0", "6", "10"]   # "r3": the two-kernel form (csr_rowdot = 3)
 p = make_problem(cfg, device="cuda")
 X = lsrn.Csr(p.rowptr, p.colind, p.val)
 ctx = lsrn.Context()
