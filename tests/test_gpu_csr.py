@@ -288,3 +288,18 @@ def test_csr_single_pass_variants_wide_ragged(ctx, variant, lam):
     assert rep["iters"] == orc["iters"] and rep["r"] == orc["r"]
     rel = np.linalg.norm(x.cpu().numpy() - orc["x"]) / np.linalg.norm(orc["x"])
     assert rel <= 1e-9, rel
+
+
+@pytest.mark.parametrize("light", [-1, 14, 48, 162, 22])
+@pytest.mark.parametrize("m,n,dense_cols,gamma", [(3000, 150, 7, 2.0), (2500, 61, 0, 2.01), (1800, 300, 3, 1.5)])
+def test_csr_light_kernel_variants_vs_oracle(ctx, light, m, n, dense_cols, gamma):
+    """Stored-G light kernel (LSRN_OPT_CSR_LIGHT = 10 columns per CTA + gathers in flight),
+    with several G chunks (1 MB budget), an odd s and a partial last sketch-row block:
+    relative Frobenius <= 1e-12 against the oracle's sketch."""
+    A = _random_csr(m, n, 5, dense_cols, 4.0, 3, seed=51)
+    with ctx.options(csr_light=light, sketch_g=1):
+        At = ctx.sketch(_gpu_csr(A), m, n, gamma).cpu().numpy()
+    p = orc_plan(m, n, gamma, 0.0)
+    assert At.shape[0] == p["s"]
+    ref = orc_sketch(A, p["s"], 5981, p["sigma_x"], p["sigma_i"])
+    assert _relfro(At, ref) <= 1e-12
