@@ -1,4 +1,5 @@
 # light kernel with two sketch rows per thread: parity tests + t4 / c4 sketch times
+# (the 10xx csr_light values were an uncommitted experiment, removed after this measurement)
 mkdir -p gpurun_out/vi
 timeout 900 python -m pytest tests/test_gpu_csr.py -x -q -p no:cacheprovider -k "light_kernel or sketch_vs_oracle or full" > gpurun_out/vi/tests.log 2>&1
 tail -1 gpurun_out/vi/tests.log
