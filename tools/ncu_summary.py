@@ -4,6 +4,7 @@
   python tools/ncu_summary.py launches <launches.csv>      # per-kernel counts, device time, share
   python tools/ncu_summary.py full <prof.ncu-rep> [...]     # key metrics of a --set full capture
   python tools/ncu_summary.py traffic <workload> <sketch.ncu-rep> <longpass.ncu-rep>   # -> profiles/traffic.json
+  python tools/ncu_summary.py dram <launches.csv>          # per-kernel DRAM bytes of a launch list
 """
 import collections
 import csv
@@ -47,6 +48,33 @@ def launches(path):
         out.append({"kernel": nm, "ours": a["ours"], "launches": a["count"], "total_us": round(a["us"], 1),
                     "avg_us": round(a["us"] / a["count"], 2), "share_of_all": round(a["us"] / total, 4)})
     return {"total_us": round(total, 1), "ours_us": round(ours_total, 1), "kernels": out}
+
+
+def dram(path):
+    """Per kernel of a launch list with dram__bytes_read.sum / dram__bytes_write.sum: launches,
+    total and average DRAM bytes (read + write) and device time."""
+    rows = list(csv.reader(open(path)))
+    i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]
+    h = rows[i]
+    kn, mv, mn, idc = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name"), h.index("ID")
+    per = collections.OrderedDict()
+    for r in rows[i + 1:]:
+        if len(r) <= mv:
+            continue
+        d = per.setdefault(r[idc], {"name": short(r[kn])})
+        unit = r[h.index("Metric Unit")] if "Metric Unit" in h else ""
+        v = float(r[mv].replace(",", ""))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1, "usecond": 1e3,
+                 "msecond": 1e6}.get(unit, 1)
+        d[r[mn]] = v * scale
+    agg = collections.OrderedDict()
+    for d in per.values():
+        a = agg.setdefault(d["name"], {"launches": 0, "dram_bytes": 0.0, "ns": 0.0})
+        a["launches"] += 1
+        a["dram_bytes"] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+        a["ns"] += d.get("gpu__time_duration.sum", 0.0)
+    return {nm: {"launches": a["launches"], "dram_bytes": a["dram_bytes"], "avg_dram_bytes": a["dram_bytes"] / a["launches"],
+                 "total_us": a["ns"] / 1e3} for nm, a in agg.items()}
 
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -101,5 +129,7 @@ if __name__ == "__main__":
         print(json.dumps(launches(sys.argv[2]), indent=1))
     elif mode == "traffic":
         print(json.dumps(traffic(sys.argv[2], sys.argv[3], sys.argv[4]), indent=1))
+    elif mode == "dram":
+        print(json.dumps(dram(sys.argv[2]), indent=1))
     else:
         print(json.dumps([full(p) for p in sys.argv[2:]], indent=1))
