@@ -1201,14 +1201,13 @@ csr_rowdot_all_pipe_kernel(const int64_t* __restrict__ rowptr, const int32_t* __
   const int64_t r0 = min(rows, warp * per), r1 = min(rows, r0 + per);
   const int64_t nchunks = (r1 - r0 + CHUNK - 1) / CHUNK;
 
-  // chunk descriptor: cb = the chunk's first entry (relative to the shard), lane l <
-  // CHUNK holds rp = row pointer of row l of the chunk minus cb (clamped to the chunk
-  // end; a chunk has at most 32 k entries since the columns of a row are distinct),
-  // lane CHUNK (or 0 when CHUNK = 32: end) the end; lng = some row > 32 entries
+  // chunk descriptor: cb = the chunk's first entry (relative to the shard); lane l holds
+  // rp = the row pointer of row min(l, nr) of the chunk minus cb (a chunk has at most
+  // CHUNK k entries since the columns of a row are distinct), end = the pointer past the
+  // chunk's last row; uo / ao = old u / acc of row l
   struct Chunk {
     int64_t cb;
     int rp, end;
-    bool lng;
     double uo, ao;
   };
   auto load_chunk = [&](int64_t ci, Chunk& C) {
@@ -1217,7 +1216,6 @@ csr_rowdot_all_pipe_kernel(const int64_t* __restrict__ rowptr, const int32_t* __
     C.end = 0;
     C.uo = 0.0;
     C.ao = 0.0;
-    C.lng = false;
     if (ci < nchunks) {
       const int64_t rc = r0 + ci * CHUNK;
       const int nr = (int)min((int64_t)CHUNK, r1 - rc);
